@@ -1,0 +1,146 @@
+"""Constitutive models and return maps, fp64, batched over a leading axis.
+
+Each function follows PAPER.md's appendix "Elasticity and plasticity details"
+(lines 502-545) in its own notation; corrections of garbled passages are the
+SURVEY.md §8(c) readings, recorded in DESIGN.md:
+  #2  fixed-corotated volumetric term is lambda (J-1) J * I
+  #3  Hencky ("StVK", line 524) is tau = U diag(2 mu eps + lambda sum(eps)) U^T
+  #4  von Mises projection divides by ||eps_hat|| (line 542 prints ||eps||)
+  #5  Drucker-Prager and von Mises use Hencky elasticity
+  #6  d = 3 in the Drucker-Prager delta-gamma
+  #21 rotation-safe SVD (det U = det V = +1, sign folded into sigma_3);
+      log-strain models clamp sigma >= 1e-4 before the log.
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+"""
+import numpy as np
+
+SIGMA_FLOOR = 1e-4   # reading #21
+
+
+def lame(E, nu):
+    """mu_hat = E/(2(1+nu)), lambda = E nu/((1+nu)(1-2nu)),
+    kappa = E/(3(1-2nu))."""
+    E = float(E)
+    nu = float(nu)
+    if not (E > 0.0 and 0.0 <= nu < 0.5):
+        raise ValueError("parameter domain: E > 0, 0 <= nu < 0.5")
+    mu = E / (2.0 * (1.0 + nu))
+    lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    kappa = E / (3.0 * (1.0 - 2.0 * nu))
+    return mu, lam, kappa
+
+
+def dp_alpha(friction_angle_deg):
+    """alpha = sqrt(2/3) * 2 sin(phi_f) / (3 - sin(phi_f))."""
+    s = np.sin(np.deg2rad(float(friction_angle_deg)))
+    return np.sqrt(2.0 / 3.0) * 2.0 * s / (3.0 - s)
+
+
+def svd_rotation_safe(F):
+    """F = U diag(sigma) V^T with det U = det V = +1 (reading #21).
+
+    A library primitive (LAPACK via numpy) is the step; the sign fix folds any
+    reflection of U or V into sigma_3 (the smallest singular value), so sigma_3
+    may be negative when det F < 0.
+    """
+    F = np.asarray(F, dtype=np.float64)
+    U, s, Vh = np.linalg.svd(F)
+    V = np.swapaxes(Vh, -1, -2).copy()
+    U = U.copy()
+    s = s.copy()
+    du = np.linalg.det(U) < 0
+    U[du, :, 2] *= -1.0
+    s[du, 2] *= -1.0
+    dv = np.linalg.det(V) < 0
+    V[dv, :, 2] *= -1.0
+    s[dv, 2] *= -1.0
+    return U, s, V
+
+
+def _diag_sandwich(A, d, B):
+    """A diag(d) B^T for batched 3x3 A, B and (n,3) d."""
+    return np.einsum("nij,nj,nkj->nik", A, d, B)
+
+
+def tau_fixed_corotated(F, mu, lam):
+    """PAPER.md line 518 (+ reading #2): tau = 2 mu (F - R) F^T + lambda (J-1) J I,
+    R = U V^T from the SVD of F (line 520)."""
+    F = np.asarray(F, dtype=np.float64)
+    U, s, V = svd_rotation_safe(F)
+    R = U @ np.swapaxes(V, -1, -2)
+    J = s[:, 0] * s[:, 1] * s[:, 2]
+    tau = 2.0 * mu * (F - R) @ np.swapaxes(F, -1, -2)
+    tau += (lam * (J - 1.0) * J)[:, None, None] * np.eye(3)
+    return tau
+
+
+def tau_hencky(U, sigma, mu, lam):
+    """PAPER.md line 524 with reading #3: tau = U diag(2 mu eps + lambda sum(eps) 1) U^T,
+    eps = log(Sigma) (Sigma clamped at 1e-4, reading #21)."""
+    eps = np.log(np.maximum(sigma, SIGMA_FLOOR))
+    d = 2.0 * mu * eps + lam * eps.sum(axis=1, keepdims=True)
+    return _diag_sandwich(U, d, U)
+
+
+def return_map_drucker_prager(sigma, mu, lam, alpha):
+    """PAPER.md lines 528-536 (Klar et al. 2016): returns Z(Sigma).
+
+      Z = 1                               if sum(eps) > 0
+      Z = Sigma                           if delta_gamma <= 0 and sum(eps) <= 0
+      Z = exp(eps - dg * eps_hat/|eps_hat|) otherwise
+      delta_gamma = |eps_hat| + alpha (d lambda + 2 mu) sum(eps) / (2 mu), d = 3.
+    """
+    s = np.maximum(np.asarray(sigma, dtype=np.float64), SIGMA_FLOOR)
+    eps = np.log(s)
+    tr = eps.sum(axis=1)
+    eps_hat = eps - tr[:, None] / 3.0
+    nrm = np.linalg.norm(eps_hat, axis=1)
+    dg = nrm + alpha * (3.0 * lam + 2.0 * mu) * tr / (2.0 * mu)
+    Z = s.copy()
+    expand = tr > 0.0
+    proj = (~expand) & (dg > 0.0)
+    Z[expand] = 1.0
+    if np.any(proj):
+        Z[proj] = np.exp(eps[proj] - (dg[proj] / nrm[proj])[:, None] * eps_hat[proj])
+    return Z
+
+
+def return_map_von_mises(sigma, mu, tau_Y):
+    """PAPER.md lines 538-545 with reading #4: returns Z(Sigma).
+
+      delta_gamma = |eps_hat|_F - tau_Y/(2 mu)
+      Z = Sigma                            if delta_gamma <= 0
+      Z = exp(eps - dg * eps_hat/|eps_hat|) otherwise
+    (With Hencky elasticity, |tau - sum(tau)/3| <= tau_Y is exactly dg <= 0.)
+    """
+    s = np.maximum(np.asarray(sigma, dtype=np.float64), SIGMA_FLOOR)
+    eps = np.log(s)
+    tr = eps.sum(axis=1)
+    eps_hat = eps - tr[:, None] / 3.0
+    nrm = np.linalg.norm(eps_hat, axis=1)
+    dg = nrm - tau_Y / (2.0 * mu)
+    Z = s.copy()
+    proj = dg > 0.0
+    if np.any(proj):
+        Z[proj] = np.exp(eps[proj] - (dg[proj] / nrm[proj])[:, None] * eps_hat[proj])
+    return Z
+
+
+def elastoplastic_update(F_trial, model, mu, lam, alpha=0.0, tau_Y=0.0):
+    """F^E = returnMap(F_trial), tau = tau(F^E).
+
+    model 0 fixed-corotated (F^E = F_trial), 1 Drucker-Prager, 2 von Mises.
+    Returns (F_E, tau).
+    """
+    F_trial = np.asarray(F_trial, dtype=np.float64)
+    if model == 0:
+        return F_trial.copy(), tau_fixed_corotated(F_trial, mu, lam)
+    U, s, V = svd_rotation_safe(F_trial)
+    if model == 1:
+        Z = return_map_drucker_prager(s, mu, lam, alpha)
+    elif model == 2:
+        Z = return_map_von_mises(s, mu, tau_Y)
+    else:
+        raise ValueError("model")
+    F_E = _diag_sandwich(U, Z, V)
+    return F_E, tau_hencky(U, Z, mu, lam)
