@@ -1,0 +1,232 @@
+/*
+ * nsf_mpm.h -- C ABI of the B200 (sm_100a) MLS-MPM substep library for
+ * arXiv 2310.17790 "Neural Stress Fields for Reduced-order Elastoplasticity
+ * and Fracture".  This header is the boundary: every entry point below is
+ * implemented by CUDA kernels in paper_2310_17790_b200/csrc/ and nothing else.
+ * No torch types cross it; pointers are plain host or device pointers.
+ *
+ * Citations are PAPER.md line numbers ("P:L") and SURVEY.md §8(c) readings
+ * ("#k"); DESIGN.md lists every reading.
+ *
+ * What the library computes (one substep, §3.3):
+ *   P2G   m_i = sum_p w_ip m_p ; m_i v_i = sum_p w_ip m_p (v_p + C_p (x_i - x_p))
+ *         with the stress force of Eq. (6) folded into the momentum:
+ *           MLS   (default, #1): - dt V0 (4/dx^2) w_ip tau_p (x_i - x_p)
+ *           GRADW (literal Eq.(6)): - dt V0 tau_p grad(w_ip)
+ *   grid  v_i = (m_i v_i)/m_i + dt g if m_i > 0, else 0 (#15); then the
+ *         wall BCs (#11, #12) and the moving plate (#12).
+ *   G2P   v_p = sum w v_i ; C_p = 4/dx^2 sum w v_i (x_i - x_p)^T ;
+ *         x_p += dt v_p ; F_trial = (I + dt G) F_E ;
+ *         F_E = returnMap(F_trial), tau = tau(F_E) (appendix).
+ *   Reduced variant: tau_p = h(X_p, z_s(n)) from the neural stress
+ *   field MLP (architecture P:498-500); no F, no SVD.
+ *
+ * Conventions
+ *   Layouts   caller arrays are row-major AoS, float32: x, v as n x 3; C, F as
+ *             n x 3 x 3 with C[p][a][b]; tau as n x 6 in Voigt order
+ *             (xx, yy, zz, yz, xz, xy).  Grid node i = (i0,i1,i2) sits at i*dx
+ *             (#8, #10); grid_res is nodes per axis and must be a multiple of 4.
+ *   Ownership the handle owns all device memory (allocated through the optional
+ *             allocator hook, else cudaMalloc).  The caller owns every buffer it
+ *             passes; the library never keeps a caller pointer after a call.
+ *   on_device 1: pointers are device pointers, valid and stream-ordered on the
+ *             handle's stream; 0: host pointers (pinned or pageable).
+ *   Synchrony nsf_mpm_substep only enqueues work and returns.  load_*,
+ *             set_latents, eval_stress_field, read_state and the debug calls
+ *             complete their own work (stream-ordered after earlier substeps)
+ *             before returning.  nsf_mpm_sync blocks.
+ *   Errors    every call returns nsf_status (0 = OK).  Argument checks happen at
+ *             call time (NSF_ERR_INVALID_ARGUMENT).  Particles outside the safe
+ *             region x/dx in [0.5, N - 1.5) are rejected at load with
+ *             NSF_ERR_OUT_OF_DOMAIN (first index in last_error).  During
+ *             substeps, out-of-domain and non-finite values set bits in a device
+ *             error word (kernels clamp indices so memory stays in bounds); the
+ *             next sync / read_state reports them.  A CUDA error poisons the
+ *             handle: every later call returns NSF_ERR_CUDA.  Inverted F
+ *             (det <= 0) is not an error (#21); it is counted.
+ *   Threads   a handle is single-owner and not thread-safe; distinct handles are
+ *             independent.
+ */
+#ifndef NSF_MPM_H
+#define NSF_MPM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSF_MPM_ABI_VERSION 1
+
+typedef struct nsf_mpm nsf_mpm; /* opaque; owns all device state */
+
+typedef enum {
+  NSF_OK = 0,
+  NSF_ERR_INVALID_ARGUMENT = 1,
+  NSF_ERR_OUT_OF_DOMAIN = 2,
+  NSF_ERR_NONFINITE = 3,
+  NSF_ERR_CUDA = 4,
+  NSF_ERR_OUT_OF_MEMORY = 5,
+  NSF_ERR_BAD_STATE = 6
+} nsf_status;
+
+/* Constitutive model (PAPER.md appendix).  DP and VM use Hencky
+ * (log-strain) elasticity (#5), with tau = U diag(2 mu eps + lambda sum eps) U^T
+ * (#3).  NSF = reduced variant, stress from the neural stress field. */
+typedef enum {
+  NSF_FIXED_COROTATED = 0, /* tau = 2 mu (F - R) F^T + lambda (J-1) J I   (#2) */
+  NSF_DRUCKER_PRAGER = 1,  /* sand return map */
+  NSF_VON_MISES = 2,       /* perfect plasticity, radial return          (#4) */
+  NSF_NEURAL_STRESS = 3    /* tau = sigma_tau h(X, z) */
+} nsf_model;
+
+/* Wall boundary condition on the nodes within bc_width of a face (#11, #12). */
+typedef enum {
+  NSF_BC_NONE = 0,
+  NSF_BC_STICKY = 1, /* v_i = 0 */
+  NSF_BC_SLIP = 2    /* zero the normal component if it points into the wall */
+} nsf_bc;
+
+typedef enum {
+  NSF_FORCE_MLS = 0,  /* grad w -> (4/dx^2) w (x_i - x_p), F_trial = (I + dt C) F (#1) */
+  NSF_FORCE_GRADW = 1 /* Eq. (6) and P:179 literally                                 */
+} nsf_force_mode;
+
+typedef struct {
+  int32_t model;                /* nsf_model                                        */
+  double E, nu, rho;            /* Pa, -, kg/m^3; E > 0, 0 <= nu < 0.5   */
+  double friction_angle_deg;    /* DP phi_f in (0, 90)    */
+  double yield_stress;          /* VM tau_Y >= 0 (Pa)    */
+  double gravity[3];            /* m/s^2, y is up                          (#13)     */
+  int32_t bc[6];                /* nsf_bc for faces -x,+x,-y,+y,-z,+z               */
+  int32_t bc_width;             /* nodes (3 in every config)               (#11)     */
+  int32_t plate_enabled;        /* moving rigid plate: nodes with y_i >= y_p(t_n)   */
+  double plate_y0;              /*   y_p(t_n) = plate_y0 + plate_velocity[1] n dt   */
+  double plate_velocity[3];     /*   get v_i = plate_velocity, after the walls (#12)*/
+  int32_t force_mode;           /* nsf_force_mode                                   */
+  int32_t deterministic;        /* reserved (1 = atomic-free ordered P2G); must be 0 */
+  int32_t n_scenes;             /* >= 1; each scene owns a grid_res^3 grid          */
+  double particle_volume;       /* V_p^0 (m^3); <= 0 -> dx^3/8 (8 ppc, #16); m = rho V0 */
+  double stress_scale;          /* sigma_tau (Pa) multiplying the NSF output (#20)   */
+} nsf_material;
+
+/* read_state field mask; dst[k] is the k-th requested field in bit order. */
+#define NSF_FIELD_X 1u   /* n x 3                                   */
+#define NSF_FIELD_V 2u   /* n x 3                                   */
+#define NSF_FIELD_C 4u   /* n x 3 x 3                               */
+#define NSF_FIELD_F 8u   /* n x 3 x 3 (elastic F_E; not for NSF)     */
+#define NSF_FIELD_TAU 16u /* n x 6 Voigt (stress used by the NEXT P2G) */
+
+/* Version of this header's ABI (NSF_MPM_ABI_VERSION). */
+int32_t nsf_mpm_abi_version(void);
+
+/* Create a simulator on the current CUDA device.  grid_res: nodes per axis
+ * (each a multiple of 4, >= 2*bc_width + 3).  dx, dt > 0 (s, m).  dx should be
+ * an exact power of two so B-spline bases are exact in fp32 (#10).  Returns
+ * NSF_ERR_INVALID_ARGUMENT on a bad parameter (see nsf_material comments). */
+nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt,
+                          const nsf_material* material, nsf_mpm** out);
+
+/* Stream for all later work (cudaStream_t; NULL = the non-blocking stream the handle
+ * created for itself, which is also the default).  Cached CUDA graphs are dropped when the stream changes. */
+nsf_status nsf_mpm_set_stream(nsf_mpm* h, void* cuda_stream);
+
+/* Optional device allocator (e.g. torch's caching allocator), used for every
+ * allocation made after this call.  alloc returns NULL on failure. */
+nsf_status nsf_mpm_set_allocator(nsf_mpm* h,
+                                 void* (*alloc)(size_t bytes, void* stream, void* ctx),
+                                 void (*release)(void* ptr, void* stream, void* ctx),
+                                 void* ctx);
+
+/* Load n particles (replaces any previous state, resets the step counter).
+ * x, v: n x 3; C, F: n x 3 x 3 (NULL -> 0 / I).  tau^0 = tau(F^0) (#9).
+ * scene_offsets: n_scenes + 1 monotone int64 with [0] = 0, [n_scenes] = n
+ * (particles of scene s are [off[s], off[s+1])); NULL allowed if n_scenes = 1.
+ * n = 0 is allowed (substeps are then no-ops).  Rejects out-of-domain
+ * particles with NSF_ERR_OUT_OF_DOMAIN. */
+nsf_status nsf_mpm_load_particles(nsf_mpm* h, int64_t n, const float* x, const float* v,
+                                  const float* C, const float* F,
+                                  const int64_t* scene_offsets, int32_t on_device);
+
+/* Neural stress field h: in_dim = 3 + r inputs (X, z),
+ * n_hidden hidden layers of `width` with ELU, out_dim = 6 (Voigt).  W_bf16:
+ * bf16 bit patterns, layer-major, each layer row-major [out][in]; b: float32
+ * biases, layer-major.  X_ref: n x 3 reference positions of the loaded
+ * particles (same order as load_particles), or NULL to keep the previous ones.
+ * Numerics (#20): layer-1 input fp32, hidden activations rounded to bf16 before
+ * layers 2..L+1, fp32 accumulation, bias and ELU in fp32.
+ * Supported: width = 128, 1 <= n_hidden <= 8, in_dim <= 16, out_dim = 6. */
+nsf_status nsf_mpm_load_stress_field(nsf_mpm* h, int32_t in_dim, int32_t width,
+                                     int32_t n_hidden, int32_t out_dim,
+                                     const uint16_t* W_bf16, const float* b,
+                                     const float* X_ref, int32_t on_device);
+
+/* Latents: z is n_scenes x r; dz (n_scenes x r or NULL = 0) is the per-substep
+ * drift, z_s(n) = z_s + n dz_s with n the handle's step counter (#26). */
+nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const float* dz,
+                               int32_t on_device);
+
+/* Enqueue n >= 0 substeps on the handle's stream (a cached CUDA graph of the
+ * substep is replayed).  Asynchronous.  NSF_ERR_BAD_STATE before
+ * load_particles, or for NSF without load_stress_field / set_latents. */
+nsf_status nsf_mpm_substep(nsf_mpm* h, int32_t n);
+
+/* Evaluate tau = sigma_tau h(X, z) at m points (m x 3) for one latent z (r
+ * floats) into tau_out (m x 6 Voigt).  Synchronous. */
+nsf_status nsf_mpm_eval_stress_field(nsf_mpm* h, const float* z, int64_t m,
+                                     const float* points, float* tau_out, int32_t on_device);
+
+/* Copy the requested fields (mask of NSF_FIELD_*) of all particles, in the order
+ * they were loaded, into dst[0..popcount(mask)-1].  Synchronous; reports
+ * deferred device errors first. */
+nsf_status nsf_mpm_read_state(nsf_mpm* h, uint32_t field_mask, float* const* dst,
+                              int32_t on_device);
+
+/* Block until all enqueued work is done; report deferred device errors
+ * (NSF_ERR_OUT_OF_DOMAIN / NSF_ERR_NONFINITE with the particle index and
+ * substep in last_error). */
+nsf_status nsf_mpm_sync(nsf_mpm* h);
+
+/* Substeps enqueued since the last load (host counter). */
+int64_t nsf_mpm_step_count(const nsf_mpm* h);
+
+/* Number of particle updates that produced det F_E <= 0 since load (#21). */
+int64_t nsf_mpm_inverted_count(nsf_mpm* h);
+
+/* Human-readable description of the last error; valid until the next call. */
+const char* nsf_mpm_last_error(const nsf_mpm* h);
+
+/* Free everything (NULL-safe). */
+void nsf_mpm_destroy(nsf_mpm* h);
+
+/* ---- diagnostics (tests and bench; not on the hot path) -------------------- */
+
+/* Binning of the current state: counts[b] = number of
+ * particles whose base cell floor(x/dx - 1/2) lies in 4x4x4-cell block b
+ * (b = (b0*NB1 + b1)*NB2 + b2 per scene, scenes concatenated, NB = grid_res/4),
+ * and perm = a permutation of 0..n-1 (load order) grouping particles by block in
+ * ascending block order.  counts has n_scenes*NB0*NB1*NB2 entries.  Either
+ * output may be NULL.  Synchronous. */
+nsf_status nsf_mpm_debug_bins(nsf_mpm* h, int32_t* counts, int32_t* perm, int32_t on_device);
+
+/* Run P2G (stage 0) or P2G + grid update (stage 1) on the current state without
+ * advancing it, and copy the dense grid, n_scenes x N0 x N1 x N2 x 4 floats in
+ * natural node order: stage 0 (m_i, m_i v_i), stage 1 (v_i, m_i).  Synchronous. */
+nsf_status nsf_mpm_debug_grid(nsf_mpm* h, int32_t stage, float* out, int32_t on_device);
+
+/* Per-kernel timing with CUDA events on the handle's stream.  While enabled,
+ * substeps are launched without a graph and every kernel launch is bracketed
+ * by events.  nsf_mpm_kernel_times fills up to max entries (name, total ms,
+ * launches) and returns the number of kernel kinds. */
+nsf_status nsf_mpm_set_profiling(nsf_mpm* h, int32_t enable);
+int32_t nsf_mpm_kernel_times(nsf_mpm* h, const char** names, double* total_ms,
+                             int64_t* launches, int32_t max);
+
+/* Number of kernel launches per substep for the current configuration. */
+int32_t nsf_mpm_launches_per_substep(nsf_mpm* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSF_MPM_H */

@@ -1,0 +1,39 @@
+// Host-side launchers for the device kernels (internal; not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "params.cuh"
+
+namespace nsf {
+
+// kernels_basic.cu
+void launch_unpack(cudaStream_t st, int64_t n, const float* x, const float* v, const float* C,
+                   const float* F, float* S, int64_t pitch, int32_t* ids, const DevParams& P,
+                   DevErr* err, int with_F);
+void launch_pack(cudaStream_t st, int64_t n, const float* S, int64_t pitch, const int32_t* ids,
+                 int plane0, int ncomp, float* out);
+void launch_p2g_direct(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
+                       const int64_t* scene_off, int n_scenes, float4* acc, const DevParams& P);
+void launch_grid_update_dense(cudaStream_t st, int64_t total_nodes, float4* acc, float4* vel,
+                              const DevParams& P, const int64_t* d_step);
+void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, const int64_t* scene_off,
+                       int n_scenes, const float4* vel, const DevParams& P, DevErr* err, int64_t* d_step,
+                       int with_F);
+void launch_grid_debug(cudaStream_t st, int stage, int64_t total_nodes, const float4* acc, float4* vel,
+                       float* out, const DevParams& P, const int64_t* d_step);
+
+// kernels_nsf.cu -- neural stress field MLP
+struct MlpDev {
+  const uint16_t* W;    // bf16 bits, layer-major [out][in]
+  const float* b;       // fp32 biases, layer-major
+  int in_dim, width, n_hidden, out_dim;
+  int64_t w_off[10];    // element offsets of each layer's weights
+  int64_t b_off[10];
+};
+// tau (SoA planes PT.. of S, or AoS m x 6 if aos_out) = stress_scale * h(X, z_scene(p) + step*dz)
+void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X /*3 planes, pitch*/, int64_t xpitch,
+                    const int64_t* scene_off, int n_scenes, const float* z, const float* dz, int r,
+                    const int64_t* d_step, const MlpDev& mlp, float stress_scale, float* tau_out,
+                    int64_t tau_pitch, int aos_out);
+
+}  // namespace nsf

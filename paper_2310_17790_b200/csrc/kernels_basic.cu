@@ -1,0 +1,383 @@
+// Particle-parallel kernels: load/unpack, read-back/pack, direct-atomic P2G,
+// dense grid update, per-particle G2P.  These are the first correct path and
+// remain the sparse path (reduced variant, one point per ~8 cells) of the
+// library; the dense path is in kernels_tiled.cu.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "kernels.h"
+#include "mpm_math.cuh"
+
+namespace nsf {
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void flag_error(DevErr* err, uint32_t bit, int idx) {
+  atomicOr(&err->bits, bit);
+  atomicMin(&err->first_index, idx);
+}
+
+__device__ __forceinline__ bool in_safe_region(float t, int N) {
+  return t >= 0.5f && t < (float)N - 1.5f;
+}
+
+// clamp a base index so that base..base+2 stays inside [0, N)
+__device__ __forceinline__ int clamp_base(int b, int N) { return min(max(b, 0), N - 3); }
+
+// ---------------------------------------------------------------------------
+// unpack AoS caller arrays into SoA planes; ids = load order; tau^0 = tau(F^0)
+__global__ void k_unpack(int64_t n, const float* __restrict__ x, const float* __restrict__ v,
+                         const float* __restrict__ C, const float* __restrict__ F, float* S,
+                         int64_t pitch, int32_t* ids, DevParams P, DevErr* err, int with_F) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  float xp[3], Fp[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    xp[a] = x[p * 3 + a];
+    S[(PX + a) * pitch + p] = xp[a];
+    S[(PV + a) * pitch + p] = v[p * 3 + a];
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    S[(PC + k) * pitch + p] = C ? C[p * 9 + k] : 0.0f;
+    Fp[k] = F ? F[p * 9 + k] : ((k % 4 == 0) ? 1.0f : 0.0f);
+    if (with_F) S[(PF + k) * pitch + p] = Fp[k];
+  }
+  ids[p] = (int32_t)p;
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) ok &= in_safe_region(xp[a] * P.inv_dx, P.N[a]);
+  if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
+  if (with_F) {
+    float tau[6];
+    elastic_tau(Fp, P.model, P.mu, P.lam, tau);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) S[(PT + k) * pitch + p] = tau[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) S[(PT + k) * pitch + p] = 0.0f;
+  }
+}
+
+void launch_unpack(cudaStream_t st, int64_t n, const float* x, const float* v, const float* C,
+                   const float* F, float* S, int64_t pitch, int32_t* ids, const DevParams& P,
+                   DevErr* err, int with_F) {
+  if (n == 0) return;
+  int bs = 128;
+  k_unpack<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(n, x, v, C, F, S, pitch, ids, P, err, with_F);
+}
+
+// scatter SoA planes back to caller order (dst row-major AoS, particle id order)
+__global__ void k_pack(int64_t n, const float* __restrict__ S, int64_t pitch,
+                       const int32_t* __restrict__ ids, int plane0, int ncomp, float* out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int64_t id = ids[j];
+  for (int k = 0; k < ncomp; ++k) out[id * ncomp + k] = S[(plane0 + k) * pitch + j];
+}
+
+void launch_pack(cudaStream_t st, int64_t n, const float* S, int64_t pitch, const int32_t* ids,
+                 int plane0, int ncomp, float* out) {
+  if (n == 0) return;
+  int bs = 256;
+  k_pack<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(n, S, pitch, ids, plane0, ncomp, out);
+}
+
+// ---------------------------------------------------------------------------
+// P2G, one thread per particle, 27 x red.global.add.v4.f32 (m, m v) per particle.
+// scene_of(p) from offsets (NSF batches); node = scene * nodes_per_scene + local.
+template <int FORCE>
+__global__ void __launch_bounds__(128) k_p2g_direct(int64_t n, const float* __restrict__ S, int64_t pitch,
+                                                    const int64_t* __restrict__ scene_off, int n_scenes,
+                                                    float4* acc, DevParams P) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int scene = 0;
+  if (n_scenes > 1) {
+    int lo = 0, hi = n_scenes;   // find s with off[s] <= p < off[s+1]
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= p) lo = mid; else hi = mid;
+    }
+    scene = lo;
+  }
+  float xp[3], vp[3], Cp[9], tp[6];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { xp[a] = S[(PX + a) * pitch + p]; vp[a] = S[(PV + a) * pitch + p]; }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Cp[k] = S[(PC + k) * pitch + p];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) tp[k] = S[(PT + k) * pitch + p];
+  Axis ax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ax[a] = bspline_axis(xp[a], P.inv_dx);
+    ax[a].base = clamp_base(ax[a].base, P.N[a]);
+  }
+  const float m = P.mass;
+  // tau as a full symmetric matrix
+  float T[9] = {tp[0], tp[5], tp[4], tp[5], tp[1], tp[3], tp[4], tp[3], tp[2]};
+  // Q = m C - (MLS) dt V0 4/dx^2 tau
+  float Q[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Q[k] = m * Cp[k] - (FORCE == 0 ? P.mls_coef * T[k] : 0.0f);
+  float4* base_ptr = acc + (int64_t)scene * P.nodes_per_scene;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
+        float d0 = ((float)a - ax[0].f) * P.dx;
+        float d1 = ((float)b - ax[1].f) * P.dx;
+        float d2 = ((float)c - ax[2].f) * P.dx;
+        float mv0 = m * vp[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2;
+        float mv1 = m * vp[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2;
+        float mv2 = m * vp[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2;
+        mv0 *= W; mv1 *= W; mv2 *= W;
+        if (FORCE == 1) {
+          float g0 = ax[0].dw[a] * ax[1].w[b] * ax[2].w[c];
+          float g1 = ax[0].w[a] * ax[1].dw[b] * ax[2].w[c];
+          float g2 = ax[0].w[a] * ax[1].w[b] * ax[2].dw[c];
+          mv0 -= P.gradw_coef * (T[0] * g0 + T[1] * g1 + T[2] * g2);
+          mv1 -= P.gradw_coef * (T[3] * g0 + T[4] * g1 + T[5] * g2);
+          mv2 -= P.gradw_coef * (T[6] * g0 + T[7] * g1 + T[8] * g2);
+        }
+        int64_t ni = node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P);
+        red_add_v4(base_ptr + ni, W * m, mv0, mv1, mv2);
+      }
+}
+
+void launch_p2g_direct(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
+                       const int64_t* scene_off, int n_scenes, float4* acc, const DevParams& P) {
+  if (n == 0) return;
+  int bs = 128;
+  unsigned g = (unsigned)((n + bs - 1) / bs);
+  if (P.force_mode == 0) k_p2g_direct<0><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, acc, P);
+  else k_p2g_direct<1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, acc, P);
+}
+
+// ---------------------------------------------------------------------------
+// Grid update for one node: v = mv/m + dt g, walls, plate.  Returns (v, m).
+__device__ __forceinline__ float4 grid_node_update(float4 a, int i, int j, int k, const DevParams& P,
+                                                   float y_plate) {
+  float m = a.x;
+  if (!(m > 0.0f)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  float v[3] = {a.y / m + P.dt * P.g[0], a.z / m + P.dt * P.g[1], a.w / m + P.dt * P.g[2]};
+  int idx[3] = {i, j, k};
+#pragma unroll
+  for (int face = 0; face < 6; ++face) {
+    int kind = P.bc[face];
+    if (kind == 0) continue;
+    int axis = face >> 1;
+    bool high = face & 1;
+    bool in = high ? (idx[axis] >= P.N[axis] - P.bc_width) : (idx[axis] < P.bc_width);
+    if (!in) continue;
+    if (kind == 1) { v[0] = v[1] = v[2] = 0.0f; }
+    else v[axis] = high ? fminf(v[axis], 0.0f) : fmaxf(v[axis], 0.0f);
+  }
+  if (P.plate_enabled && (float)j * P.dx >= y_plate) {
+    v[0] = P.plate_v[0]; v[1] = P.plate_v[1]; v[2] = P.plate_v[2];
+  }
+  return make_float4(v[0], v[1], v[2], m);
+}
+
+__device__ __forceinline__ float plate_y(const DevParams& P, int64_t step) {
+  // y_p(t_n) = y0 + v_y * n dt (reading #12); computed in double to keep t exact
+  return (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)step * (double)P.dt));
+}
+
+// dense update over every node of every scene: vel = update(acc); acc = 0
+__global__ void k_grid_update_dense(int64_t total_nodes, float4* acc, float4* vel, DevParams P,
+                                    const int64_t* d_step) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= total_nodes) return;
+  float4 a = acc[g];
+  if (a.x == 0.0f && a.y == 0.0f && a.z == 0.0f && a.w == 0.0f) {
+    vel[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  int64_t local = g % P.nodes_per_scene;
+  int64_t blk = local >> 6;
+  int l = (int)(local & 63);
+  int b2 = (int)(blk % P.NB[2]);
+  int b1 = (int)((blk / P.NB[2]) % P.NB[1]);
+  int b0 = (int)(blk / ((int64_t)P.NB[2] * P.NB[1]));
+  int i = b0 * 4 + (l >> 4), j = b1 * 4 + ((l >> 2) & 3), k = b2 * 4 + (l & 3);
+  vel[g] = grid_node_update(a, i, j, k, P, plate_y(P, *d_step));
+  acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+void launch_grid_update_dense(cudaStream_t st, int64_t total_nodes, float4* acc, float4* vel,
+                              const DevParams& P, const int64_t* d_step) {
+  int bs = 256;
+  k_grid_update_dense<<<(unsigned)((total_nodes + bs - 1) / bs), bs, 0, st>>>(total_nodes, acc, vel, P, d_step);
+}
+
+// ---------------------------------------------------------------------------
+// G2P + constitutive, one thread per particle, in place (reads and writes index p).
+// WITH_F = 0 is the reduced (NSF) variant: no F, no SVD, tau untouched.
+template <int FORCE, int WITH_F>
+__global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t pitch,
+                                                    const int64_t* __restrict__ scene_off, int n_scenes,
+                                                    const float4* __restrict__ vel, DevParams P,
+                                                    DevErr* err, int64_t* d_step) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p == 0 && d_step) atomicAdd((unsigned long long*)d_step, 1ull);
+  if (p >= n) return;
+  int scene = 0;
+  if (n_scenes > 1) {
+    int lo = 0, hi = n_scenes;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= p) lo = mid; else hi = mid;
+    }
+    scene = lo;
+  }
+  float xp[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) xp[a] = S[(PX + a) * pitch + p];
+  Axis ax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ax[a] = bspline_axis(xp[a], P.inv_dx);
+    ax[a].base = clamp_base(ax[a].base, P.N[a]);
+  }
+  const float4* vb = vel + (int64_t)scene * P.nodes_per_scene;
+  float v[3] = {0.f, 0.f, 0.f};
+  float Bm[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
+        float4 vi = __ldg(vb + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P));
+        float wv0 = W * vi.x, wv1 = W * vi.y, wv2 = W * vi.z;
+        v[0] += wv0; v[1] += wv1; v[2] += wv2;
+        float d0 = ((float)a - ax[0].f) * P.dx;
+        float d1 = ((float)b - ax[1].f) * P.dx;
+        float d2 = ((float)c - ax[2].f) * P.dx;
+        Bm[0] += wv0 * d0; Bm[1] += wv0 * d1; Bm[2] += wv0 * d2;
+        Bm[3] += wv1 * d0; Bm[4] += wv1 * d1; Bm[5] += wv1 * d2;
+        Bm[6] += wv2 * d0; Bm[7] += wv2 * d1; Bm[8] += wv2 * d2;
+        if (FORCE == 1 && WITH_F) {
+          float g0 = ax[0].dw[a] * ax[1].w[b] * ax[2].w[c];
+          float g1 = ax[0].w[a] * ax[1].dw[b] * ax[2].w[c];
+          float g2 = ax[0].w[a] * ax[1].w[b] * ax[2].dw[c];
+          G[0] += vi.x * g0; G[1] += vi.x * g1; G[2] += vi.x * g2;
+          G[3] += vi.y * g0; G[4] += vi.y * g1; G[5] += vi.y * g2;
+          G[6] += vi.z * g0; G[7] += vi.z * g1; G[8] += vi.z * g2;
+        }
+      }
+  const float cC = 4.0f * P.inv_dx * P.inv_dx;   // 12/(dx^2 (b+1)), b = 2
+  float Cn[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Cn[k] = cC * Bm[k];
+  float xn[3];
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    xn[a] = xp[a] + P.dt * v[a];
+    ok &= in_safe_region(xn[a] * P.inv_dx, P.N[a]);
+  }
+  bool finite = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    S[(PX + a) * pitch + p] = xn[a];
+    S[(PV + a) * pitch + p] = v[a];
+    finite &= isfinite(xn[a]) && isfinite(v[a]);
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) S[(PC + k) * pitch + p] = Cn[k];
+  if (WITH_F) {
+    float Fp[9], Ft[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Fp[k] = S[(PF + k) * pitch + p];
+    if (FORCE == 0) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) G[k] = Cn[k];
+    }
+    // F_trial = (I + dt G) F
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        Ft[i * 3 + j] = Fp[i * 3 + j] + P.dt * (G[i * 3 + 0] * Fp[0 * 3 + j] + G[i * 3 + 1] * Fp[1 * 3 + j] +
+                                                G[i * 3 + 2] * Fp[2 * 3 + j]);
+    float FE[9], tau[6];
+    float J = elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) { S[(PF + k) * pitch + p] = FE[k]; finite &= isfinite(FE[k]); }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { S[(PT + k) * pitch + p] = tau[k]; finite &= isfinite(tau[k]); }
+  }
+  if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
+  if (!finite) flag_error(err, ERR_NONFINITE, (int)p);
+}
+
+void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, const int64_t* scene_off,
+                       int n_scenes, const float4* vel, const DevParams& P, DevErr* err, int64_t* d_step,
+                       int with_F) {
+  int bs = 128;
+  unsigned g = (unsigned)((n + bs - 1) / bs);
+  if (g == 0) g = 1;   // still bump the step counter
+  if (with_F) {
+    if (P.force_mode == 0) k_g2p_direct<0, 1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
+    else k_g2p_direct<1, 1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
+  } else {
+    k_g2p_direct<0, 0><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// debug: copy the blocked grid into natural order (scene, i, j, k, 4)
+__global__ void k_grid_to_dense(int64_t total_nodes, const float4* __restrict__ g, float* out, DevParams P) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= total_nodes) return;
+  int64_t scene = q / P.nodes_per_scene;
+  int64_t r = q % P.nodes_per_scene;
+  int k = (int)(r % P.N[2]);
+  int j = (int)((r / P.N[2]) % P.N[1]);
+  int i = (int)(r / ((int64_t)P.N[2] * P.N[1]));
+  float4 a = g[scene * P.nodes_per_scene + node_index(i, j, k, P)];
+  out[q * 4 + 0] = a.x; out[q * 4 + 1] = a.y; out[q * 4 + 2] = a.z; out[q * 4 + 3] = a.w;
+}
+
+// debug: grid update that keeps the accumulator (stage-1 dump), natural order out
+__global__ void k_grid_update_debug(int64_t total_nodes, const float4* __restrict__ acc, float4* vel,
+                                    DevParams P, const int64_t* d_step) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= total_nodes) return;
+  int64_t local = g % P.nodes_per_scene;
+  int64_t blk = local >> 6;
+  int l = (int)(local & 63);
+  int b2 = (int)(blk % P.NB[2]);
+  int b1 = (int)((blk / P.NB[2]) % P.NB[1]);
+  int b0 = (int)(blk / ((int64_t)P.NB[2] * P.NB[1]));
+  int i = b0 * 4 + (l >> 4), j = b1 * 4 + ((l >> 2) & 3), k = b2 * 4 + (l & 3);
+  vel[g] = grid_node_update(acc[g], i, j, k, P, plate_y(P, *d_step));
+}
+
+void launch_grid_debug(cudaStream_t st, int stage, int64_t total_nodes, const float4* acc, float4* vel,
+                       float* out, const DevParams& P, const int64_t* d_step) {
+  int bs = 256;
+  unsigned g = (unsigned)((total_nodes + bs - 1) / bs);
+  if (stage == 1) {
+    k_grid_update_debug<<<g, bs, 0, st>>>(total_nodes, acc, vel, P, d_step);
+    k_grid_to_dense<<<g, bs, 0, st>>>(total_nodes, vel, out, P);
+  } else {
+    k_grid_to_dense<<<g, bs, 0, st>>>(total_nodes, acc, out, P);
+  }
+}
+
+}  // namespace nsf

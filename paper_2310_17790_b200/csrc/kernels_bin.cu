@@ -1,0 +1,200 @@
+// Binning: counting sort of particle slots by the
+// 4x4x4-cell block containing base_p = floor(x_p/dx - 1/2), so that the P2G and
+// G2P CTAs own grid tiles.  Keys are integers computed from exact fp32 products
+// (reading #10), so counts and block_start are bit-exact against the oracle's
+// block_keys; the order inside a block is not unique.
+//
+//   keys_hist : key[j], counts[key]++            (warp-aggregated atomics)
+//   scan      : single-pass decoupled look-back exclusive scan of counts ->
+//               block_start, scatter cursors, compacted non-empty block list;
+//               zeroes counts for the next substep
+//   scatter   : perm[cursor[key]++] = j          (warp-aggregated atomics)
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "pipeline.h"
+
+namespace nsf {
+
+__device__ __forceinline__ int block_key_of(float x0, float x1, float x2, int scene, const DevParams& P) {
+  int b[3];
+  float xs[3] = {x0, x1, x2};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float t = xs[a] * P.inv_dx;
+    int base = (int)floorf(t - 0.5f);
+    base = min(max(base, 0), P.N[a] - 3);
+    b[a] = base >> 2;
+  }
+  return (int)(scene * P.blocks_per_scene + block_id(b[0], b[1], b[2], P));
+}
+
+// warp-aggregated atomicAdd(&arr[key], 1): returns this lane's slot
+__device__ __forceinline__ int aggregated_increment(int* arr, int key, unsigned active) {
+  unsigned peers = __match_any_sync(active, key);
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(peers) - 1;
+  int rank = __popc(peers & ((1u << lane) - 1));
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&arr[key], __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + rank;
+}
+
+__global__ void k_keys_hist(int64_t n, const float* __restrict__ S, int64_t pitch,
+                            const int64_t* __restrict__ scene_off, int n_scenes, int32_t* keys,
+                            int32_t* counts, DevParams P) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned active = __ballot_sync(0xffffffffu, j < n);
+  if (j >= n) return;
+  int scene = 0;
+  if (n_scenes > 1) {
+    int lo = 0, hi = n_scenes;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= j) lo = mid; else hi = mid;
+    }
+    scene = lo;
+  }
+  int key = block_key_of(S[(PX + 0) * pitch + j], S[(PX + 1) * pitch + j], S[(PX + 2) * pitch + j], scene, P);
+  keys[j] = key;
+  aggregated_increment(counts, key, active);
+}
+
+void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch, const int64_t* scene_off,
+                      int n_scenes, int32_t* keys, int32_t* counts, const DevParams& P) {
+  if (n == 0) return;
+  int bs = 256;
+  k_keys_hist<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, keys, counts, P);
+}
+
+// ---------------------------------------------------------------------------
+// decoupled look-back scan.  Packed 64-bit running value: particle count in the
+// low 32 bits, non-empty-block count in bits 32..57; status flag in bits 62..63.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagInc = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* counts, int32_t* block_start,
+                                                       int32_t* cursor, int32_t* nonempty, int32_t* n_nonempty,
+                                                       unsigned long long* status, unsigned int* ticket,
+                                                       int64_t n_tiles) {
+  __shared__ unsigned long long warp_sums[kScanThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_tile;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int c[kScanItems];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) c[k] = (base + k < total) ? counts[base + k] : 0;
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) mine += (unsigned long long)c[k] + ((c[k] > 0 ? 1ull : 0ull) << 32);
+  // block-wide inclusive scan of `mine`
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_sums[warp] = inc;
+  __syncthreads();
+  unsigned long long warp_off = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    if (w < warp) warp_off += warp_sums[w];
+    agg += warp_sums[w];
+  }
+  // look-back
+  if (threadIdx.x == 0) {
+    unsigned long long prefix = 0;
+    if (tile == 0) {
+      atomicExch(&status[0], kFlagInc | agg);
+    } else {
+      atomicExch(&status[tile], kFlagAgg | agg);
+      int64_t t = tile - 1;
+      while (true) {
+        unsigned long long s = *(volatile unsigned long long*)&status[t];
+        if ((s >> 62) == 0) continue;   // not yet published
+        prefix += s & kValMask;
+        if ((s & ~kValMask) == kFlagInc) break;
+        --t;
+      }
+      atomicExch(&status[tile], kFlagInc | (prefix + agg));
+    }
+    s_prefix = prefix;
+  }
+  __syncthreads();
+  unsigned long long run = s_prefix + warp_off + (inc - mine);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = base + k;
+    if (i < total) {
+      int start = (int)(run & 0xffffffffull);
+      block_start[i] = start;
+      cursor[i] = start;
+      if (c[k] > 0) nonempty[(int)(run >> 32)] = (int)i;
+      counts[i] = 0;
+    }
+    run += (unsigned long long)c[k] + ((c[k] > 0 ? 1ull : 0ull) << 32);
+  }
+  if (tile == n_tiles - 1 && threadIdx.x == kScanThreads - 1) {
+    // run now holds the grand total (all later items are padding)
+    block_start[total] = (int)(run & 0xffffffffull);
+    *n_nonempty = (int)(run >> 32);
+  }
+}
+
+void launch_scan(cudaStream_t st, PipelineBuffers* pb) {
+  cudaMemsetAsync(pb->scan_status, 0, sizeof(unsigned long long) * pb->scan_tiles, st);
+  cudaMemsetAsync(pb->scan_ticket, 0, sizeof(unsigned int), st);
+  k_scan<<<(unsigned)pb->scan_tiles, kScanThreads, 0, st>>>(pb->total_blocks, pb->counts, pb->block_start,
+                                                             pb->cursor, pb->nonempty, pb->n_nonempty,
+                                                             pb->scan_status, pb->scan_ticket, pb->scan_tiles);
+}
+
+int64_t scan_tiles_for(int64_t total_blocks) { return (total_blocks + kScanTile - 1) / kScanTile; }
+
+// ---------------------------------------------------------------------------
+__global__ void k_scatter(int64_t n, const int32_t* __restrict__ keys, int32_t* cursor, int32_t* perm) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned active = __ballot_sync(0xffffffffu, j < n);
+  if (j >= n) return;
+  int slot = aggregated_increment(cursor, keys[j], active);
+  perm[slot] = (int32_t)j;
+}
+
+void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cursor, int32_t* perm) {
+  if (n == 0) return;
+  int bs = 256;
+  k_scatter<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(n, keys, cursor, perm);
+}
+
+__global__ void k_gather_ids(int64_t n, const int32_t* __restrict__ perm, const int32_t* __restrict__ ids,
+                             int32_t* out) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) out[k] = ids[perm[k]];
+}
+
+void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out) {
+  if (n == 0) return;
+  k_gather_ids<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, ids, out);
+}
+
+__global__ void k_aos_to_planes(int64_t n, const float* __restrict__ aos, int ncomp, float* planes, int64_t pitch) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = 0; k < ncomp; ++k) planes[k * pitch + i] = aos[i * ncomp + k];
+}
+
+void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch) {
+  if (n == 0) return;
+  k_aos_to_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, aos, ncomp, planes, pitch);
+}
+
+}  // namespace nsf

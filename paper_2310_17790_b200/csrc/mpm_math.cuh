@@ -1,0 +1,270 @@
+// Per-particle device math: quadratic B-spline stencil, rotation-safe 3x3 SVD,
+// polar rotation, constitutive models and return maps (fp32, in registers).
+//
+// PAPER.md citations ("P:L"):
+//   B-spline weights w_ip, degree b = 2 ............ P:165, P:180 (readings #7, #10)
+//   fixed corotated tau = 2 mu (F-R) F^T + lambda (J-1) J I ... P:518 (#2)
+//   Hencky tau = U diag(2 mu eps + lambda sum eps) U^T ...... P:524 (#3)
+//   Drucker-Prager Z(Sigma) .......................... P:528-536 (#6)
+//   von Mises Z(Sigma) .............................. P:538-545 (#4)
+//   rotation-safe SVD, sigma >= 1e-4 before logs ..... reading #21
+#pragma once
+#include <cmath>
+#include "params.cuh"
+
+namespace nsf {
+
+// ---------------------------------------------------------------------------
+// Quadratic B-spline on one axis.  t = x * inv_dx is exact for power-of-two dx
+// (#10), so base and f agree bit-for-bit with the fp64 oracle.
+struct Axis {
+  int base;
+  float f;
+  float w[3];
+  float dw[3];   // d w / d x  (only used by GRADW)
+};
+
+__device__ __forceinline__ Axis bspline_axis(float x, float inv_dx) {
+  Axis a;
+  float t = x * inv_dx;
+  float b = floorf(t - 0.5f);
+  a.base = (int)b;
+  a.f = t - b;
+  float f = a.f;
+  float u = 1.5f - f, m = f - 1.0f, l = f - 0.5f;
+  a.w[0] = 0.5f * u * u;
+  a.w[1] = 0.75f - m * m;
+  a.w[2] = 0.5f * l * l;
+  a.dw[0] = -u * inv_dx;
+  a.dw[1] = -2.0f * m * inv_dx;
+  a.dw[2] = l * inv_dx;
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// small 3x3 helpers (row-major float[9])
+__device__ __forceinline__ float det3(const float A[9]) {
+  return A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+         A[2] * (A[3] * A[7] - A[4] * A[6]);
+}
+
+// One cyclic-Jacobi rotation zeroing S[p][q] of the symmetric S, accumulating V.
+// (Classic two-sided Jacobi eigenvalue step on S = A^T A.)
+__device__ __forceinline__ void jacobi_pq(float S[3][3], float V[3][3], int p, int q) {
+  float apq = S[p][q];
+  if (apq == 0.0f) return;
+  float app = S[p][p], aqq = S[q][q];
+  float theta = (aqq - app) / (2.0f * apq);
+  float t = copysignf(1.0f, theta) / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f)));
+  float c = rsqrtf(fmaf(t, t, 1.0f));
+  float s = t * c;
+  S[p][p] = app - t * apq;
+  S[q][q] = aqq + t * apq;
+  S[p][q] = 0.0f;
+  S[q][p] = 0.0f;
+  int r = 3 - p - q;
+  float srp = S[r][p], srq = S[r][q];
+  float nrp = c * srp - s * srq;
+  float nrq = s * srp + c * srq;
+  S[r][p] = nrp; S[p][r] = nrp;
+  S[r][q] = nrq; S[q][r] = nrq;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float vip = V[i][p], viq = V[i][q];
+    V[i][p] = c * vip - s * viq;
+    V[i][q] = s * vip + c * viq;
+  }
+}
+
+// Givens rotation on rows (a, b) of B zeroing B[b][col]; the same row rotation
+// is applied to Qt (so that Qt B = R at the end).
+__device__ __forceinline__ void givens_rows(float B[3][3], float Qt[3][3], int a, int b, int col) {
+  float x = B[a][col], y = B[b][col];
+  float r2 = fmaf(x, x, y * y);
+  float c = 1.0f, s = 0.0f;
+  if (r2 > 1e-37f) {
+    float ir = rsqrtf(r2);
+    c = x * ir;
+    s = y * ir;
+  }
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    float ba = B[a][j], bb = B[b][j];
+    B[a][j] = c * ba + s * bb;
+    B[b][j] = -s * ba + c * bb;
+    float qa = Qt[a][j], qb = Qt[b][j];
+    Qt[a][j] = c * qa + s * qb;
+    Qt[b][j] = -s * qa + c * qb;
+  }
+}
+
+// Rotation-safe SVD A = U diag(sig) V^T, det U = det V = +1, sig sorted by
+// decreasing magnitude with any reflection folded into sig[2] (reading #21).
+// Jacobi eigen-decomposition of A^T A gives V; QR (Givens) of A V gives U, sig.
+__device__ __forceinline__ void svd3(const float A[9], float U[3][3], float sig[3], float V[3][3]) {
+  float S[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      S[i][j] = A[0 * 3 + i] * A[0 * 3 + j] + A[1 * 3 + i] * A[1 * 3 + j] + A[2 * 3 + i] * A[2 * 3 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0f : 0.0f;
+
+  for (int sweep = 0; sweep < 6; ++sweep) {
+    float off = fabsf(S[0][1]) + fabsf(S[0][2]) + fabsf(S[1][2]);
+    float dia = fabsf(S[0][0]) + fabsf(S[1][1]) + fabsf(S[2][2]);
+    if (off <= 1e-9f * dia) break;
+    jacobi_pq(S, V, 0, 1);
+    jacobi_pq(S, V, 0, 2);
+    jacobi_pq(S, V, 1, 2);
+  }
+  // B = A V
+  float B[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      B[i][j] = A[i * 3 + 0] * V[0][j] + A[i * 3 + 1] * V[1][j] + A[i * 3 + 2] * V[2][j];
+  // sort columns by decreasing norm; each swap negates one column so det V stays +1
+  float n0 = B[0][0] * B[0][0] + B[1][0] * B[1][0] + B[2][0] * B[2][0];
+  float n1 = B[0][1] * B[0][1] + B[1][1] * B[1][1] + B[2][1] * B[2][1];
+  float n2 = B[0][2] * B[0][2] + B[1][2] * B[1][2] + B[2][2] * B[2][2];
+  auto swapcol = [&](int a, int b) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      float t = B[i][a]; B[i][a] = -B[i][b]; B[i][b] = t;
+      float u = V[i][a]; V[i][a] = -V[i][b]; V[i][b] = u;
+    }
+  };
+  if (n0 < n1) { swapcol(0, 1); float t = n0; n0 = n1; n1 = t; }
+  if (n0 < n2) { swapcol(0, 2); float t = n0; n0 = n2; n2 = t; }
+  if (n1 < n2) { swapcol(1, 2); float t = n1; n1 = n2; n2 = t; }
+  // QR of B by Givens: Qt B = R, U = Qt^T
+  float Qt[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Qt[i][j] = (i == j) ? 1.0f : 0.0f;
+  givens_rows(B, Qt, 0, 1, 0);
+  givens_rows(B, Qt, 0, 2, 0);
+  givens_rows(B, Qt, 1, 2, 1);
+  sig[0] = B[0][0];
+  sig[1] = B[1][1];
+  sig[2] = B[2][2];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) U[i][j] = Qt[j][i];
+}
+
+// ---------------------------------------------------------------------------
+// constitutive update: F_trial -> (F_E, tau Voigt).  Returns det(F_E).
+//   model 0: fixed corotated   1: Drucker-Prager + Hencky   2: von Mises + Hencky
+__device__ __forceinline__ float elastoplastic(const float Ft[9], int model, float mu, float lam,
+                                               float alpha, float tau_Y, float FE[9], float tau[6]) {
+  float U[3][3], V[3][3], s[3];
+  svd3(Ft, U, s, V);
+  if (model == 0) {
+    // R = U V^T ; tau = 2 mu (F - R) F^T + lambda (J - 1) J I
+    float R[9], D[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        R[i * 3 + j] = U[i][0] * V[j][0] + U[i][1] * V[j][1] + U[i][2] * V[j][2];
+        D[i * 3 + j] = Ft[i * 3 + j] - R[i * 3 + j];
+      }
+    float J = det3(Ft);
+    float vol = lam * (J - 1.0f) * J;
+    float T[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        T[i][j] = 2.0f * mu * (D[i * 3 + 0] * Ft[j * 3 + 0] + D[i * 3 + 1] * Ft[j * 3 + 1] +
+                               D[i * 3 + 2] * Ft[j * 3 + 2]);
+    tau[0] = T[0][0] + vol;
+    tau[1] = T[1][1] + vol;
+    tau[2] = T[2][2] + vol;
+    tau[3] = 0.5f * (T[1][2] + T[2][1]);
+    tau[4] = 0.5f * (T[0][2] + T[2][0]);
+    tau[5] = 0.5f * (T[0][1] + T[1][0]);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+    return J;
+  }
+  // log-strain models (reading #21: clamp sigma >= 1e-4)
+  const float kFloor = 1e-4f;
+  bool clamped = (s[0] < kFloor) | (s[1] < kFloor) | (s[2] < kFloor);
+  float sc[3] = {fmaxf(s[0], kFloor), fmaxf(s[1], kFloor), fmaxf(s[2], kFloor)};
+  float e[3] = {logf(sc[0]), logf(sc[1]), logf(sc[2])};
+  float tr = e[0] + e[1] + e[2];
+  float eh[3] = {e[0] - tr * (1.0f / 3.0f), e[1] - tr * (1.0f / 3.0f), e[2] - tr * (1.0f / 3.0f)};
+  float nrm = sqrtf(eh[0] * eh[0] + eh[1] * eh[1] + eh[2] * eh[2]);
+  float dg;
+  bool expand = false;
+  if (model == 1) {
+    expand = tr > 0.0f;
+    dg = nrm + alpha * (3.0f * lam + 2.0f * mu) * tr / (2.0f * mu);
+  } else {
+    dg = nrm - tau_Y / (2.0f * mu);
+  }
+  float le[3];   // log Z
+  bool elastic = false;
+  if (expand) {
+    le[0] = le[1] = le[2] = 0.0f;
+  } else if (dg <= 0.0f) {
+    le[0] = e[0]; le[1] = e[1]; le[2] = e[2];
+    elastic = true;
+  } else {
+    float k = dg / nrm;
+    le[0] = e[0] - k * eh[0];
+    le[1] = e[1] - k * eh[1];
+    le[2] = e[2] - k * eh[2];
+  }
+  float detFE;
+  if (elastic && !clamped) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+    detFE = det3(Ft);
+  } else {
+    float Z[3];
+    if (elastic) { Z[0] = sc[0]; Z[1] = sc[1]; Z[2] = sc[2]; }
+    else { Z[0] = expf(le[0]); Z[1] = expf(le[1]); Z[2] = expf(le[2]); }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        FE[i * 3 + j] = U[i][0] * Z[0] * V[j][0] + U[i][1] * Z[1] * V[j][1] + U[i][2] * Z[2] * V[j][2];
+    detFE = Z[0] * Z[1] * Z[2];
+  }
+  const float kLogFloor = -9.210340371976184f;   // log(1e-4)
+  float l0 = fmaxf(le[0], kLogFloor), l1 = fmaxf(le[1], kLogFloor), l2 = fmaxf(le[2], kLogFloor);
+  float sum = l0 + l1 + l2;
+  float d0 = 2.0f * mu * l0 + lam * sum, d1 = 2.0f * mu * l1 + lam * sum, d2 = 2.0f * mu * l2 + lam * sum;
+  // tau = U diag(d) U^T
+  tau[0] = U[0][0] * U[0][0] * d0 + U[0][1] * U[0][1] * d1 + U[0][2] * U[0][2] * d2;
+  tau[1] = U[1][0] * U[1][0] * d0 + U[1][1] * U[1][1] * d1 + U[1][2] * U[1][2] * d2;
+  tau[2] = U[2][0] * U[2][0] * d0 + U[2][1] * U[2][1] * d1 + U[2][2] * U[2][2] * d2;
+  tau[3] = U[1][0] * U[2][0] * d0 + U[1][1] * U[2][1] * d1 + U[1][2] * U[2][2] * d2;
+  tau[4] = U[0][0] * U[2][0] * d0 + U[0][1] * U[2][1] * d1 + U[0][2] * U[2][2] * d2;
+  tau[5] = U[0][0] * U[1][0] * d0 + U[0][1] * U[1][1] * d1 + U[0][2] * U[1][2] * d2;
+  return detFE;
+}
+
+// Elastic stress of a given (admissible) F, used for tau^0 at load (reading #9).
+__device__ __forceinline__ void elastic_tau(const float F[9], int model, float mu, float lam, float tau[6]) {
+  float FE[9];
+  // FC: same formula; DP/VM: Hencky of F itself (no return map at load)
+  if (model == 0) {
+    elastoplastic(F, 0, mu, lam, 0.0f, 0.0f, FE, tau);
+  } else {
+    // tau_Y = +inf -> von Mises never yields -> pure Hencky
+    elastoplastic(F, 2, mu, lam, 0.0f, INFINITY, FE, tau);
+  }
+}
+
+}  // namespace nsf

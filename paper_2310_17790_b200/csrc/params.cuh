@@ -1,0 +1,64 @@
+// Device-side parameters and grid indexing shared by every kernel.
+// Layout:
+//   grid  : 4x4x4-node blocks, each a contiguous 1 KB of float4; block id
+//           b = (b0*NB1 + b1)*NB2 + b2, node (l0,l1,l2) in block at l0*16 + l1*4 + l2;
+//           scenes are concatenated (scene s starts at s * nodes_per_scene).
+//   particles: SoA component planes, float32, each plane `pitch` floats long.
+#pragma once
+#include <cstdint>
+
+namespace nsf {
+
+constexpr int kBlock = 4;            // cells / nodes per block edge
+constexpr int kBlockNodes = 64;      // 4^3
+
+// plane indices inside one particle buffer set
+enum Plane : int {
+  PX = 0,   // x0..x2
+  PV = 3,   // v0..v2
+  PC = 6,   // C00..C22 (row-major)
+  PF = 15,  // F00..F22
+  PT = 24,  // tau Voigt xx,yy,zz,yz,xz,xy
+  kPlanes = 30
+};
+
+enum ErrBits : uint32_t { ERR_OUT_OF_DOMAIN = 1u, ERR_NONFINITE = 2u };
+
+struct DevErr {
+  uint32_t bits;
+  int32_t first_index;   // atomicMin over offending particle ids
+  int64_t step;          // substep at which the first error was seen (approximate)
+  unsigned long long inverted;  // count of det F_E <= 0 updates
+};
+
+struct DevParams {
+  int N[3];          // nodes per axis
+  int NB[3];         // blocks per axis
+  int n_scenes;
+  long long nodes_per_scene;
+  long long blocks_per_scene;
+  float dx, inv_dx, dt;
+  float mass, V0;
+  float mu, lam, alpha, tau_Y;
+  float g[3];
+  int bc[6];
+  int bc_width;
+  int plate_enabled;
+  float plate_y0;
+  float plate_v[3];
+  int model;
+  int force_mode;
+  float mls_coef;    // dt V0 4/dx^2
+  float gradw_coef;  // dt V0
+  float stress_scale;
+};
+
+__host__ __device__ inline long long block_id(int b0, int b1, int b2, const DevParams& P) {
+  return ((long long)b0 * P.NB[1] + b1) * P.NB[2] + b2;
+}
+
+__host__ __device__ inline long long node_index(int i, int j, int k, const DevParams& P) {
+  return block_id(i >> 2, j >> 2, k >> 2, P) * kBlockNodes + ((i & 3) << 4) + ((j & 3) << 2) + (k & 3);
+}
+
+}  // namespace nsf

@@ -1,0 +1,153 @@
+// Substep pipeline: the order of kernels for one MLS-MPM substep (PAPER.md
+// §3.3) and for the reduced variant.
+#include <cuda_runtime.h>
+#include <cstring>
+#include "pipeline.h"
+
+namespace nsf {
+
+int64_t scan_tiles_for(int64_t total_blocks);
+
+#define PLAUNCH(h, name, ...)           \
+  do {                                  \
+    cudaEvent_t _ev = nullptr;          \
+    prof_begin(h, name, &_ev);          \
+    __VA_ARGS__;                        \
+    prof_end(h, name, _ev);             \
+  } while (0)
+
+int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t total_blocks) {
+  pb->total_blocks = total_blocks;
+  pb->scan_tiles = scan_tiles_for(total_blocks);
+  pb->counts = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
+  pb->block_start = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * (total_blocks + 1));
+  pb->cursor = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
+  pb->nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
+  pb->n_nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 4);
+  pb->scan_status = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * pb->scan_tiles);
+  pb->scan_ticket = (unsigned int*)pipeline_alloc(h, sizeof(unsigned int) * 4);
+  if (!pb->counts || !pb->block_start || !pb->cursor || !pb->nonempty || !pb->n_nonempty || !pb->scan_status ||
+      !pb->scan_ticket)
+    return -1;
+  HandleView v = view(h);
+  if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * total_blocks, v.stream) != cudaSuccess) return -1;
+  pb->tiled = false;
+  (void)P;
+  return 0;
+}
+
+nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
+  if (pb->keys) pipeline_free(h, pb->keys);
+  if (pb->perm) pipeline_free(h, pb->perm);
+  pb->keys = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
+  pb->perm = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
+  pb->pitch = pitch;
+  if (!pb->keys || !pb->perm) return NSF_ERR_OUT_OF_MEMORY;
+  return NSF_OK;
+}
+
+nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  (void)pb;
+  return NSF_OK;
+}
+
+void pipeline_on_mlp(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  (void)pb;
+}
+
+bool pipeline_graphable(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  (void)pb;
+  return true;
+}
+
+// build the binning of buffer `cur` (keys + counts -> block_start, perm, non-empty list)
+static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
+  PLAUNCH(h, "bin_keys_hist",
+          launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
+  PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+  PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
+}
+
+int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur) {
+  HandleView v = view(h);
+  const bool nsf_model = v.model == NSF_NEURAL_STRESS;
+  int launches = 0;
+  if (nsf_model) {
+    PLAUNCH(h, "nsf_mlp",
+            launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
+                           v.P->stress_scale, v.S[cur] + PT * v.pitch, v.pitch, 0));
+    ++launches;
+  }
+  PLAUNCH(h, "p2g_direct", launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P));
+  PLAUNCH(h, "grid_update_dense", launch_grid_update_dense(v.stream, v.total_nodes, v.acc, v.vel, *v.P, v.d_step));
+  PLAUNCH(h, "g2p_direct",
+          launch_g2p_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.vel, *v.P, v.err, v.d_step,
+                            nsf_model ? 0 : 1));
+  launches += (v.n > 0 ? 3 : 2);
+  pb->launches = launches;
+  return cur;
+}
+
+void pipeline_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch) {
+  launch_aos_to_planes(st, n, aos, ncomp, planes, pitch);
+}
+
+void pipeline_eval_mlp(nsf_mpm* h, PipelineBuffers* pb, int64_t m, const float* planes, int64_t pitch,
+                       const float* z, int r, float* tau_aos) {
+  (void)pb;
+  HandleView v = view(h);
+  PLAUNCH(h, "nsf_mlp_eval",
+          launch_nsf_mlp(v.stream, m, planes, pitch, nullptr, 1, z, nullptr, r, nullptr, *v.mlp, v.P->stress_scale,
+                         tau_aos, 0, 1));
+}
+
+int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* counts, int32_t* perm, int on_device) {
+  HandleView v = view(h);
+  // counts: histogram only (then clear), perm: full binning mapped to load order
+  if (counts) {
+    launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
+    if (cudaMemcpyAsync(counts, pb->counts, sizeof(int32_t) * pb->total_blocks,
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, v.stream) != cudaSuccess)
+      return -1;
+    if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess) return -1;
+  }
+  if (perm) {
+    enqueue_binning(h, pb, v, cur);
+    int32_t* tmp = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * (v.n + 1));
+    if (!tmp) return -1;
+    launch_gather_ids(v.stream, v.n, pb->perm, v.ids[cur], tmp);
+    cudaError_t e = cudaMemcpyAsync(perm, tmp, sizeof(int32_t) * v.n,
+                                    on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, v.stream);
+    cudaStreamSynchronize(v.stream);
+    pipeline_free(h, tmp);
+    if (e != cudaSuccess) return -1;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, float* out) {
+  HandleView v = view(h);
+  (void)pb;
+  if (v.model == NSF_NEURAL_STRESS)
+    launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
+                   v.P->stress_scale, v.S[cur] + PT * v.pitch, v.pitch, 0);
+  launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P);
+  launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
+  if (cudaMemsetAsync(v.acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return -1;
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int pipeline_launches_per_substep(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  return pb->launches;
+}
+
+void pipeline_destroy(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  (void)pb;   // buffers are tracked and freed by the handle's allocation list
+}
+
+}  // namespace nsf

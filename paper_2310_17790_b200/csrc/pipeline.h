@@ -1,0 +1,86 @@
+// Substep pipeline (internal): which kernels run, in which order, on which
+// buffers.  runtime.cu owns the handle; this layer only sees a HandleView.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "../../include/nsf_mpm.h"
+#include "kernels.h"
+#include "params.cuh"
+
+namespace nsf {
+
+struct PipelineBuffers {
+  // binning: block key per particle slot, per-block counts,
+  // start offsets (exclusive scan), scatter cursors, permutation, active list
+  int32_t* keys = nullptr;          // [pitch]
+  int32_t* counts = nullptr;        // [total_blocks]      (zero between substeps)
+  int32_t* block_start = nullptr;   // [total_blocks + 1]
+  int32_t* cursor = nullptr;        // [total_blocks]
+  int32_t* perm = nullptr;          // [pitch]  sorted slot -> storage slot
+  int32_t* nonempty = nullptr;      // [total_blocks] list of non-empty block ids
+  int32_t* n_nonempty = nullptr;    // [1]
+  unsigned long long* scan_status = nullptr;  // [scan tiles]
+  unsigned int* scan_ticket = nullptr;        // [1]
+  int64_t scan_tiles = 0;
+  int64_t total_blocks = 0;
+  int64_t pitch = 0;
+  bool tiled = false;               // dense tiled path (full-order models)
+  int launches = 0;                 // kernels per substep (last enqueued)
+};
+
+struct HandleView {
+  const DevParams* P;
+  cudaStream_t stream;
+  int64_t n, pitch;
+  float* S[2];
+  int32_t* ids[2];
+  const int64_t* scene_off;
+  const int64_t* scene_off_host;
+  int n_scenes;
+  float4* acc;
+  float4* vel;
+  int64_t total_nodes, total_blocks;
+  DevErr* err;
+  int64_t* d_step;
+  const MlpDev* mlp;
+  const float* X;
+  const float* z;
+  const float* dz;
+  int r;
+  int model;
+};
+
+// provided by runtime.cu
+HandleView view(nsf_mpm* h);
+void set_cur(nsf_mpm* h, int cur);
+void* pipeline_alloc(nsf_mpm* h, size_t bytes);
+void pipeline_free(nsf_mpm* h, void* p);
+void prof_begin(nsf_mpm* h, const char* name, cudaEvent_t* a);
+void prof_end(nsf_mpm* h, const char* name, cudaEvent_t a);
+
+// provided by pipeline.cu
+int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t total_blocks);
+nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch);
+nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb);
+void pipeline_on_mlp(nsf_mpm* h, PipelineBuffers* pb);
+bool pipeline_graphable(nsf_mpm* h, PipelineBuffers* pb);
+int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur);   // returns next buffer or -1
+void pipeline_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes,
+                            int64_t pitch);
+void pipeline_eval_mlp(nsf_mpm* h, PipelineBuffers* pb, int64_t m, const float* planes, int64_t pitch,
+                       const float* z, int r, float* tau_aos);
+int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* counts, int32_t* perm,
+                        int on_device);
+int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, float* out);
+int pipeline_launches_per_substep(nsf_mpm* h, PipelineBuffers* pb);
+void pipeline_destroy(nsf_mpm* h, PipelineBuffers* pb);
+
+// kernels_bin.cu
+void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch, const int64_t* scene_off,
+                      int n_scenes, int32_t* keys, int32_t* counts, const DevParams& P);
+void launch_scan(cudaStream_t st, PipelineBuffers* pb);
+void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cursor, int32_t* perm);
+void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out);
+void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch);
+
+}  // namespace nsf
