@@ -1,0 +1,349 @@
+#!/usr/bin/env python3
+"""Benchmark of the MLS-MPM substep hot path on B200 (BASELINE.json metric:
+particle-substeps/s on 1 B200; achieved HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+One "step" = one full substep (binning, P2G, grid update, G2P + constitutive
+update) over the whole workload.  Default workload
+is BASELINE.json config 3 (1,000,000-particle von Mises block with a moving
+plate on a 256^3 grid), the configuration the metric's 50%-of-HBM target is
+quoted on.  Inputs are synthetic and seeded (scenes/), resident in HBM when
+the timed region starts; the state (2 x 120 MB) and the bytes moved per
+substep (~268 MB) exceed the 126 MB L2, so no explicit flush is needed.
+
+Multi-GPU: replicas only: each rank simulates its own
+replica of the workload, no data-path collective; value = all particles x K /
+max-over-ranks time; "scaling": "weak".
+
+--impl reference: the fp64 CPU oracle (oracle/, test infrastructure), timed on
+the host cores, each step one oracle substep on a bounded contiguous sample of
+the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+# the oracle legs (cpu_baseline, --impl reference) are timed single-threaded
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
+
+CONFIG_DESC = {
+    "C1": "elastic cube drop, 4,096 particles, 32^3 grid, fixed-corotated",
+    "C2": "sand column collapse, 200,000 particles, 128^3 grid, Drucker-Prager",
+    "C3": "metal compression, 1,000,000 particles, 256^3 grid, von Mises + moving plate",
+    "C4": "large sparse scene, 8,000,000 particles (64 balls), 512^3 grid, fixed-corotated",
+}
+
+# Algorithmic bytes per unit:
+# per particle-substep for particle kernels, per touched node for the grid.
+KERNEL_BYTES_PER_PARTICLE = {
+    "p2g_direct": 84.0,          # x, v, C, tau read (fp32 SoA)
+    "p2g_tiled": 88.0,           # + perm
+    "g2p_direct": 48.0 + 120.0,  # x, F read; x, v, C, F, tau written
+    "g2p_tiled": 4.0 + 48.0 + 120.0 + 4.0,  # perm, x, F in; 5 fields + next key out
+    "bin_keys_hist": 12.0 + 4.0,
+    "bin_scatter": 8.0,
+}
+B_ALG_PER_PARTICLE_SUBSTEP = 268.0   # 84 + 48 + 120 + 16
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.dev = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.dev, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.dev, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.dev)
+                for bit, nm in self.REASONS.items():
+                    if r & bit and nm != "gpu_idle":
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_scene(name):
+    import scenes
+    return {"C1": scenes.c1, "C2": scenes.c2, "C3": scenes.c3, "C4": scenes.c4}[name]()
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """fp64 oracle on host cores; each step = one oracle substep on a bounded
+    contiguous sample of the workload."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import mpm
+    sc = make_scene(args.config)
+    P = mpm.params_from_config(sc.cfg)
+    S = min(args.ref_sample, sc.n)
+    st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S], "F": sc.F[:S],
+          "tau": mpm.initial_tau(sc.F[:S], P)}
+    for k in range(args.warmup):
+        st = mpm.substep(st, P, k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        st = mpm.substep(st, P, args.warmup + k)
+    dt = time.perf_counter() - t0
+    value = S * args.steps / dt
+    line = {"metric": "particle-substeps/s", "value": value, "unit": "particle-substeps/s",
+            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (scenes/, seeded)",
+            "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
+                       "sample": f"first {S} particles (cell order) of the workload, one oracle substep per step"},
+            "cpu_baseline": {"value": value, "unit": "particle-substeps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{S} particles x {args.steps} substeps"},
+            "e2e": {"value": value, "unit": "particle-substeps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(sc, budget_s=15.0, sample=50000):
+    """Oracle as it stands, single thread, on a bounded sample (rank 0, N=1)."""
+    from oracle import mpm
+    P = mpm.params_from_config(sc.cfg)
+    S = min(sample, sc.n)
+    st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S], "F": sc.F[:S], "tau": mpm.initial_tau(sc.F[:S], P)}
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        st = mpm.substep(st, P, k)
+        k += 1
+        if time.perf_counter() - t0 > budget_s or k >= 50:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": S * k / dt, "unit": "particle-substeps/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {S} particles of the workload x {k} substeps ({dt:.1f} s, fp64 numpy, 1 thread)"}
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2310_17790_b200 as nsf
+
+    sc = make_scene(args.config)
+    n = sc.n
+    stream = torch.cuda.Stream(device=dev)
+    sim = nsf.Simulator(sc.cfg, stream=stream.cuda_stream)
+    xs = {k: torch.from_numpy(getattr(sc, k)).to(dev) for k in ("x", "v", "C", "F")}
+    torch.cuda.synchronize()
+    sim.load(xs["x"], xs["v"], xs["C"], xs["F"])
+    # warm-up (also captures the CUDA graph)
+    sim.substep(args.warmup)
+    sim.sync()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K substeps, inputs resident in HBM ----
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        sim.substep(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    sim.sync()   # surfaces deferred device errors
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    per_sub = nsf.nsf_mpm_launches_per_substep(sim.h)
+    value = world * n * args.steps / (ms * 1e-3)
+
+    # ---- per-kernel timing pass (CUDA events around each launch, same stream) ----
+    nsf.nsf_mpm_set_profiling(sim.h, True)
+    sim.substep(args.steps)
+    sim.sync()
+    kt = nsf.nsf_mpm_kernel_times(sim.h)
+    nsf.nsf_mpm_set_profiling(sim.h, False)
+    peak, peak_src = load_peaks()
+    top = max(kt.items(), key=lambda kv: kv[1][0]) if kt else None
+    roof = None
+    if top is not None:
+        name, (tot_ms, cnt) = top
+        bpp = KERNEL_BYTES_PER_PARTICLE.get(name)
+        avg_ms = tot_ms / max(cnt, 1)
+        if bpp is not None:
+            achieved = bpp * n / (avg_ms * 1e-3) / 1e9
+            traffic = load_traffic().get(args.config, {}).get(name)
+            roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "bytes_per_launch": bpp * n, "avg_launch_ms": avg_ms,
+                    "share_of_step": tot_ms / sum(v[0] for v in kt.values()),
+                    "peak_source": peak_src}
+    step_gbs = B_ALG_PER_PARTICLE_SUBSTEP * n / (ms / args.steps * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers ----
+    pin = {k: torch.from_numpy(getattr(sc, k)).pin_memory() for k in ("x", "v", "C", "F")}
+    out_x = torch.empty((n, 3), dtype=torch.float32).pin_memory()
+    out_v = torch.empty((n, 3), dtype=torch.float32).pin_memory()
+    import ctypes
+    lib = nsf.lib()
+    h2d = sum(t.numel() * 4 for t in pin.values())
+    d2h = 2 * n * 3 * 4
+    e2e_iters = max(1, args.e2e_iters)
+    sim.load(pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy())
+    sim.substep(2)
+    sim.sync()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_iters):
+        nsf.nsf_mpm_load_particles(sim.h, pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy())
+        nsf.nsf_mpm_substep(sim.h, args.steps)
+        ptrs = (ctypes.c_void_p * 2)(out_x.data_ptr(), out_v.data_ptr())
+        st = lib.nsf_mpm_read_state(sim.h, nsf.NSF_FIELD_X | nsf.NSF_FIELD_V, ptrs, 0)
+        assert st == 0, nsf.nsf_mpm_last_error(sim.h)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_iters
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * n * args.steps / e2e_s
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(sc)
+
+    sim.close()
+    if rank == 0:
+        line = {
+            "metric": "particle-substeps/s", "value": value, "unit": "particle-substeps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenes/, seeded)",
+            "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
+                       "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
+                       "replicas": world, "l2": "inputs larger than L2 (state 2x120 MB, ~268 MB moved per substep)",
+                       "step": "one full substep: binning, P2G, grid update, G2P + return map"},
+            "hbm_alg_gbs_whole_step": step_gbs,
+            "hbm_alg_frac_whole_step": step_gbs / peak,
+            "roofline": roof,
+            "kernel_ms_per_substep": {k: v[0] / max(args.steps, 1) for k, v in kt.items()},
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": "particle-substeps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "definition": f"one e2e step = load state from pinned host, {args.steps} substeps, "
+                                  "read x and v back to pinned host"},
+            "gpu_launches": per_sub * args.steps,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-iters", type=int, default=2)
+    ap.add_argument("--ref-sample", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -46,9 +46,17 @@ nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
   return NSF_OK;
 }
 
+// Invariant of the dense (tiled) path between substeps: keys[] and counts[]
+// describe the particles of the current buffer (written by the last G2P, or
+// here after a load).
 nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
-  (void)h;
-  (void)pb;
+  HandleView v = view(h);
+  pb->tiled = v.model != NSF_NEURAL_STRESS;
+  if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess)
+    return NSF_ERR_CUDA;
+  if (pb->tiled)
+    launch_keys_hist(v.stream, v.n, v.S[0], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
+  if (cudaGetLastError() != cudaSuccess) return NSF_ERR_CUDA;
   return NSF_OK;
 }
 
@@ -71,22 +79,47 @@ static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v
   PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
 }
 
+// One substep.  Dense full-order path (tiled):
+//   scan -> scatter -> P2G (tiled MLS, or direct for GRADW) -> grid update over
+//   touched blocks -> G2P (sort-on-write into the other buffer, next keys+hist)
+// Reduced (NSF) path: keys+hist -> scan -> MLP -> direct P2G -> grid update over
+//   touched blocks -> direct G2P (points are ~0.1 per cell: tiles do not pay).
 int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur) {
   HandleView v = view(h);
   const bool nsf_model = v.model == NSF_NEURAL_STRESS;
   int launches = 0;
-  if (nsf_model) {
-    PLAUNCH(h, "nsf_mlp",
-            launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
-                           v.P->stress_scale, v.S[cur] + PT * v.pitch, v.pitch, 0));
-    ++launches;
+  if (!nsf_model) {
+    const int nxt = 1 - cur;
+    PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+    PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
+    launches += 1 + (v.n > 0);
+    if (v.P->force_mode == NSF_FORCE_MLS) {
+      PLAUNCH(h, "p2g_tiled", launch_p2g_tiled(v.stream, v.S[cur], v.pitch, pb->perm, pb, v.acc, *v.P));
+      ++launches;
+    } else {
+      PLAUNCH(h, "p2g_direct",
+              launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P));
+      launches += (v.n > 0);
+    }
+    PLAUNCH(h, "grid_update", launch_grid_update_blocks(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
+    PLAUNCH(h, "g2p_tiled",
+            launch_g2p_tiled(v.stream, v.S[cur], v.S[nxt], v.pitch, v.ids[cur], v.ids[nxt], pb, v.vel, *v.P, v.err,
+                             v.d_step));
+    launches += 2;
+    pb->launches = launches;
+    return nxt;
   }
+  PLAUNCH(h, "bin_keys_hist",
+          launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
+  PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+  PLAUNCH(h, "nsf_mlp",
+          launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
+                         v.P->stress_scale, v.S[cur] + PT * v.pitch, v.pitch, 0));
   PLAUNCH(h, "p2g_direct", launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P));
-  PLAUNCH(h, "grid_update_dense", launch_grid_update_dense(v.stream, v.total_nodes, v.acc, v.vel, *v.P, v.d_step));
+  PLAUNCH(h, "grid_update", launch_grid_update_blocks(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
   PLAUNCH(h, "g2p_direct",
-          launch_g2p_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.vel, *v.P, v.err, v.d_step,
-                            nsf_model ? 0 : 1));
-  launches += (v.n > 0 ? 3 : 2);
+          launch_g2p_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.vel, *v.P, v.err, v.d_step, 0));
+  launches += (v.n > 0 ? 6 : 3);
   pb->launches = launches;
   return cur;
 }
@@ -106,7 +139,9 @@ void pipeline_eval_mlp(nsf_mpm* h, PipelineBuffers* pb, int64_t m, const float* 
 
 int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* counts, int32_t* perm, int on_device) {
   HandleView v = view(h);
-  // counts: histogram only (then clear), perm: full binning mapped to load order
+  // counts: histogram only (then clear), perm: full binning mapped to load order;
+  // finally restore the between-substep invariant (keys/counts of buffer cur)
+  if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess) return -1;
   if (counts) {
     launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
     if (cudaMemcpyAsync(counts, pb->counts, sizeof(int32_t) * pb->total_blocks,
@@ -125,6 +160,8 @@ int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* count
     pipeline_free(h, tmp);
     if (e != cudaSuccess) return -1;
   }
+  if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess) return -1;
+  if (pb->tiled) launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -83,4 +83,13 @@ void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cu
 void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out);
 void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch);
 
+// kernels_tiled.cu
+void launch_p2g_tiled(cudaStream_t st, const float* S, int64_t pitch, const int32_t* perm, const PipelineBuffers* pb,
+                      float4* acc, const DevParams& P);
+void launch_grid_update_blocks(cudaStream_t st, const PipelineBuffers* pb, float4* acc, float4* vel,
+                               const DevParams& P, const int64_t* d_step);
+void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t pitch, const int32_t* ids_in,
+                      int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const DevParams& P, DevErr* err,
+                      int64_t* d_step);
+
 }  // namespace nsf

@@ -53,7 +53,22 @@ def small_scenes():
         "VM_gradw": S.block_scene("VMg", 32, (9, 3, 8), (21, 13, 22), S.VON_MISES, 15,
                                   keep=4000, vnoise=0.2, Fnoise=0.08, Cnoise=2.0,
                                   force_mode=S.FORCE_GRADW),
+        # ~90 particles per cell: many rows per cell (rounds) and >2048 per block (segments)
+        "dense_cluster": dense_cluster(),
     }
+
+
+def dense_cluster():
+    sc = scenes.block_scene("dense", 32, (12, 12, 12), (18, 18, 18), scenes.FIXED_COROTATED, 16,
+                            vnoise=0.3, Fnoise=0.01, Cnoise=1.0)
+    rng = np.random.default_rng(16)
+    n = 20000
+    x = rng.uniform(12.0 / 32, 18.0 / 32, size=(n, 3)).astype(np.float32)
+    sc.x = x
+    sc.v = (rng.normal(size=(n, 3)) * 0.3).astype(np.float32)
+    sc.C = (rng.normal(size=(n, 3, 3)) * 1.0).astype(np.float32)
+    sc.F = (np.eye(3) + rng.normal(size=(n, 3, 3)) * 0.01).astype(np.float32)
+    return sc
 
 
 @pytest.mark.parametrize("name", list(small_scenes().keys()))
