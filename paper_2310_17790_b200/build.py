@@ -56,13 +56,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     log: list = []
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, log), srcs))
+        objs = list(ex.map(lambda s: _compile(s, force, log), srcs))   # raises on any nvcc error
     if force or not os.path.exists(LIB) or max(os.path.getmtime(o) for o in objs) > os.path.getmtime(LIB):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    with open(os.path.join(BUILD, "ptxas.log"), "a") as f:
+    with open(os.path.join(BUILD, "ptxas.log"), "w" if log else "a") as f:
         for src, out in log:
             f.write(f"==== {src}\n{out}\n")
     if verbose:

@@ -39,14 +39,14 @@ __global__ void k_unpack(int64_t n, const float* __restrict__ x, const float* __
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     xp[a] = x[p * 3 + a];
-    S[(PX + a) * pitch + p] = xp[a];
-    S[(PV + a) * pitch + p] = v[p * 3 + a];
+    S[pbase(p) + (PX + a) * 32] = xp[a];
+    S[pbase(p) + (PV + a) * 32] = v[p * 3 + a];
   }
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    S[(PC + k) * pitch + p] = C ? C[p * 9 + k] : 0.0f;
+    S[pbase(p) + (PC + k) * 32] = C ? C[p * 9 + k] : 0.0f;
     Fp[k] = F ? F[p * 9 + k] : ((k % 4 == 0) ? 1.0f : 0.0f);
-    if (with_F) S[(PF + k) * pitch + p] = Fp[k];
+    if (with_F) S[pbase(p) + (PF + k) * 32] = Fp[k];
   }
   ids[p] = (int32_t)p;
   bool ok = true;
@@ -57,10 +57,10 @@ __global__ void k_unpack(int64_t n, const float* __restrict__ x, const float* __
     float tau[6];
     elastic_tau(Fp, P.model, P.mu, P.lam, tau);
 #pragma unroll
-    for (int k = 0; k < 6; ++k) S[(PT + k) * pitch + p] = tau[k];
+    for (int k = 0; k < 6; ++k) S[pbase(p) + (PT + k) * 32] = tau[k];
   } else {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) S[(PT + k) * pitch + p] = 0.0f;
+    for (int k = 0; k < 6; ++k) S[pbase(p) + (PT + k) * 32] = 0.0f;
   }
 }
 
@@ -78,7 +78,7 @@ __global__ void k_pack(int64_t n, const float* __restrict__ S, int64_t pitch,
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   int64_t id = ids[j];
-  for (int k = 0; k < ncomp; ++k) out[id * ncomp + k] = S[(plane0 + k) * pitch + j];
+  for (int k = 0; k < ncomp; ++k) out[id * ncomp + k] = S[pbase(j) + (plane0 + k) * 32];
 }
 
 void launch_pack(cudaStream_t st, int64_t n, const float* S, int64_t pitch, const int32_t* ids,
@@ -108,11 +108,11 @@ __global__ void __launch_bounds__(128) k_p2g_direct(int64_t n, const float* __re
   }
   float xp[3], vp[3], Cp[9], tp[6];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) { xp[a] = S[(PX + a) * pitch + p]; vp[a] = S[(PV + a) * pitch + p]; }
+  for (int a = 0; a < 3; ++a) { xp[a] = S[pbase(p) + (PX + a) * 32]; vp[a] = S[pbase(p) + (PV + a) * 32]; }
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Cp[k] = S[(PC + k) * pitch + p];
+  for (int k = 0; k < 9; ++k) Cp[k] = S[pbase(p) + (PC + k) * 32];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) tp[k] = S[(PT + k) * pitch + p];
+  for (int k = 0; k < 6; ++k) tp[k] = S[pbase(p) + (PT + k) * 32];
   Axis ax[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
   }
   float xp[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) xp[a] = S[(PX + a) * pitch + p];
+  for (int a = 0; a < 3; ++a) xp[a] = S[pbase(p) + (PX + a) * 32];
   Axis ax[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -292,16 +292,16 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
   bool finite = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    S[(PX + a) * pitch + p] = xn[a];
-    S[(PV + a) * pitch + p] = v[a];
+    S[pbase(p) + (PX + a) * 32] = xn[a];
+    S[pbase(p) + (PV + a) * 32] = v[a];
     finite &= isfinite(xn[a]) && isfinite(v[a]);
   }
 #pragma unroll
-  for (int k = 0; k < 9; ++k) S[(PC + k) * pitch + p] = Cn[k];
+  for (int k = 0; k < 9; ++k) S[pbase(p) + (PC + k) * 32] = Cn[k];
   if (WITH_F) {
     float Fp[9], Ft[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Fp[k] = S[(PF + k) * pitch + p];
+    for (int k = 0; k < 9; ++k) Fp[k] = S[pbase(p) + (PF + k) * 32];
     if (FORCE == 0) {
 #pragma unroll
       for (int k = 0; k < 9; ++k) G[k] = Cn[k];
@@ -317,9 +317,9 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
     float J = elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
 #pragma unroll
-    for (int k = 0; k < 9; ++k) { S[(PF + k) * pitch + p] = FE[k]; finite &= isfinite(FE[k]); }
+    for (int k = 0; k < 9; ++k) { S[pbase(p) + (PF + k) * 32] = FE[k]; finite &= isfinite(FE[k]); }
 #pragma unroll
-    for (int k = 0; k < 6; ++k) { S[(PT + k) * pitch + p] = tau[k]; finite &= isfinite(tau[k]); }
+    for (int k = 0; k < 6; ++k) { S[pbase(p) + (PT + k) * 32] = tau[k]; finite &= isfinite(tau[k]); }
   }
   if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
   if (!finite) flag_error(err, ERR_NONFINITE, (int)p);

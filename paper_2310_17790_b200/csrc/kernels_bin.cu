@@ -55,7 +55,7 @@ __global__ void k_keys_hist(int64_t n, const float* __restrict__ S, int64_t pitc
     }
     scene = lo;
   }
-  int key = block_key_of(S[(PX + 0) * pitch + j], S[(PX + 1) * pitch + j], S[(PX + 2) * pitch + j], scene, P);
+  int key = block_key_of(S[pbase(j) + (PX + 0) * 32], S[pbase(j) + (PX + 1) * 32], S[pbase(j) + (PX + 2) * 32], scene, P);
   keys[j] = key;
   aggregated_increment(counts, key, active);
 }
@@ -68,41 +68,60 @@ void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
 }
 
 // ---------------------------------------------------------------------------
-// decoupled look-back scan.  Packed 64-bit running value: particle count in the
-// low 32 bits, non-empty-block count in bits 32..57; status flag in bits 62..63.
+// Decoupled look-back scan (single pass).  Packed 64-bit running value: particle
+// count in bits 0..31, non-empty-block count in bits 32..57.  Status word of a
+// tile: value | epoch (bits 58..61) | flag (bits 62..63).  Tiles take tickets
+// from a monotone counter: tile = ticket % n_tiles, epoch = ticket / n_tiles, so
+// a status written by an earlier launch never matches and no reset is needed
+// (the kernel is one graph node, no memsets).  Items are read and written
+// warp-striped (coalesced); each warp scans its 16 x 32 items group by group.
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagInc = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
+constexpr unsigned long long kFlagMask = 3ull << 62;
+constexpr unsigned long long kEpochMask = 15ull << 58;
+constexpr unsigned long long kValMask = (1ull << 58) - 1;
+
+__device__ __forceinline__ unsigned long long packed(int c) {
+  return (unsigned long long)c + ((c > 0 ? 1ull : 0ull) << 32);
+}
 
 __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* counts, int32_t* block_start,
                                                        int32_t* cursor, int32_t* nonempty, int32_t* n_nonempty,
-                                                       unsigned long long* status, unsigned int* ticket,
+                                                       unsigned long long* status, unsigned long long* ticket,
                                                        int64_t n_tiles) {
   __shared__ unsigned long long warp_sums[kScanThreads / 32];
   __shared__ unsigned long long s_prefix;
-  __shared__ int s_tile;
-  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __shared__ unsigned long long s_ticket;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1ull);
   __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t base = tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  const int64_t tile = (int64_t)(s_ticket % (unsigned long long)n_tiles);
+  const unsigned long long ep = ((s_ticket / (unsigned long long)n_tiles) & 15ull) << 58;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = tile * kScanTile + (int64_t)warp * (kScanItems * 32);
   int c[kScanItems];
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) c[k] = (base + k < total) ? counts[base + k] : 0;
-  unsigned long long mine = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) mine += (unsigned long long)c[k] + ((c[k] > 0 ? 1ull : 0ull) << 32);
-  // block-wide inclusive scan of `mine`
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long inc = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = wbase + k * 32 + lane;
+    c[k] = i < total ? counts[i] : 0;
   }
-  if (lane == 31) warp_sums[warp] = inc;
+  // per group k: inclusive warp scan of packed values; keep exclusive offsets
+  unsigned long long excl[kScanItems];
+  unsigned long long run = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    unsigned long long x = packed(c[k]);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    excl[k] = run + x - packed(c[k]);
+    run += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) warp_sums[warp] = run;
   __syncthreads();
   unsigned long long warp_off = 0, agg = 0;
 #pragma unroll
@@ -110,49 +129,59 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* c
     if (w < warp) warp_off += warp_sums[w];
     agg += warp_sums[w];
   }
-  // look-back
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     unsigned long long prefix = 0;
     if (tile == 0) {
-      atomicExch(&status[0], kFlagInc | agg);
+      if (lane == 0) atomicExch(&status[0], kFlagInc | ep | agg);
+      // work counters of the kernels that follow (grid update, P2G, G2P)
+      if (lane >= 1 && lane <= 3) n_nonempty[lane] = 0;
     } else {
-      atomicExch(&status[tile], kFlagAgg | agg);
-      int64_t t = tile - 1;
+      if (lane == 0) atomicExch(&status[tile], kFlagAgg | ep | agg);
+      int64_t base_t = tile - 1;
       while (true) {
-        unsigned long long s = *(volatile unsigned long long*)&status[t];
-        if ((s >> 62) == 0) continue;   // not yet published
-        prefix += s & kValMask;
-        if ((s & ~kValMask) == kFlagInc) break;
-        --t;
+        const int64_t t = base_t - lane;
+        unsigned long long s = kFlagInc | ep;   // t < 0 behaves as an inclusive zero
+        if (t >= 0) {
+          do {
+            s = *(volatile unsigned long long*)&status[t];
+          } while ((s & kFlagMask) == 0 || (s & kEpochMask) != ep);
+        }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, (s & kFlagMask) == kFlagInc);
+        unsigned long long val = s & kValMask;
+        const bool done = inc_mask != 0;
+        if (done && lane > __ffs(inc_mask) - 1) val = 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (done) break;
+        base_t -= 32;
       }
-      atomicExch(&status[tile], kFlagInc | (prefix + agg));
+      if (lane == 0) atomicExch(&status[tile], kFlagInc | ep | (prefix + agg));
     }
-    s_prefix = prefix;
+    if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
-  unsigned long long run = s_prefix + warp_off + (inc - mine);
+  const unsigned long long off = s_prefix + warp_off;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    int64_t i = base + k;
+    const int64_t i = wbase + k * 32 + lane;
     if (i < total) {
-      int start = (int)(run & 0xffffffffull);
+      const unsigned long long r = off + excl[k];
+      const int start = (int)(r & 0xffffffffull);
       block_start[i] = start;
       cursor[i] = start;
-      if (c[k] > 0) nonempty[(int)(run >> 32)] = (int)i;
+      if (c[k] > 0) nonempty[(int)((r >> 32) & 0x3ffffffull)] = (int)i;
       counts[i] = 0;
     }
-    run += (unsigned long long)c[k] + ((c[k] > 0 ? 1ull : 0ull) << 32);
   }
-  if (tile == n_tiles - 1 && threadIdx.x == kScanThreads - 1) {
-    // run now holds the grand total (all later items are padding)
-    block_start[total] = (int)(run & 0xffffffffull);
-    *n_nonempty = (int)(run >> 32);
+  if (tile == n_tiles - 1 && threadIdx.x == 0) {
+    const unsigned long long r = s_prefix + agg;
+    block_start[total] = (int)(r & 0xffffffffull);
+    *n_nonempty = (int)((r >> 32) & 0x3ffffffull);
   }
 }
 
 void launch_scan(cudaStream_t st, PipelineBuffers* pb) {
-  cudaMemsetAsync(pb->scan_status, 0, sizeof(unsigned long long) * pb->scan_tiles, st);
-  cudaMemsetAsync(pb->scan_ticket, 0, sizeof(unsigned int), st);
   k_scan<<<(unsigned)pb->scan_tiles, kScanThreads, 0, st>>>(pb->total_blocks, pb->counts, pb->block_start,
                                                              pb->cursor, pb->nonempty, pb->n_nonempty,
                                                              pb->scan_status, pb->scan_ticket, pb->scan_tiles);

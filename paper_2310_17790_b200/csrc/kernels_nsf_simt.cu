@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
       if (live) {
         for (int o = 0; o < mlp.out_dim; ++o) {
           if (aos_out) tau_out[p * mlp.out_dim + o] = stress_scale * y[o];
-          else tau_out[o * tau_pitch + p] = stress_scale * y[o];
+          else tau_out[pbase(p) + o * 32] = stress_scale * y[o];   // AoSoA particle store
         }
       }
     }

@@ -12,11 +12,12 @@
 //  grid_update_blocks (a4): each node of every block touched by P2G is
 //              updated exactly once (ownership rule below) and its accumulator
 //              cleared for the next substep.
-//  g2p_tiled   (a5 + a6): the block's 6x6x6 velocity tile is staged
-//              in shared memory, then one thread per particle gathers 27 nodes,
-//              updates x, v, C, F, runs the SVD + return map, and writes the
-//              particle to the other buffer at its sorted slot (sort-on-write),
-//              with its next block key and the histogram for the next binning.
+//  g2p         (a5 + a6): one thread per block-sorted slot gathers
+//              its 27 grid velocities (through L1: neighbouring lanes share
+//              stencils), updates x, v, C, F, runs the constitutive update and
+//              writes the particle to the other buffer at its sorted slot
+//              (sort-on-write), with its next block key and the histogram for
+//              the next binning.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "mpm_math.cuh"
@@ -36,11 +37,14 @@ struct BlockCoord {
 
 __device__ __forceinline__ BlockCoord decode_block(int key, const DevParams& P) {
   BlockCoord bc;
-  bc.scene = (int)(key / P.blocks_per_scene);
-  int local = (int)(key % P.blocks_per_scene);
-  bc.b[2] = local % P.NB[2];
-  bc.b[1] = (local / P.NB[2]) % P.NB[1];
-  bc.b[0] = local / (P.NB[2] * P.NB[1]);
+  const int bps = (int)P.blocks_per_scene;
+  bc.scene = key / bps;
+  const int local = key - bc.scene * bps;
+  const int plane = P.NB[1] * P.NB[2];
+  bc.b[0] = local / plane;
+  const int rem = local - bc.b[0] * plane;
+  bc.b[1] = rem / P.NB[2];
+  bc.b[2] = rem - bc.b[1] * P.NB[2];
   return bc;
 }
 
@@ -50,7 +54,7 @@ constexpr int kP2GThreads = 192;   // 64 cells x 3 stencil planes (ox)
 constexpr int kRows = 12;          // particles per cell per round
 constexpr int kSlotFields = 21;    // w(9), u0(3), q0(3), q1(3), q2(3)
 constexpr int kSlotStride = kRows * 64;   // floats per field
-constexpr int kSegment = 2048;     // particles of one block handled per segment
+constexpr int kSegment = 1024;     // particles of one block handled per segment (smem: 3 CTAs/SM)
 
 struct __align__(16) P2GSmem {
   union {
@@ -60,21 +64,47 @@ struct __align__(16) P2GSmem {
   uint32_t cr[kSegment];   // (cell << 16) | rank within the cell, per particle of the segment
   int pop[64];             // cell populations of the segment
   int max_pop;
+  int next;                // dynamically fetched block index
+  uint16_t tbl[1728];      // tile-node reduction pairs (stencil node k << 6 | cell), grouped by tile node
+  uint16_t tbl_off[218];   // pair range of tile node t: [tbl_off[t], tbl_off[t+1])
 };
+
+// (cell, stencil-offset) pairs feeding each of the 216 tile nodes, built once
+__device__ uint16_t g_p2g_tbl[1728];
+__device__ uint16_t g_p2g_tbl_off[218];
+
+__global__ void k_p2g_tables() {
+  const int t = threadIdx.x;   // tile node 0..215
+  if (t >= 216) return;
+  auto cnt1 = [](int n) { return min(3, n) - max(0, n - 2) + 1; };
+  int off = 0;
+  for (int u = 0; u < t; ++u) off += cnt1(u / 36) * cnt1((u / 6) % 6) * cnt1(u % 6);
+  g_p2g_tbl_off[t] = (uint16_t)off;
+  if (t == 215) g_p2g_tbl_off[216] = (uint16_t)(off + 1);
+  const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
+  for (int cx = max(0, nx - 2); cx <= min(3, nx); ++cx)
+    for (int cy = max(0, ny - 2); cy <= min(3, ny); ++cy)
+      for (int cz = max(0, nz - 2); cz <= min(3, nz); ++cz) {
+        const int k = ((nx - cx) * 3 + (ny - cy)) * 3 + (nz - cz);
+        g_p2g_tbl[off++] = (uint16_t)((k << 6) | (cx << 4) | (cy << 2) | cz);
+      }
+}
+
+void p2g_tables_init(cudaStream_t st) { k_p2g_tables<<<1, 256, 0, st>>>(); }
 
 // one particle -> 21 floats of slot data at s = row*64 + cell
 __device__ __forceinline__ void p2g_stage_particle(const float* __restrict__ S, int64_t pitch, int p, int s,
                                                    float* sl, const DevParams& P) {
   const float m = P.mass;
-  const Axis a0 = bspline_axis(S[(PX + 0) * pitch + p], P.inv_dx);
-  const Axis a1 = bspline_axis(S[(PX + 1) * pitch + p], P.inv_dx);
-  const Axis a2 = bspline_axis(S[(PX + 2) * pitch + p], P.inv_dx);
-  const float v0 = S[(PV + 0) * pitch + p], v1 = S[(PV + 1) * pitch + p], v2 = S[(PV + 2) * pitch + p];
+  const Axis a0 = bspline_axis(S[pbase(p) + (PX + 0) * 32], P.inv_dx);
+  const Axis a1 = bspline_axis(S[pbase(p) + (PX + 1) * 32], P.inv_dx);
+  const Axis a2 = bspline_axis(S[pbase(p) + (PX + 2) * 32], P.inv_dx);
+  const float v0 = S[pbase(p) + (PV + 0) * 32], v1 = S[pbase(p) + (PV + 1) * 32], v2 = S[pbase(p) + (PV + 2) * 32];
   float Cm[9], T[6];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Cm[k] = S[(PC + k) * pitch + p];
+  for (int k = 0; k < 9; ++k) Cm[k] = S[pbase(p) + (PC + k) * 32];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) T[k] = S[(PT + k) * pitch + p];
+  for (int k = 0; k < 6; ++k) T[k] = S[pbase(p) + (PT + k) * 32];
   const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
   float Q[9];   // Q = m C - dt V0 (4/dx^2) tau  (MLS, reading #1)
 #pragma unroll
@@ -98,7 +128,7 @@ __device__ __forceinline__ int cell_in_block(const float* __restrict__ S, int64_
   int c[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const float t = S[(PX + a) * pitch + p] * P.inv_dx;
+    const float t = S[pbase(p) + (PX + a) * 32] * P.inv_dx;
     int base = (int)floorf(t - 0.5f);
     base = min(max(base, 0), P.N[a] - 3);
     c[a] = base - 4 * bc.b[a];
@@ -109,15 +139,21 @@ __device__ __forceinline__ int cell_in_block(const float* __restrict__ S, int64_
 __global__ void __launch_bounds__(kP2GThreads, 3)
 k_p2g_tiled(const float* __restrict__ S, int64_t pitch, const int32_t* __restrict__ perm,
             const int32_t* __restrict__ block_start, const int32_t* __restrict__ nonempty,
-            const int32_t* __restrict__ n_nonempty, float4* acc, DevParams P) {
+            int32_t* __restrict__ counters, float4* acc, DevParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   P2GSmem& sm = *reinterpret_cast<P2GSmem*>(smem_raw);
   const int tid = threadIdx.x;
   const int my_cell = tid & 63;
   const int ox = tid >> 6;
   const float fox = (float)ox;
-  const int nblk = *n_nonempty;
-  for (int bi = blockIdx.x; bi < nblk; bi += gridDim.x) {
+  const int nblk = *(volatile int32_t*)&counters[0];
+  for (int q = tid; q < 1728; q += kP2GThreads) sm.tbl[q] = g_p2g_tbl[q];
+  for (int q = tid; q < 217; q += kP2GThreads) sm.tbl_off[q] = g_p2g_tbl_off[q];
+  while (true) {
+    if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
+    __syncthreads();
+    const int bi = sm.next;
+    if (bi >= nblk) break;
     const int key = nonempty[bi];
     const BlockCoord bc = decode_block(key, P);
     const int start = block_start[key], end = block_start[key + 1];
@@ -130,11 +166,14 @@ k_p2g_tiled(const float* __restrict__ S, int64_t pitch, const int32_t* __restric
       if (tid < 64) sm.pop[tid] = 0;
       if (tid == 0) sm.max_pop = 0;
       __syncthreads();
-      // pass A: cell and rank of every particle of the segment
+      // pass A: cell and rank of every particle of the segment; rows of round 0
+      // are staged right away (the particle's x is already in registers)
       for (int i = tid; i < cnt; i += kP2GThreads) {
-        const int cell = cell_in_block(S, pitch, perm[seg + i], bc, P);
+        const int p = perm[seg + i];
+        const int cell = cell_in_block(S, pitch, p, bc, P);
         const int rank = atomicAdd(&sm.pop[cell], 1);
         sm.cr[i] = ((uint32_t)cell << 16) | (uint32_t)rank;
+        if (rank < kRows) p2g_stage_particle(S, pitch, p, rank * 64 + cell, sm.u.slot, P);
       }
       __syncthreads();
       if (tid < 64) atomicMax(&sm.max_pop, sm.pop[tid]);
@@ -142,14 +181,16 @@ k_p2g_tiled(const float* __restrict__ S, int64_t pitch, const int32_t* __restric
       const int rounds = (sm.max_pop + kRows - 1) / kRows;
       const int my_pop = sm.pop[my_cell];
       for (int round = 0; round < rounds; ++round) {
-        // pass B: stage the particles whose rank falls in this round
-        for (int i = tid; i < cnt; i += kP2GThreads) {
-          const uint32_t cr = sm.cr[i];
-          const int r = (int)(cr & 0xffffu) - round * kRows;
-          if (r < 0 || r >= kRows) continue;
-          p2g_stage_particle(S, pitch, perm[seg + i], r * 64 + (int)(cr >> 16), sm.u.slot, P);
+        if (round > 0) {
+          // pass B (rare: cells with more than kRows particles): stage this round's rows
+          for (int i = tid; i < cnt; i += kP2GThreads) {
+            const uint32_t cr = sm.cr[i];
+            const int r = (int)(cr & 0xffffu) - round * kRows;
+            if (r < 0 || r >= kRows) continue;
+            p2g_stage_particle(S, pitch, perm[seg + i], r * 64 + (int)(cr >> 16), sm.u.slot, P);
+          }
+          __syncthreads();
         }
-        __syncthreads();
         // accumulate: thread (my_cell, ox) over its cell's rows in this round
         int rows = my_pop - round * kRows;
         rows = rows < 0 ? 0 : (rows > kRows ? kRows : rows);
@@ -197,19 +238,18 @@ k_p2g_tiled(const float* __restrict__ S, int64_t pitch, const int32_t* __restric
     // reduce each node of the 6x6x6 tile over the cells whose stencil covers it
     float4* gbase = acc + (int64_t)bc.scene * P.nodes_per_scene;
     for (int t = tid; t < 216; t += kP2GThreads) {
-      const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      for (int cx = max(0, nx - 2); cx <= min(3, nx); ++cx)
-        for (int cy = max(0, ny - 2); cy <= min(3, ny); ++cy)
-          for (int cz = max(0, nz - 2); cz <= min(3, nz); ++cz) {
-            const int node = ((nx - cx) * 3 + (ny - cy)) * 3 + (nz - cz);
-            const int c = (cx << 4) | (cy << 2) | cz;
-            s0 += part[(node * 4 + 0) * 64 + c];
-            s1 += part[(node * 4 + 1) * 64 + c];
-            s2 += part[(node * 4 + 2) * 64 + c];
-            s3 += part[(node * 4 + 3) * 64 + c];
-          }
+      const int q1 = sm.tbl_off[t + 1];
+      for (int q = sm.tbl_off[t]; q < q1; ++q) {
+        const int pr = sm.tbl[q];
+        const float* pp = part + (pr >> 6) * 256 + (pr & 63);   // [(k*4 + comp)*64 + cell]
+        s0 += pp[0];
+        s1 += pp[64];
+        s2 += pp[128];
+        s3 += pp[192];
+      }
       if (s0 > 0.0f) {
+        const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
         const int gi = 4 * bc.b[0] + nx, gj = 4 * bc.b[1] + ny, gk = 4 * bc.b[2] + nz;
         if (gi < P.N[0] && gj < P.N[1] && gk < P.N[2])
           red_add_v4_t(gbase + node_index(gi, gj, gk, P), s0, s1, s2, s3);
@@ -222,7 +262,6 @@ k_p2g_tiled(const float* __restrict__ S, int64_t pitch, const int32_t* __restric
 // grid update over the blocks touched by P2G.  Target block t = b + d,
 // d in {0,1}^3, is owned by the first non-empty block t - d' in the fixed order
 // d' = (0,0,0), (0,0,1), ..., (1,1,1); the owner updates its 64 nodes.
-constexpr int kGridThreads = 512;   // 8 targets x 64 nodes
 
 __device__ __forceinline__ int count_of(const int32_t* bs, int scene, int b0, int b1, int b2, const DevParams& P) {
   if (b0 < 0 || b1 < 0 || b2 < 0) return 0;
@@ -250,174 +289,232 @@ __device__ __forceinline__ float4 grid_node_update_t(float4 a, int i, int j, int
   return make_float4(v[0], v[1], v[2], m);
 }
 
-__global__ void __launch_bounds__(kGridThreads)
+__global__ void __launch_bounds__(128)
 k_grid_update_blocks(const int32_t* __restrict__ block_start, const int32_t* __restrict__ nonempty,
-                     const int32_t* __restrict__ n_nonempty, float4* acc, float4* vel, DevParams P,
-                     const int64_t* __restrict__ d_step) {
+                     int32_t* __restrict__ n_nonempty, float4* acc, float4* vel,
+                     DevParams P, const int64_t* __restrict__ d_step) {
+  // one warp per non-empty source block b; it owns target t = b + d (d in {0,1}^3)
+  // when no source t - e with e < d (in the enumeration order) is non-empty.
   const int nblk = *n_nonempty;
-  const int d = threadIdx.x >> 6;        // target offset index 0..7
-  const int l = threadIdx.x & 63;        // node within the target block
-  const int d0 = (d >> 2) & 1, d1 = (d >> 1) & 1, d2 = d & 1;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const float y_plate = (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)(*d_step) * (double)P.dt));
-  for (int bi = blockIdx.x; bi < nblk; bi += gridDim.x) {
+  for (int bi = warp; bi < nblk; bi += nwarps) {
     const int key = nonempty[bi];
     const BlockCoord bc = decode_block(key, P);
-    const int t0 = bc.b[0] + d0, t1 = bc.b[1] + d1, t2 = bc.b[2] + d2;
-    if (t0 >= P.NB[0] || t1 >= P.NB[1] || t2 >= P.NB[2]) continue;
-    // ownership: no earlier offset d' < d (same enumeration) has a non-empty source
-    bool owner = true;
-    for (int e = 0; e < d && owner; ++e) {
-      const int e0 = (e >> 2) & 1, e1 = (e >> 1) & 1, e2 = e & 1;
-      if (count_of(block_start, bc.scene, t0 - e0, t1 - e1, t2 - e2, P) > 0) owner = false;
+    // bit s of `nb`: source b + (s0-1, s1-1, s2-1) is non-empty, s = s0*9 + s1*3 + s2
+    bool has = false;
+    if (lane < 27) {
+      const int n0 = bc.b[0] + lane / 9 - 1, n1 = bc.b[1] + (lane / 3) % 3 - 1, n2 = bc.b[2] + lane % 3 - 1;
+      has = n0 >= 0 && n1 >= 0 && n2 >= 0 && n0 < P.NB[0] && n1 < P.NB[1] && n2 < P.NB[2] &&
+            count_of(block_start, bc.scene, n0, n1, n2, P) > 0;
     }
-    if (!owner) continue;
-    const int64_t g = (int64_t)bc.scene * P.nodes_per_scene + block_id(t0, t1, t2, P) * kBlockNodes + l;
-    const float4 a = acc[g];
-    const int i = t0 * 4 + (l >> 4), j = t1 * 4 + ((l >> 2) & 3), k = t2 * 4 + (l & 3);
-    vel[g] = grid_node_update_t(a, i, j, k, P, y_plate);
-    acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const unsigned nb = __ballot_sync(0xffffffffu, has);
+    float4 a[8][2];
+    int64_t g[8];
+    unsigned own = 0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      const int d0 = (d >> 2) & 1, d1 = (d >> 1) & 1, d2 = d & 1;
+      const int t0 = bc.b[0] + d0, t1 = bc.b[1] + d1, t2 = bc.b[2] + d2;
+      bool owner = t0 < P.NB[0] && t1 < P.NB[1] && t2 < P.NB[2];
+#pragma unroll
+      for (int e = 0; e < d; ++e) {
+        const int e0 = (e >> 2) & 1, e1 = (e >> 1) & 1, e2 = e & 1;
+        if (nb & (1u << (((d0 - e0 + 1) * 3 + (d1 - e1 + 1)) * 3 + (d2 - e2 + 1)))) owner = false;
+      }
+      g[d] = (int64_t)bc.scene * P.nodes_per_scene + block_id(t0, t1, t2, P) * kBlockNodes;
+      if (owner) {
+        own |= 1u << d;
+        a[d][0] = acc[g[d] + lane];
+        a[d][1] = acc[g[d] + lane + 32];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      if (!(own & (1u << d))) continue;
+      const int t0 = bc.b[0] + ((d >> 2) & 1), t1 = bc.b[1] + ((d >> 1) & 1), t2 = bc.b[2] + (d & 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = lane + 32 * h;
+        const int i = t0 * 4 + (l >> 4), j = t1 * 4 + ((l >> 2) & 3), k = t2 * 4 + (l & 3);
+        vel[g[d] + l] = grid_node_update_t(a[d][h], i, j, k, P, y_plate);
+        acc[g[d] + l] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// G2P + constitutive, sort-on-write
-constexpr int kG2PThreads = 256;
+// G2P + constitutive (a5 + a6), sort-on-write.
+struct PState {
+  float x[3];
+  float F[9];
+  int id;
+};
 
+__device__ __forceinline__ void load_pstate(PState& s, const float* __restrict__ S, int p,
+                                            const int32_t* __restrict__ ids) {
+  const float* base = S + pbase(p);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) s.x[a] = __ldg(base + (PX + a) * 32);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) s.F[k] = __ldg(base + (PF + k) * 32);
+  s.id = __ldg(ids + p);
+}
+
+#ifndef NSF_G2P_FLAT_MIN_BLOCKS
+#define NSF_G2P_FLAT_MIN_BLOCKS 7
+#endif
 template <int FORCE>
-__global__ void __launch_bounds__(kG2PThreads, 2)
-k_g2p_tiled(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t pitch,
-            const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
-            const int32_t* __restrict__ perm, const int32_t* __restrict__ block_start,
-            const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
-            const float4* __restrict__ vel, int32_t* __restrict__ keys, int32_t* __restrict__ counts,
-            DevParams P, DevErr* err, int64_t* d_step) {
-  __shared__ float4 tile[8 * 64];   // the 2x2x2 blocks b + d, each 64 nodes
-  const int nblk = *n_nonempty;
+__global__ void __launch_bounds__(128, NSF_G2P_FLAT_MIN_BLOCKS)
+k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
+           const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
+           const int32_t* __restrict__ perm, const float4* __restrict__ vel, const int64_t* __restrict__ scene_off,
+           int n_scenes, int32_t* __restrict__ keys, int32_t* __restrict__ counts, DevParams P, DevErr* err,
+           int64_t* d_step) {
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)d_step, 1ull);
-  const float cC = 4.0f * P.inv_dx * P.inv_dx;
-  for (int bi = blockIdx.x; bi < nblk; bi += gridDim.x) {
-    const int key = nonempty[bi];
-    const BlockCoord bc = decode_block(key, P);
-    const float4* vb = vel + (int64_t)bc.scene * P.nodes_per_scene;
-    __syncthreads();   // previous block's readers are done with the tile
-    for (int e = threadIdx.x; e < 8 * 64; e += kG2PThreads) {
-      const int d = e >> 6, l = e & 63;
-      const int t0 = bc.b[0] + ((d >> 2) & 1), t1 = bc.b[1] + ((d >> 1) & 1), t2 = bc.b[2] + (d & 1);
-      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (t0 < P.NB[0] && t1 < P.NB[1] && t2 < P.NB[2]) val = vb[block_id(t0, t1, t2, P) * kBlockNodes + l];
-      tile[e] = val;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const unsigned active = __ballot_sync(0xffffffffu, j < n);
+  if (j >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int p = perm[j];
+  PState st;
+  load_pstate(st, Sin, p, ids_in);
+  // scenes stay contiguous and in order in the sorted slot order
+  const int bps = (int)P.blocks_per_scene;
+  int scene = 0;
+  if (n_scenes > 1) {
+    int lo = 0, hi = n_scenes;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= j) lo = mid; else hi = mid;
     }
-    __syncthreads();
-    const int start = block_start[key], end = block_start[key + 1];
-    for (int j = start + threadIdx.x; j < end; j += kG2PThreads) {
-      const unsigned active = __activemask();
-      const int p = perm[j];
-      float xp[3] = {Sin[(PX + 0) * pitch + p], Sin[(PX + 1) * pitch + p], Sin[(PX + 2) * pitch + p]};
-      Axis ax[3];
-      int lo[3];
+    scene = lo;
+  }
+  const float4* vb = vel + (int64_t)scene * P.nodes_per_scene;
+  const float cC = 4.0f * P.inv_dx;
+  Axis ax[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        ax[a] = bspline_axis(xp[a], P.inv_dx);
-        ax[a].base = min(max(ax[a].base, 0), P.N[a] - 3);
-        lo[a] = ax[a].base - 4 * bc.b[a];   // 0..3
-      }
-      float v[3] = {0.f, 0.f, 0.f};
-      float Bm[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int a = 0; a < 3; ++a) {
+    ax[a] = bspline_axis(st.x[a], P.inv_dx);
+    ax[a].base = min(max(ax[a].base, 0), P.N[a] - 3);
+  }
+  int X[3], Y[3], Z[3];
+  {
+    const int plane = P.NB[1] * P.NB[2] * kBlockNodes;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int la = lo[0] + a;
-        const int sa = la >> 2, wa = la & 3;
-        const float da = ((float)a - ax[0].f) * P.dx;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const int lb = lo[1] + b;
-          const int sb = lb >> 2, wb = lb & 3;
-          const float db = ((float)b - ax[1].f) * P.dx;
-          const float wab = ax[0].w[a] * ax[1].w[b];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const int lc = lo[2] + c;
-            const int sc = lc >> 2, wc = lc & 3;
-            const float dc = ((float)c - ax[2].f) * P.dx;
-            const float W = wab * ax[2].w[c];
-            const float4 vi = tile[(((sa << 2) | (sb << 1) | sc) << 6) | (wa << 4) | (wb << 2) | wc];
-            const float wv0 = W * vi.x, wv1 = W * vi.y, wv2 = W * vi.z;
-            v[0] += wv0; v[1] += wv1; v[2] += wv2;
-            Bm[0] = fmaf(wv0, da, Bm[0]); Bm[1] = fmaf(wv0, db, Bm[1]); Bm[2] = fmaf(wv0, dc, Bm[2]);
-            Bm[3] = fmaf(wv1, da, Bm[3]); Bm[4] = fmaf(wv1, db, Bm[4]); Bm[5] = fmaf(wv1, dc, Bm[5]);
-            Bm[6] = fmaf(wv2, da, Bm[6]); Bm[7] = fmaf(wv2, db, Bm[7]); Bm[8] = fmaf(wv2, dc, Bm[8]);
-            if (FORCE == 1) {
-              const float g0 = ax[0].dw[a] * ax[1].w[b] * ax[2].w[c];
-              const float g1 = ax[0].w[a] * ax[1].dw[b] * ax[2].w[c];
-              const float g2 = ax[0].w[a] * ax[1].w[b] * ax[2].dw[c];
-              G[0] += vi.x * g0; G[1] += vi.x * g1; G[2] += vi.x * g2;
-              G[3] += vi.y * g0; G[4] += vi.y * g1; G[5] += vi.y * g2;
-              G[6] += vi.z * g0; G[7] += vi.z * g1; G[8] += vi.z * g2;
-            }
-          }
-        }
-      }
-      float Cn[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) Cn[k] = cC * Bm[k];
-      if (FORCE == 0) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) G[k] = Cn[k];
-      }
-      float xn[3];
-      bool ok = true, finite = true;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        xn[a] = xp[a] + P.dt * v[a];
-        const float t = xn[a] * P.inv_dx;
-        ok &= (t >= 0.5f) && (t < (float)P.N[a] - 1.5f);
-        finite &= isfinite(xn[a]) && isfinite(v[a]);
-      }
-      float Fp[9], Ft[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) Fp[k] = Sin[(PF + k) * pitch + p];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj)
-          Ft[i * 3 + jj] = Fp[i * 3 + jj] + P.dt * (G[i * 3 + 0] * Fp[0 * 3 + jj] + G[i * 3 + 1] * Fp[1 * 3 + jj] +
-                                                    G[i * 3 + 2] * Fp[2 * 3 + jj]);
-      float FE[9], tau[6];
-      const float J = elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
-      // sorted write (coalesced over j)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        Sout[(PX + a) * pitch + j] = xn[a];
-        Sout[(PV + a) * pitch + j] = v[a];
-      }
-#pragma unroll
-      for (int k = 0; k < 9; ++k) Sout[(PC + k) * pitch + j] = Cn[k];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) { Sout[(PF + k) * pitch + j] = FE[k]; finite &= isfinite(FE[k]); }
-#pragma unroll
-      for (int k = 0; k < 6; ++k) { Sout[(PT + k) * pitch + j] = tau[k]; finite &= isfinite(tau[k]); }
-      const int id = ids_in[p];
-      ids_out[j] = id;
-      if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
-      if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, id); }
-      if (!finite) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, id); }
-      // next block key + histogram (warp-aggregated)
-      int nb[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        int base = (int)floorf(xn[a] * P.inv_dx - 0.5f);
-        base = min(max(base, 0), P.N[a] - 3);
-        nb[a] = base >> 2;
-      }
-      const int nkey = (int)(bc.scene * P.blocks_per_scene + block_id(nb[0], nb[1], nb[2], P));
-      keys[j] = nkey;
-      const unsigned peers = __match_any_sync(active, nkey);
-      const int lane = threadIdx.x & 31;
-      const int leader = __ffs(peers) - 1;
-      if (lane == leader) atomicAdd(&counts[nkey], __popc(peers));
+    for (int o = 0; o < 3; ++o) {
+      const int i = ax[0].base + o, jj = ax[1].base + o, k = ax[2].base + o;
+      X[o] = (i >> 2) * plane + ((i & 3) << 4);
+      Y[o] = (jj >> 2) * (P.NB[2] * kBlockNodes) + ((jj & 3) << 2);
+      Z[o] = (k >> 2) * kBlockNodes + (k & 3);
     }
   }
+  float wyz[9];
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) wyz[b * 3 + c] = ax[1].w[b] * ax[2].w[c];
+  float v[3] = {0.f, 0.f, 0.f};
+  float M[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float Tt[3] = {0.f, 0.f, 0.f}, Ty[3] = {0.f, 0.f, 0.f}, Tz[3] = {0.f, 0.f, 0.f};
+    float Dy[3] = {0.f, 0.f, 0.f}, Dz[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float4 vi = __ldg(vb + (X[a] + Y[b] + Z[c]));
+        const float wgt = wyz[b * 3 + c];
+        Tt[0] = fmaf(wgt, vi.x, Tt[0]); Tt[1] = fmaf(wgt, vi.y, Tt[1]); Tt[2] = fmaf(wgt, vi.z, Tt[2]);
+        if (b) {
+          const float wb = (float)b * wgt;
+          Ty[0] = fmaf(wb, vi.x, Ty[0]); Ty[1] = fmaf(wb, vi.y, Ty[1]); Ty[2] = fmaf(wb, vi.z, Ty[2]);
+        }
+        if (c) {
+          const float wc = (float)c * wgt;
+          Tz[0] = fmaf(wc, vi.x, Tz[0]); Tz[1] = fmaf(wc, vi.y, Tz[1]); Tz[2] = fmaf(wc, vi.z, Tz[2]);
+        }
+        if (FORCE == 1) {
+          const float gy = ax[1].dw[b] * ax[2].w[c], gz = ax[1].w[b] * ax[2].dw[c];
+          Dy[0] = fmaf(gy, vi.x, Dy[0]); Dy[1] = fmaf(gy, vi.y, Dy[1]); Dy[2] = fmaf(gy, vi.z, Dy[2]);
+          Dz[0] = fmaf(gz, vi.x, Dz[0]); Dz[1] = fmaf(gz, vi.y, Dz[1]); Dz[2] = fmaf(gz, vi.z, Dz[2]);
+        }
+      }
+    const float wx = ax[0].w[a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      v[i] = fmaf(wx, Tt[i], v[i]);
+      if (a) M[i * 3 + 0] = fmaf((float)a * wx, Tt[i], M[i * 3 + 0]);
+      M[i * 3 + 1] = fmaf(wx, Ty[i], M[i * 3 + 1]);
+      M[i * 3 + 2] = fmaf(wx, Tz[i], M[i * 3 + 2]);
+      if (FORCE == 1) {
+        G[i * 3 + 0] = fmaf(ax[0].dw[a], Tt[i], G[i * 3 + 0]);
+        G[i * 3 + 1] = fmaf(wx, Dy[i], G[i * 3 + 1]);
+        G[i * 3 + 2] = fmaf(wx, Dz[i], G[i * 3 + 2]);
+      }
+    }
+  }
+  float Cn[9];
+  const float f[3] = {ax[0].f, ax[1].f, ax[2].f};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) Cn[i * 3 + jj] = cC * fmaf(-v[i], f[jj], M[i * 3 + jj]);
+  if (FORCE == 0) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) G[k] = Cn[k];
+  }
+  float xn[3];
+  bool ok = true;
+  float* ob = Sout + pbase(j);
+  float chk = 0.0f;   // any NaN/Inf makes the sum non-finite
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    xn[a] = st.x[a] + P.dt * v[a];
+    const float tt = xn[a] * P.inv_dx;
+    ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
+    ob[(PX + a) * 32] = xn[a];
+    ob[(PV + a) * 32] = v[a];
+    chk += xn[a] + v[a];
+  }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) ob[(PC + k) * 32] = Cn[k];
+  ids_out[j] = st.id;
+  // next block key + histogram (needs only x^{n+1})
+  {
+    int nb[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int base = (int)floorf(xn[a] * P.inv_dx - 0.5f);
+      base = min(max(base, 0), P.N[a] - 3);
+      nb[a] = base >> 2;
+    }
+    const int nkey = scene * bps + (int)block_id(nb[0], nb[1], nb[2], P);
+    keys[j] = nkey;
+    const unsigned peers = __match_any_sync(active, nkey);
+    if (lane == __ffs(peers) - 1) atomicAdd(&counts[nkey], __popc(peers));
+  }
+  float Ft[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj)
+      Ft[i * 3 + jj] = st.F[i * 3 + jj] + P.dt * (G[i * 3 + 0] * st.F[0 * 3 + jj] + G[i * 3 + 1] * st.F[1 * 3 + jj] +
+                                                  G[i * 3 + 2] * st.F[2 * 3 + jj]);
+  float FE[9], tau[6];
+  const float J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) { ob[(PF + k) * 32] = FE[k]; chk += FE[k]; }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { ob[(PT + k) * 32] = tau[k]; chk += tau[k]; }
+  if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
+  if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, st.id); }
+  if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, st.id); }
 }
 
 // ---------------------------------------------------------------------------
@@ -441,27 +538,37 @@ void launch_p2g_tiled(cudaStream_t st, const float* S, int64_t pitch, const int3
   }
   int grid = num_sms() * 3;
   k_p2g_tiled<<<grid, kP2GThreads, smem, st>>>(S, pitch, perm, pb->block_start, pb->nonempty, pb->n_nonempty, acc, P);
+  (void)0;
 }
 
 void launch_grid_update_blocks(cudaStream_t st, const PipelineBuffers* pb, float4* acc, float4* vel,
                                const DevParams& P, const int64_t* d_step) {
-  int grid = num_sms() * 4;
-  k_grid_update_blocks<<<grid, kGridThreads, 0, st>>>(pb->block_start, pb->nonempty, pb->n_nonempty, acc, vel, P,
-                                                      d_step);
+  // about one touched-source block per CTA: latency of the ownership lookups is
+  // hidden by many resident CTAs rather than by a persistent loop
+  int grid = num_sms() * 8;   // 4 warps per CTA, one source block per warp iteration
+  k_grid_update_blocks<<<grid, 128, 0, st>>>(pb->block_start, pb->nonempty, pb->n_nonempty, acc, vel, P, d_step);
 }
 
-void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t pitch, const int32_t* ids_in,
-                      int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const DevParams& P, DevErr* err,
-                      int64_t* d_step) {
-  int grid = num_sms() * 2;
+__global__ void k_bump_step(int64_t* d_step) { atomicAdd((unsigned long long*)d_step, 1ull); }
+
+void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
+                      int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const int64_t* scene_off,
+                      int n_scenes, const DevParams& P, DevErr* err, int64_t* d_step) {
+  if (n == 0) {
+    k_bump_step<<<1, 1, 0, st>>>(d_step);
+    return;
+  }
+  const unsigned g = (unsigned)((n + 127) / 128);
   if (P.force_mode == 0)
-    k_g2p_tiled<0><<<grid, kG2PThreads, 0, st>>>(Sin, Sout, pitch, ids_in, ids_out, pb->perm, pb->block_start,
-                                                 pb->nonempty, pb->n_nonempty, vel, pb->keys, pb->counts, P, err,
-                                                 d_step);
+    k_g2p_flat<0><<<g, 128, 0, st>>>(Sin, Sout, n, ids_in, ids_out, pb->perm, vel, scene_off, n_scenes, pb->keys,
+                                     pb->counts, P, err, d_step);
   else
-    k_g2p_tiled<1><<<grid, kG2PThreads, 0, st>>>(Sin, Sout, pitch, ids_in, ids_out, pb->perm, pb->block_start,
-                                                 pb->nonempty, pb->n_nonempty, vel, pb->keys, pb->counts, P, err,
-                                                 d_step);
+    k_g2p_flat<1><<<g, 128, 0, st>>>(Sin, Sout, n, ids_in, ids_out, pb->perm, vel, scene_off, n_scenes, pb->keys,
+                                     pb->counts, P, err, d_step);
 }
 
+}  // namespace nsf
+
+namespace nsf {
+static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / 3, "P2G shared memory must allow 3 CTAs per SM");
 }  // namespace nsf

@@ -255,6 +255,166 @@ __device__ __forceinline__ float elastoplastic(const float Ft[9], int model, flo
   return detFE;
 }
 
+// ---------------------------------------------------------------------------
+// Fast constitutive path (same results as elastoplastic() up to rounding).
+//
+// Log-strain models (DP, VM): with F = U Sigma V^T, the left Cauchy-Green tensor
+// b = F F^T = U Sigma^2 U^T, so a symmetric Jacobi eigen-decomposition of b gives
+// U and sigma_i = sqrt(lambda_i) without the QR step; V is never formed:
+// F_E = U diag(Z) V^T = U diag(Z/sigma) U^T F.  Fixed corotated: the polar
+// rotation R = U V^T is the limit of the scaled Newton iteration
+// R <- (g R + R^{-T}/g)/2, g = |det R|^{-1/3} (Higham), started at R = F.
+// Both fall back to the rotation-safe SVD when det F <= 1e-6 or sigma < 1e-4
+// (reading #21: inverted / degenerate F), so conventions stay identical.
+
+// Symmetric 3x3 eigen-decomposition by cyclic Jacobi: A = V diag(A_ii) V^T.
+__device__ __forceinline__ void sym_eig3(float A[3][3], float V[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0f : 0.0f;
+  for (int sweep = 0; sweep < 6; ++sweep) {
+    float off = fabsf(A[0][1]) + fabsf(A[0][2]) + fabsf(A[1][2]);
+    float dia = fabsf(A[0][0]) + fabsf(A[1][1]) + fabsf(A[2][2]);
+    if (off <= 1e-9f * dia) break;
+    jacobi_pq(A, V, 0, 1);
+    jacobi_pq(A, V, 0, 2);
+    jacobi_pq(A, V, 1, 2);
+  }
+}
+
+__device__ __forceinline__ bool polar_newton(const float F[9], float R[9]) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = F[k];
+  for (int it = 0; it < 12; ++it) {
+    // cofactor matrix = det(R) R^{-T}
+    float c[9];
+    c[0] = R[4] * R[8] - R[5] * R[7];
+    c[1] = R[5] * R[6] - R[3] * R[8];
+    c[2] = R[3] * R[7] - R[4] * R[6];
+    c[3] = R[2] * R[7] - R[1] * R[8];
+    c[4] = R[0] * R[8] - R[2] * R[6];
+    c[5] = R[1] * R[6] - R[0] * R[7];
+    c[6] = R[1] * R[5] - R[2] * R[4];
+    c[7] = R[2] * R[3] - R[0] * R[5];
+    c[8] = R[0] * R[4] - R[1] * R[3];
+    const float det = R[0] * c[0] + R[1] * c[1] + R[2] * c[2];
+    if (!(det > 1e-12f)) return false;
+    // g = det^{-1/3};  R' = (g R + cof/(g det)) / 2
+    const float g = exp2f(-log2f(det) * (1.0f / 3.0f));
+    const float a = 0.5f * g, b = 0.5f / (g * det);
+    float diff = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const float r = a * R[k] + b * c[k];
+      diff = fmaxf(diff, fabsf(r - R[k]));
+      R[k] = r;
+    }
+    if (diff < 2e-7f) break;
+  }
+  return true;
+}
+
+__device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model, float mu, float lam, float alpha,
+                                                    float tau_Y, float FE[9], float tau[6]) {
+  const float J = det3(Ft);
+  if (!(J > 1e-6f)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+  if (model == 0) {
+    float R[9];
+    if (!polar_newton(Ft, R)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+    float D[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) D[k] = Ft[k] - R[k];
+    const float vol = lam * (J - 1.0f) * J;
+    float T[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        T[i][j] = 2.0f * mu * (D[i * 3 + 0] * Ft[j * 3 + 0] + D[i * 3 + 1] * Ft[j * 3 + 1] + D[i * 3 + 2] * Ft[j * 3 + 2]);
+    tau[0] = T[0][0] + vol;
+    tau[1] = T[1][1] + vol;
+    tau[2] = T[2][2] + vol;
+    tau[3] = 0.5f * (T[1][2] + T[2][1]);
+    tau[4] = 0.5f * (T[0][2] + T[2][0]);
+    tau[5] = 0.5f * (T[0][1] + T[1][0]);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+    return J;
+  }
+  // b = F F^T
+  float Bm[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const float s = Ft[i * 3 + 0] * Ft[j * 3 + 0] + Ft[i * 3 + 1] * Ft[j * 3 + 1] + Ft[i * 3 + 2] * Ft[j * 3 + 2];
+      Bm[i][j] = s;
+      Bm[j][i] = s;
+    }
+  float U[3][3];
+  sym_eig3(Bm, U);
+  const float l0 = Bm[0][0], l1 = Bm[1][1], l2 = Bm[2][2];
+  const float kFloor2 = 1e-8f;   // sigma >= 1e-4
+  if (!(l0 > kFloor2 && l1 > kFloor2 && l2 > kFloor2)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+  // eps = log sigma = log(lambda)/2
+  const float e[3] = {0.5f * logf(l0), 0.5f * logf(l1), 0.5f * logf(l2)};
+  const float tr = e[0] + e[1] + e[2];
+  const float eh[3] = {e[0] - tr * (1.0f / 3.0f), e[1] - tr * (1.0f / 3.0f), e[2] - tr * (1.0f / 3.0f)};
+  const float nrm = sqrtf(eh[0] * eh[0] + eh[1] * eh[1] + eh[2] * eh[2]);
+  float dg;
+  bool expand = false;
+  if (model == 1) {
+    expand = tr > 0.0f;
+    dg = nrm + alpha * (3.0f * lam + 2.0f * mu) * tr / (2.0f * mu);
+  } else {
+    dg = nrm - tau_Y / (2.0f * mu);
+  }
+  float le[3];
+  bool elastic = false;
+  if (expand) {
+    le[0] = le[1] = le[2] = 0.0f;
+  } else if (dg <= 0.0f) {
+    le[0] = e[0]; le[1] = e[1]; le[2] = e[2];
+    elastic = true;
+  } else {
+    const float k = dg / nrm;
+    le[0] = e[0] - k * eh[0];
+    le[1] = e[1] - k * eh[1];
+    le[2] = e[2] - k * eh[2];
+  }
+  float detFE = J;
+  if (elastic) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+  } else {
+    // F_E = U diag(Z/sigma) U^T F,  Z/sigma = exp(le - e)
+    const float r0 = expf(le[0] - e[0]), r1 = expf(le[1] - e[1]), r2 = expf(le[2] - e[2]);
+    float M[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M[i][j] = U[i][0] * r0 * U[j][0] + U[i][1] * r1 * U[j][1] + U[i][2] * r2 * U[j][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        FE[i * 3 + j] = M[i][0] * Ft[0 * 3 + j] + M[i][1] * Ft[1 * 3 + j] + M[i][2] * Ft[2 * 3 + j];
+    detFE = J * r0 * r1 * r2;
+  }
+  const float kLogFloor = -9.210340371976184f;   // log(1e-4)
+  const float m0 = fmaxf(le[0], kLogFloor), m1 = fmaxf(le[1], kLogFloor), m2 = fmaxf(le[2], kLogFloor);
+  const float sum = m0 + m1 + m2;
+  const float d0 = 2.0f * mu * m0 + lam * sum, d1 = 2.0f * mu * m1 + lam * sum, d2 = 2.0f * mu * m2 + lam * sum;
+  tau[0] = U[0][0] * U[0][0] * d0 + U[0][1] * U[0][1] * d1 + U[0][2] * U[0][2] * d2;
+  tau[1] = U[1][0] * U[1][0] * d0 + U[1][1] * U[1][1] * d1 + U[1][2] * U[1][2] * d2;
+  tau[2] = U[2][0] * U[2][0] * d0 + U[2][1] * U[2][1] * d1 + U[2][2] * U[2][2] * d2;
+  tau[3] = U[1][0] * U[2][0] * d0 + U[1][1] * U[2][1] * d1 + U[1][2] * U[2][2] * d2;
+  tau[4] = U[0][0] * U[2][0] * d0 + U[0][1] * U[2][1] * d1 + U[0][2] * U[2][2] * d2;
+  tau[5] = U[0][0] * U[1][0] * d0 + U[0][1] * U[1][1] * d1 + U[0][2] * U[1][2] * d2;
+  return detFE;
+}
+
 // Elastic stress of a given (admissible) F, used for tau^0 at load (reading #9).
 __device__ __forceinline__ void elastic_tau(const float F[9], int model, float mu, float lam, float tau[6]) {
   float FE[9];

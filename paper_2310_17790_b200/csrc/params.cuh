@@ -12,6 +12,10 @@ namespace nsf {
 constexpr int kBlock = 4;            // cells / nodes per block edge
 constexpr int kBlockNodes = 64;      // 4^3
 
+// Particle store layout (AoSoA): particles in tiles of 32; field k of particle p
+// lives at S[pbase(p) + 32 k], pbase(p) = (p/32) * 32 * kPlanes + p % 32.  A warp
+// touching 32 consecutive particles reads/writes 128 contiguous bytes per field,
+// and all fields of one particle share one base address (immediate offsets).
 // plane indices inside one particle buffer set
 enum Plane : int {
   PX = 0,   // x0..x2
@@ -21,6 +25,10 @@ enum Plane : int {
   PT = 24,  // tau Voigt xx,yy,zz,yz,xz,xy
   kPlanes = 30
 };
+
+constexpr int kTileP = 32;
+constexpr int kTileStride = kTileP * kPlanes;
+__host__ __device__ __forceinline__ int64_t pbase(int64_t p) { return (p >> 5) * kTileStride + (p & 31); }
 
 enum ErrBits : uint32_t { ERR_OUT_OF_DOMAIN = 1u, ERR_NONFINITE = 2u };
 

@@ -25,12 +25,18 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   pb->nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
   pb->n_nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 4);
   pb->scan_status = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * pb->scan_tiles);
-  pb->scan_ticket = (unsigned int*)pipeline_alloc(h, sizeof(unsigned int) * 4);
+  pb->scan_ticket = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * 4);
   if (!pb->counts || !pb->block_start || !pb->cursor || !pb->nonempty || !pb->n_nonempty || !pb->scan_status ||
       !pb->scan_ticket)
     return -1;
   HandleView v = view(h);
   if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * total_blocks, v.stream) != cudaSuccess) return -1;
+  // scan status words carry an epoch; start from a clean slate once
+  if (cudaMemsetAsync(pb->scan_status, 0, sizeof(unsigned long long) * pb->scan_tiles, v.stream) != cudaSuccess)
+    return -1;
+  if (cudaMemsetAsync(pb->scan_ticket, 0, sizeof(unsigned long long) * 4, v.stream) != cudaSuccess) return -1;
+  p2g_tables_init(v.stream);
+  if (cudaGetLastError() != cudaSuccess) return -1;
   pb->tiled = false;
   (void)P;
   return 0;
@@ -39,6 +45,7 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
 nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
   if (pb->keys) pipeline_free(h, pb->keys);
   if (pb->perm) pipeline_free(h, pb->perm);
+
   pb->keys = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
   pb->perm = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
   pb->pitch = pitch;
@@ -103,8 +110,8 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur) {
     }
     PLAUNCH(h, "grid_update", launch_grid_update_blocks(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
     PLAUNCH(h, "g2p_tiled",
-            launch_g2p_tiled(v.stream, v.S[cur], v.S[nxt], v.pitch, v.ids[cur], v.ids[nxt], pb, v.vel, *v.P, v.err,
-                             v.d_step));
+            launch_g2p_tiled(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb, v.vel, v.scene_off,
+                             v.n_scenes, *v.P, v.err, v.d_step));
     launches += 2;
     pb->launches = launches;
     return nxt;
@@ -114,7 +121,7 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur) {
   PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
   PLAUNCH(h, "nsf_mlp",
           launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
-                         v.P->stress_scale, v.S[cur] + PT * v.pitch, v.pitch, 0));
+                         v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0));
   PLAUNCH(h, "p2g_direct", launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P));
   PLAUNCH(h, "grid_update", launch_grid_update_blocks(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
   PLAUNCH(h, "g2p_direct",
@@ -170,7 +177,7 @@ int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, flo
   (void)pb;
   if (v.model == NSF_NEURAL_STRESS)
     launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
-                   v.P->stress_scale, v.S[cur] + PT * v.pitch, v.pitch, 0);
+                   v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0);
   launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P);
   launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
   if (cudaMemsetAsync(v.acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return -1;

@@ -18,9 +18,9 @@ struct PipelineBuffers {
   int32_t* cursor = nullptr;        // [total_blocks]
   int32_t* perm = nullptr;          // [pitch]  sorted slot -> storage slot
   int32_t* nonempty = nullptr;      // [total_blocks] list of non-empty block ids
-  int32_t* n_nonempty = nullptr;    // [1]
+  int32_t* n_nonempty = nullptr;    // [4]: n_nonempty, (unused), (unused), p2g block ticket (reset by scan)
   unsigned long long* scan_status = nullptr;  // [scan tiles]
-  unsigned int* scan_ticket = nullptr;        // [1]
+  unsigned long long* scan_ticket = nullptr;  // [1] monotone ticket counter
   int64_t scan_tiles = 0;
   int64_t total_blocks = 0;
   int64_t pitch = 0;
@@ -88,8 +88,9 @@ void launch_p2g_tiled(cudaStream_t st, const float* S, int64_t pitch, const int3
                       float4* acc, const DevParams& P);
 void launch_grid_update_blocks(cudaStream_t st, const PipelineBuffers* pb, float4* acc, float4* vel,
                                const DevParams& P, const int64_t* d_step);
-void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t pitch, const int32_t* ids_in,
-                      int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const DevParams& P, DevErr* err,
-                      int64_t* d_step);
+void p2g_tables_init(cudaStream_t st);
+void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
+                      int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const int64_t* scene_off,
+                      int n_scenes, const DevParams& P, DevErr* err, int64_t* d_step);
 
 }  // namespace nsf
