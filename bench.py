@@ -43,7 +43,10 @@ CONFIG_DESC = {
     "C2": "sand column collapse, 200,000 particles, 128^3 grid, Drucker-Prager",
     "C3": "metal compression, 1,000,000 particles, 256^3 grid, von Mises + moving plate",
     "C4": "large sparse scene, 8,000,000 particles (64 balls), 512^3 grid, fixed-corotated",
+    "C5": "reduced-order batch: 256 scenes x 2,048 sampled points, NSF MLP (9-128x4-6, bf16) + MPM on per-scene 64^3 grids",
 }
+# FLOPs per point of the NSF MLP (C5): 2 * (9*128 + 3*128*128 + 128*6)
+MLP_FLOP_PER_POINT = 2.0 * (9 * 128 + 3 * 128 * 128 + 128 * 6)
 
 # Algorithmic bytes per unit:
 # per particle-substep for particle kernels, per touched node for the grid.
@@ -127,7 +130,7 @@ def dist_env():
 
 def make_scene(name):
     import scenes
-    return {"C1": scenes.c1, "C2": scenes.c2, "C3": scenes.c3, "C4": scenes.c4}[name]()
+    return {"C1": scenes.c1, "C2": scenes.c2, "C3": scenes.c3, "C4": scenes.c4, "C5": scenes.c5}[name]()
 
 
 # ---------------------------------------------------------------------------
@@ -142,13 +145,26 @@ def run_reference(args):
     sc = make_scene(args.config)
     P = mpm.params_from_config(sc.cfg)
     S = min(args.ref_sample, sc.n)
-    st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S], "F": sc.F[:S],
-          "tau": mpm.initial_tau(sc.F[:S], P)}
+    if args.config == "C5":
+        import oracle
+        S = int(sc.scene_offsets[1])          # one scene per step
+        st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S]}
+        off = np.array([0, S])
+
+        def one(st, k):
+            return oracle.reduced_substep(st, P, off, sc.X_ref[:S], sc.mlp, sc.cfg.stress_scale,
+                                          sc.z0[:1], sc.dz[:1], k)
+    else:
+        st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S], "F": sc.F[:S],
+              "tau": mpm.initial_tau(sc.F[:S], P)}
+
+        def one(st, k):
+            return mpm.substep(st, P, k)
     for k in range(args.warmup):
-        st = mpm.substep(st, P, k)
+        st = one(st, k)
     t0 = time.perf_counter()
     for k in range(args.steps):
-        st = mpm.substep(st, P, args.warmup + k)
+        st = one(st, args.warmup + k)
     dt = time.perf_counter() - t0
     value = S * args.steps / dt
     line = {"metric": "particle-substeps/s", "value": value, "unit": "particle-substeps/s",
@@ -168,13 +184,26 @@ def run_reference(args):
 def cpu_baseline(sc, budget_s=15.0, sample=50000):
     """Oracle as it stands, single thread, on a bounded sample (rank 0, N=1)."""
     from oracle import mpm
+    import oracle
     P = mpm.params_from_config(sc.cfg)
     S = min(sample, sc.n)
-    st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S], "F": sc.F[:S], "tau": mpm.initial_tau(sc.F[:S], P)}
+    if sc.mlp is not None:   # reduced variant: whole scenes (MLP + MPM per scene)
+        ns = max(1, int(np.searchsorted(sc.scene_offsets, S, side="right")) - 1)
+        S = int(sc.scene_offsets[ns])
+        st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S]}
+
+        def one(st, k):
+            return oracle.reduced_substep(st, P, sc.scene_offsets[:ns + 1], sc.X_ref[:S], sc.mlp,
+                                          sc.cfg.stress_scale, sc.z0, sc.dz, k)
+    else:
+        st = {"x": sc.x[:S], "v": sc.v[:S], "C": sc.C[:S], "F": sc.F[:S], "tau": mpm.initial_tau(sc.F[:S], P)}
+
+        def one(st, k):
+            return mpm.substep(st, P, k)
     t0 = time.perf_counter()
     k = 0
     while True:
-        st = mpm.substep(st, P, k)
+        st = one(st, k)
         k += 1
         if time.perf_counter() - t0 > budget_s or k >= 50:
             break
@@ -207,9 +236,7 @@ def run_ours(args):
     n = sc.n
     stream = torch.cuda.Stream(device=dev)
     sim = nsf.Simulator(sc.cfg, stream=stream.cuda_stream)
-    xs = {k: torch.from_numpy(getattr(sc, k)).to(dev) for k in ("x", "v", "C", "F")}
-    torch.cuda.synchronize()
-    sim.load(xs["x"], xs["v"], xs["C"], xs["F"])
+    sim.load_scene(sc)            # state (+ MLP and latents for C5) resident in HBM
     # warm-up (also captures the CUDA graph)
     sim.substep(args.warmup)
     sim.sync()
@@ -254,7 +281,17 @@ def run_ours(args):
         name, (tot_ms, cnt) = top
         bpp = KERNEL_BYTES_PER_PARTICLE.get(name)
         avg_ms = tot_ms / max(cnt, 1)
-        if bpp is not None:
+        if name == "nsf_mlp":
+            pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+                os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+            peak_t = float(pk.get("bf16_tflops_sustained", 1400.0))
+            achieved = MLP_FLOP_PER_POINT * n / (avg_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "kernel": name, "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
+                    "frac": achieved / peak_t, "traffic": load_traffic().get(args.config, {}).get(name),
+                    "flops_per_launch": MLP_FLOP_PER_POINT * n, "avg_launch_ms": avg_ms,
+                    "share_of_step": tot_ms / sum(v[0] for v in kt.values()),
+                    "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops_sustained)" if pk else "fallback"}
+        elif bpp is not None:
             achieved = bpp * n / (avg_ms * 1e-3) / 1e9
             traffic = load_traffic().get(args.config, {}).get(name)
             roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -265,7 +302,7 @@ def run_ours(args):
     step_gbs = B_ALG_PER_PARTICLE_SUBSTEP * n / (ms / args.steps * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
-    pin = {k: torch.from_numpy(getattr(sc, k)).pin_memory() for k in ("x", "v", "C", "F")}
+    pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(sc, k))).pin_memory() for k in ("x", "v", "C", "F")}
     out_x = torch.empty((n, 3), dtype=torch.float32).pin_memory()
     out_v = torch.empty((n, 3), dtype=torch.float32).pin_memory()
     import ctypes
@@ -273,13 +310,14 @@ def run_ours(args):
     h2d = sum(t.numel() * 4 for t in pin.values())
     d2h = 2 * n * 3 * 4
     e2e_iters = max(1, args.e2e_iters)
-    sim.load(pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy())
+    sim.load(pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy(), sc.scene_offsets)
     sim.substep(2)
     sim.sync()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_iters):
-        nsf.nsf_mpm_load_particles(sim.h, pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy())
+        nsf.nsf_mpm_load_particles(sim.h, pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy(),
+                                   sc.scene_offsets)
         nsf.nsf_mpm_substep(sim.h, args.steps)
         ptrs = (ctypes.c_void_p * 2)(out_x.data_ptr(), out_v.data_ptr())
         st = lib.nsf_mpm_read_state(sim.h, nsf.NSF_FIELD_X | nsf.NSF_FIELD_V, ptrs, 0)
@@ -307,7 +345,9 @@ def run_ours(args):
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                        "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
                        "replicas": world, "l2": "inputs larger than L2 (state 2x120 MB, ~268 MB moved per substep)",
-                       "step": "one full substep: binning, P2G, grid update, G2P + return map"},
+                       "step": ("one full substep: binning, NSF MLP (tcgen05), P2G, grid update, G2P"
+                                if args.config == "C5" else
+                                "one full substep: binning, P2G, grid update, G2P + return map")},
             "hbm_alg_gbs_whole_step": step_gbs,
             "hbm_alg_frac_whole_step": step_gbs / peak,
             "roofline": roof,

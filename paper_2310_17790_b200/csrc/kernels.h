@@ -30,7 +30,13 @@ struct MlpDev {
   int64_t w_off[10];    // element offsets of each layer's weights
   int64_t b_off[10];
 };
-// tau (SoA planes PT.. of S, or AoS m x 6 if aos_out) = stress_scale * h(X, z_scene(p) + step*dz)
+// tcgen05 tensor-core MLP (kernels_nsf_tc.cu): width 128, 2..4 hidden layers
+bool nsf_mlp_tc_supported(const MlpDev& mlp);
+void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
+                       int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
+                       const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out);
+// tau (AoSoA tau fields of the particle store, or AoS m x 6 if aos_out) = stress_scale * h(X, z_scene(p) + step*dz);
+// dispatches to the tensor-core kernel when supported (NSF_MLP_SIMT=1 forces the CUDA-core kernel)
 void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X /*3 planes, pitch*/, int64_t xpitch,
                     const int64_t* scene_off, int n_scenes, const float* z, const float* dz, int r,
                     const int64_t* d_step, const MlpDev& mlp, float stress_scale, float* tau_out,

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "kernels.h"
 
 namespace nsf {
@@ -140,6 +141,15 @@ void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, 
                     int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
                     const MlpDev& mlp, float stress_scale, float* tau_out, int64_t tau_pitch, int aos_out) {
   if (n == 0) return;
+  static int force_simt = -1;
+  if (force_simt < 0) {
+    const char* e = getenv("NSF_MLP_SIMT");
+    force_simt = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  if (!force_simt && nsf_mlp_tc_supported(mlp)) {
+    launch_nsf_mlp_tc(st, n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp, stress_scale, tau_out, aos_out);
+    return;
+  }
   int L = mlp.n_hidden + 1;
   size_t wbytes = (size_t)((mlp.w_off[L] + 7) & ~7ll) * 2;
   size_t smem = wbytes + 2 * (size_t)kMaxWidth * kTile * 2;

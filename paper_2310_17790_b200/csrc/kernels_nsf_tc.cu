@@ -1,0 +1,356 @@
+// Neural stress field MLP on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+//   tau = sigma_tau * h(X, z),  h = W_out r(ELU(W_L r(... ELU(W_1 u + b_1) ...)) + b_L) + b_out
+//   (Eq. (9); architecture P:498-500; numerics reading #20:
+//    layer-1 input fp32, activations rounded to bf16 before every later layer,
+//    fp32 accumulation, bias and ELU in fp32)
+//
+// One persistent CTA per SM, 256 threads = two independent "streams" of 128
+// points (one warpgroup each), so that one stream's CUDA-core epilogue (bias,
+// ELU, bf16 rounding) overlaps the other stream's MMAs.  Per stream and tile:
+//   layer 1 (K = in_dim <= 16): fp32 FMA on CUDA cores, one thread per point,
+//     result rounded to bf16 into the stream's A tile (128 x 128, K-major,
+//     128B-swizzled, the canonical UMMA layout);
+//   hidden layers 2..L: tcgen05.mma.cta_group::1.kind::f16, M = N = 128,
+//     K = 8 x 16, A = activations (smem), B = W_l (smem, resident for the whole
+//     kernel), D = fp32 in TMEM (128 lanes x 128 columns); the epilogue reads D
+//     with tcgen05.ld (thread = TMEM lane = point) and rewrites the A tile;
+//   output layer: the same MMA with N = 16 (W_out zero-padded to 16 rows).
+// TMEM: stream s uses columns [256 s, 256 s + 144).  Completion of each MMA
+// group is signalled by tcgen05.commit to a per-stream mbarrier.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "kernels.h"
+#include "params.cuh"
+
+namespace nsf {
+
+namespace tc {
+
+constexpr int kThreads = 256;       // 2 streams x 128 points
+constexpr int kM = 128;             // points per tile (MMA M)
+constexpr int kW = 128;             // layer width (MMA N and K)
+constexpr int kMaxHiddenMMA = 3;    // hidden layers on tensor cores (n_hidden <= 4)
+constexpr int kOutN = 16;           // padded output width
+constexpr int kTileBytes = kM * kW * 2;        // 32 KB bf16, two 64-wide K atoms of 16 KB
+constexpr int kOutBBytes = kOutN * kW * 2;     // 4 KB
+
+struct __align__(1024) Smem {
+  uint8_t wB[kMaxHiddenMMA][kTileBytes];   // W_2..W_L as B operands (N x K, K-major, SW128)
+  uint8_t wOut[kOutBBytes];                 // W_out padded to 16 rows
+  uint8_t a[2][kTileBytes];                 // per-stream activation tile
+  float w1[16][kW];                         // layer-1 weights, fp32, [in][out]
+  float bias[kMaxHiddenMMA + 1][kW];        // b_1 .. b_L
+  float bout[kOutN];
+  unsigned long long bar[2];                // per-stream MMA-completion mbarriers
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// byte offset of element (row, k) in a K-major, 128B-swizzled tile of `rows` rows
+// (Swizzle<3,4,3>: the 16-byte chunk index within a 128-byte row is XORed with row % 8)
+__device__ __forceinline__ uint32_t sw128_offset(int row, int k, int rows) {
+  const int atom = k >> 6, kk = k & 63;
+  return (uint32_t)(atom * rows * 128 + row * 128 + ((((kk >> 3) ^ (row & 7))) << 4) + ((kk & 7) << 1));
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B, LBO = 16 B, version 1
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)1 << 16;                          // leading byte offset (16 B units)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B bf16, both K-major, M x N
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void stream_barrier(int s) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + s) : "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float elu(float a) { return a > 0.0f ? a : __expf(a) - 1.0f; }
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);   // RNE
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// write 32 activations (columns c0..c0+31) of row `row` into the swizzled A tile
+__device__ __forceinline__ void store_act32(uint8_t* tile, int row, int c0, const float* h) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = c0 + 8 * q;
+    uint4 u;
+    u.x = pack_bf16(h[8 * q + 0], h[8 * q + 1]);
+    u.y = pack_bf16(h[8 * q + 2], h[8 * q + 3]);
+    u.z = pack_bf16(h[8 * q + 4], h[8 * q + 5]);
+    u.w = pack_bf16(h[8 * q + 6], h[8 * q + 7]);
+    *reinterpret_cast<uint4*>(tile + sw128_offset(row, k, kM)) = u;
+  }
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+__global__ void __launch_bounds__(kThreads, 1)
+k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64_t* __restrict__ scene_off,
+             int n_scenes, const float* __restrict__ z, const float* __restrict__ dz, int r,
+             const int64_t* __restrict__ d_step, MlpDev mlp, float stress_scale, float* __restrict__ tau_out,
+             int aos_out) {
+  extern __shared__ uint8_t smem_raw[];
+  // align to 1024 B (SWIZZLE_128B atoms)
+  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x;
+  const int s = tid >> 7;          // stream
+  const int t = tid & 127;         // point within the tile == TMEM lane
+  const int warp = tid >> 5;
+  const int L = mlp.n_hidden + 1;  // linear layers
+  const int n_mma_hidden = mlp.n_hidden - 1;
+  const int in_dim = mlp.in_dim;
+
+  // ---- one-time setup: weights into smem (swizzled B operands), biases, TMEM, barriers
+  for (int l = 0; l < n_mma_hidden; ++l) {
+    const uint16_t* W = mlp.W + mlp.w_off[l + 1];   // [128 out][128 in]
+    for (int c = tid; c < kW * (kW / 8); c += kThreads) {
+      const int nrow = c >> 4, kc = c & 15;
+      const uint4 v = *reinterpret_cast<const uint4*>(W + nrow * kW + kc * 8);
+      *reinterpret_cast<uint4*>(sm.wB[l] + sw128_offset(nrow, kc * 8, kW)) = v;
+    }
+  }
+  {
+    const uint16_t* W = mlp.W + mlp.w_off[L - 1];   // [out_dim][128]
+    for (int c = tid; c < kOutN * (kW / 8); c += kThreads) {
+      const int nrow = c >> 4, kc = c & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (nrow < mlp.out_dim) v = *reinterpret_cast<const uint4*>(W + nrow * kW + kc * 8);
+      *reinterpret_cast<uint4*>(sm.wOut + sw128_offset(nrow, kc * 8, kOutN)) = v;
+    }
+  }
+  for (int e = tid; e < 16 * kW; e += kThreads) {
+    const int i = e / kW, j = e % kW;
+    sm.w1[i][j] = i < in_dim ? __uint_as_float(((uint32_t)mlp.W[mlp.w_off[0] + j * in_dim + i]) << 16) : 0.0f;
+  }
+  for (int e = tid; e < (kMaxHiddenMMA + 1) * kW; e += kThreads) {
+    const int l = e / kW, j = e % kW;
+    sm.bias[l][j] = l < mlp.n_hidden ? mlp.b[mlp.b_off[l] + j] : 0.0f;
+  }
+  if (tid < kOutN) sm.bout[tid] = tid < mlp.out_dim ? mlp.b[mlp.b_off[L - 1] + tid] : 0.0f;
+  if (tid == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t d_col = tmem + 256u * s;                 // hidden-layer accumulator (128 cols)
+  const uint32_t o_col = tmem + 256u * s + 128u;          // output accumulator (16 cols)
+  const uint32_t lane_sel = ((uint32_t)(32 * (warp & 3))) << 16;
+  const int64_t step = d_step ? *d_step : 0;
+  uint8_t* A = sm.a[s];
+  const uint32_t a_saddr = smem_u32(A);
+  constexpr uint32_t kIdescH = make_idesc(kM, kW);
+  constexpr uint32_t kIdescO = make_idesc(kM, kOutN);
+  uint32_t phase = 0;
+
+  const int64_t n_tiles = (n + kM - 1) / kM;
+  for (int64_t tile = (int64_t)blockIdx.x * 2 + s; tile < n_tiles; tile += (int64_t)gridDim.x * 2) {
+    const int64_t p = tile * kM + t;
+    const bool live = p < n;
+    // ---- layer 1 on CUDA cores (fp32 input, reading #20) ----
+    float u[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) u[i] = 0.0f;
+    if (live) {
+      int scene = 0;
+      if (n_scenes > 1 && scene_off) {
+        int lo = 0, hi = n_scenes;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (scene_off[mid] <= p) lo = mid; else hi = mid;
+        }
+        scene = lo;
+      }
+      u[0] = X[0 * xpitch + p];
+      u[1] = X[1 * xpitch + p];
+      u[2] = X[2 * xpitch + p];
+      for (int k = 0; k < r && k < 13; ++k)
+        u[3 + k] = z[scene * r + k] + (float)step * (dz ? dz[scene * r + k] : 0.0f);
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < kW; c0 += 32) {
+      float h[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float a = sm.bias[0][c0 + j];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a = fmaf(sm.w1[i][c0 + j], u[i], a);
+        h[j] = elu(a);
+      }
+      store_act32(A, t, c0, h);
+    }
+    fence_async_smem();
+    stream_barrier(s);
+    // ---- hidden layers on tensor cores ----
+    for (int l = 0; l < n_mma_hidden; ++l) {
+      if (t == 0) {
+        fence_after();
+        const uint32_t b_saddr = smem_u32(sm.wB[l]);
+#pragma unroll
+        for (int kk = 0; kk < kW / 16; ++kk) {
+          const uint32_t koff = (uint32_t)((kk >> 2) * (kM * 128) + (kk & 3) * 32);
+          const uint32_t kofb = (uint32_t)((kk >> 2) * (kW * 128) + (kk & 3) * 32);
+          mma_bf16(d_col, make_desc(a_saddr + koff), make_desc(b_saddr + kofb), kIdescH, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.bar[s]);
+      }
+      mbar_wait(&sm.bar[s], phase);
+      phase ^= 1;
+      fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < kW; c0 += 32) {
+        float h[32];
+        tmem_ld32(d_col + lane_sel + c0, h);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h[j] = elu(h[j] + sm.bias[l + 1][c0 + j]);
+        store_act32(A, t, c0, h);
+      }
+      fence_before();
+      fence_async_smem();
+      stream_barrier(s);
+    }
+    // ---- output layer (N = 16, zero-padded) ----
+    if (t == 0) {
+      fence_after();
+      const uint32_t b_saddr = smem_u32(sm.wOut);
+#pragma unroll
+      for (int kk = 0; kk < kW / 16; ++kk) {
+        const uint32_t koff = (uint32_t)((kk >> 2) * (kM * 128) + (kk & 3) * 32);
+        const uint32_t kofb = (uint32_t)((kk >> 2) * (kOutN * 128) + (kk & 3) * 32);
+        mma_bf16(o_col, make_desc(a_saddr + koff), make_desc(b_saddr + kofb), kIdescO, kk > 0 ? 1u : 0u);
+      }
+      mma_commit(&sm.bar[s]);
+    }
+    mbar_wait(&sm.bar[s], phase);
+    phase ^= 1;
+    fence_after();
+    float y[8];
+    tmem_ld8(o_col + lane_sel, y);
+    if (live) {
+      for (int o = 0; o < mlp.out_dim && o < 8; ++o) {
+        const float val = stress_scale * (y[o] + sm.bout[o]);
+        if (aos_out) tau_out[p * mlp.out_dim + o] = val;
+        else tau_out[pbase(p) + o * 32] = val;   // AoSoA particle store (tau fields)
+      }
+    }
+    fence_before();
+    stream_barrier(s);   // the A tile and accumulators are free for the next tile
+  }
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+bool nsf_mlp_tc_supported(const MlpDev& mlp) {
+  return mlp.width == kW && mlp.n_hidden >= 2 && mlp.n_hidden - 1 <= kMaxHiddenMMA && mlp.in_dim <= 16 &&
+         mlp.out_dim <= 8;
+}
+
+void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
+                       int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
+                       const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out) {
+  if (n == 0) return;
+  static int n_sms = 0;
+  static bool attr = false;
+  const size_t smem = sizeof(Smem) + 1024;
+  if (!attr) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_nsf_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int64_t tiles = (n + kM - 1) / kM;
+  int64_t grid = (tiles + 1) / 2;
+  if (grid > n_sms) grid = n_sms;
+  k_nsf_mlp_tc<<<(unsigned)grid, kThreads, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp,
+                                                       stress_scale, tau_out, aos_out);
+}
+
+}  // namespace nsf
