@@ -5,9 +5,9 @@
 //    layer-1 input fp32, activations rounded to bf16 before every later layer,
 //    fp32 accumulation, bias and ELU in fp32)
 //
-// One persistent CTA per SM, 256 threads = two independent "streams" of 128
-// points (one warpgroup each), so that one stream's CUDA-core epilogue (bias,
-// ELU, bf16 rounding) overlaps the other stream's MMAs.  Per stream and tile:
+// One persistent CTA per SM, 384 threads = three independent "streams" of 128
+// points (one warpgroup each), so that the streams' CUDA-core epilogues (bias,
+// ELU, bf16 rounding) overlap each other's MMAs.  Per stream and tile:
 //   layer 1 (K = in_dim <= 16): fp32 FMA on CUDA cores, one thread per point,
 //     result rounded to bf16 into the stream's A tile (128 x 128, K-major,
 //     128B-swizzled, the canonical UMMA layout);
@@ -16,7 +16,7 @@
 //     kernel), D = fp32 in TMEM (128 lanes x 128 columns); the epilogue reads D
 //     with tcgen05.ld (thread = TMEM lane = point) and rewrites the A tile;
 //   output layer: the same MMA with N = 16 (W_out zero-padded to 16 rows).
-// TMEM: stream s uses columns [256 s, 256 s + 144).  Completion of each MMA
+// TMEM: stream s uses columns [160 s, 160 s + 144).  Completion of each MMA
 // group is signalled by tcgen05.commit to a per-stream mbarrier.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -28,7 +28,9 @@ namespace nsf {
 
 namespace tc {
 
-constexpr int kThreads = 256;       // 2 streams x 128 points
+constexpr int kStreams = 3;         // independent 128-point tile streams per CTA
+constexpr int kThreads = 128 * kStreams;
+constexpr int kTmemStride = 160;    // TMEM columns per stream (128 hidden + 16 output, 32-aligned)
 constexpr int kM = 128;             // points per tile (MMA M)
 constexpr int kW = 128;             // layer width (MMA N and K)
 constexpr int kMaxHiddenMMA = 3;    // hidden layers on tensor cores (n_hidden <= 4)
@@ -39,11 +41,11 @@ constexpr int kOutBBytes = kOutN * kW * 2;     // 4 KB
 struct __align__(1024) Smem {
   uint8_t wB[kMaxHiddenMMA][kTileBytes];   // W_2..W_L as B operands (N x K, K-major, SW128)
   uint8_t wOut[kOutBBytes];                 // W_out padded to 16 rows
-  uint8_t a[2][kTileBytes];                 // per-stream activation tile
+  uint8_t a[kStreams][kTileBytes];          // per-stream activation tile
   float w1[16][kW];                         // layer-1 weights, fp32, [in][out]
   float bias[kMaxHiddenMMA + 1][kW];        // b_1 .. b_L
   float bout[kOutN];
-  unsigned long long bar[2];                // per-stream MMA-completion mbarriers
+  unsigned long long bar[kStreams];          // per-stream MMA-completion mbarriers
   uint32_t tmem_base;
 };
 
@@ -134,15 +136,30 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float elu(float a) { return a > 0.0f ? a : __expf(a) - 1.0f; }
+// ELU(a) = a (a > 0), e^a - 1 (a <= 0), fp32 with ex2.approx (MUFU)
+__device__ __forceinline__ float elu(float a) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(a * 1.4426950408889634f));
+  return a > 0.0f ? a : e - 1.0f;
+}
+
+__device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+  return v;
+}
+__device__ __forceinline__ void sts_u4(uint32_t saddr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);   // RNE
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// write 32 activations (columns c0..c0+31) of row `row` into the swizzled A tile
-__device__ __forceinline__ void store_act32(uint8_t* tile, int row, int c0, const float* h) {
+// write 32 activations (columns c0..c0+31) of row `row` into the swizzled A tile at shared address `tile`
+__device__ __forceinline__ void store_act32(uint32_t tile, int row, int c0, const float* h) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = c0 + 8 * q;
@@ -151,7 +168,7 @@ __device__ __forceinline__ void store_act32(uint8_t* tile, int row, int c0, cons
     u.y = pack_bf16(h[8 * q + 2], h[8 * q + 3]);
     u.z = pack_bf16(h[8 * q + 4], h[8 * q + 5]);
     u.w = pack_bf16(h[8 * q + 6], h[8 * q + 7]);
-    *reinterpret_cast<uint4*>(tile + sw128_offset(row, k, kM)) = u;
+    sts_u4(tile + sw128_offset(row, k, kM), u);
   }
 }
 
@@ -203,8 +220,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   }
   if (tid < kOutN) sm.bout[tid] = tid < mlp.out_dim ? mlp.b[mlp.b_off[L - 1] + tid] : 0.0f;
   if (tid == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    for (int k = 0; k < kStreams; ++k) mbar_init(&sm.bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -217,18 +233,19 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   __syncthreads();
   fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const uint32_t d_col = tmem + 256u * s;                 // hidden-layer accumulator (128 cols)
-  const uint32_t o_col = tmem + 256u * s + 128u;          // output accumulator (16 cols)
+  const uint32_t d_col = tmem + (uint32_t)(kTmemStride * s);          // hidden-layer accumulator (128 cols)
+  const uint32_t o_col = tmem + (uint32_t)(kTmemStride * s) + 128u;   // output accumulator (16 cols)
   const uint32_t lane_sel = ((uint32_t)(32 * (warp & 3))) << 16;
   const int64_t step = d_step ? *d_step : 0;
-  uint8_t* A = sm.a[s];
-  const uint32_t a_saddr = smem_u32(A);
+  const uint32_t a_saddr = smem_u32(sm.a[s]);
+  const uint32_t w1_saddr = smem_u32(&sm.w1[0][0]);
+  const uint32_t bias_saddr = smem_u32(&sm.bias[0][0]);
   constexpr uint32_t kIdescH = make_idesc(kM, kW);
   constexpr uint32_t kIdescO = make_idesc(kM, kOutN);
   uint32_t phase = 0;
 
   const int64_t n_tiles = (n + kM - 1) / kM;
-  for (int64_t tile = (int64_t)blockIdx.x * 2 + s; tile < n_tiles; tile += (int64_t)gridDim.x * 2) {
+  for (int64_t tile = (int64_t)blockIdx.x * kStreams + s; tile < n_tiles; tile += (int64_t)gridDim.x * kStreams) {
     const int64_t p = tile * kM + t;
     const bool live = p < n;
     // ---- layer 1 on CUDA cores (fp32 input, reading #20) ----
@@ -255,13 +272,27 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     for (int c0 = 0; c0 < kW; c0 += 32) {
       float h[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float a = sm.bias[0][c0 + j];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) a = fmaf(sm.w1[i][c0 + j], u[i], a);
-        h[j] = elu(a);
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = lds_f4(bias_saddr + (uint32_t)(c0 + 4 * q) * 4u);
+        h[4 * q] = b.x; h[4 * q + 1] = b.y; h[4 * q + 2] = b.z; h[4 * q + 3] = b.w;
       }
-      store_act32(A, t, c0, h);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < in_dim) {   // warp-uniform
+          const float ui = u[i];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {   // broadcast reads of W_1[i][c0..c0+31]
+            const float4 wv = lds_f4(w1_saddr + (uint32_t)(i * kW + c0 + 4 * q) * 4u);
+            h[4 * q] = fmaf(wv.x, ui, h[4 * q]);
+            h[4 * q + 1] = fmaf(wv.y, ui, h[4 * q + 1]);
+            h[4 * q + 2] = fmaf(wv.z, ui, h[4 * q + 2]);
+            h[4 * q + 3] = fmaf(wv.w, ui, h[4 * q + 3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) h[j] = elu(h[j]);
+      store_act32(a_saddr, t, c0, h);
     }
     fence_async_smem();
     stream_barrier(s);
@@ -286,8 +317,14 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
         float h[32];
         tmem_ld32(d_col + lane_sel + c0, h);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] = elu(h[j] + sm.bias[l + 1][c0 + j]);
-        store_act32(A, t, c0, h);
+        for (int q = 0; q < 8; ++q) {
+          const float4 b = lds_f4(bias_saddr + (uint32_t)((l + 1) * kW + c0 + 4 * q) * 4u);
+          h[4 * q] = elu(h[4 * q] + b.x);
+          h[4 * q + 1] = elu(h[4 * q + 1] + b.y);
+          h[4 * q + 2] = elu(h[4 * q + 2] + b.z);
+          h[4 * q + 3] = elu(h[4 * q + 3] + b.w);
+        }
+        store_act32(a_saddr, t, c0, h);
       }
       fence_before();
       fence_async_smem();
@@ -347,7 +384,7 @@ void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitc
     attr = true;
   }
   const int64_t tiles = (n + kM - 1) / kM;
-  int64_t grid = (tiles + 1) / 2;
+  int64_t grid = (tiles + kStreams - 1) / kStreams;
   if (grid > n_sms) grid = n_sms;
   k_nsf_mlp_tc<<<(unsigned)grid, kThreads, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp,
                                                        stress_scale, tau_out, aos_out);
