@@ -55,6 +55,11 @@ KERNEL_BYTES_PER_PARTICLE = {
     "p2g_tiled": 88.0,           # + perm
     "g2p_direct": 48.0 + 120.0,  # x, F read; x, v, C, F, tau written
     "g2p_tiled": 4.0 + 48.0 + 120.0 + 4.0,  # perm, x, F in; 5 fields + next key out
+    "g2p": 48.0 + 120.0,         # split path G2P (GRADW): x, F read; x, v, C, F, tau written
+    "g2p2g": 48.0 + 120.0,       # fused G2P + next P2G, state in place: x, F read; x, v, C, F, tau written
+                                 # (v, C, tau are consumed from registers by the fused P2G; grid traffic
+                                 # stays in L2 -- it is counted per touched node under grid_update)
+    "reorder": 2 * 120.0 + 12.0, # every 32nd substep: 30 planes read + written, perm + ids
     "bin_keys_hist": 12.0 + 4.0,
     "bin_scatter": 8.0,
 }
@@ -253,12 +258,14 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(local) as clk:
+        launches0 = nsf.nsf_mpm_launch_count(sim.h)
         e0.record(stream)
         sim.substep(args.steps)
         e1.record(stream)
         e1.synchronize()
     barrier()
     ms = e0.elapsed_time(e1)
+    launches = nsf.nsf_mpm_launch_count(sim.h) - launches0
     sim.sync()   # surfaces deferred device errors
     if world > 1:
         import torch.distributed as dist
@@ -344,7 +351,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenes/, seeded)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                        "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
-                       "replicas": world, "l2": "inputs larger than L2 (state 2x120 MB, ~268 MB moved per substep)",
+                       "replicas": world, "l2": ("inputs larger than L2 (particle state 120 B x n = 120 MB for C3, rewritten every substep)"
+                              if n * 120 > 126e6 else "inputs smaller than L2 (state L2-resident between substeps)"),
                        "step": ("one full substep: binning, NSF MLP (tcgen05), P2G, grid update, G2P"
                                 if args.config == "C5" else
                                 "one full substep: binning, P2G, grid update, G2P + return map")},
@@ -357,7 +365,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h,
                     "definition": f"one e2e step = load state from pinned host, {args.steps} substeps, "
                                   "read x and v back to pinned host"},
-            "gpu_launches": per_sub * args.steps,
+            "gpu_launches": launches,
+            "launches_per_substep": launches / max(args.steps, 1),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))

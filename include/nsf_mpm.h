@@ -223,8 +223,12 @@ nsf_status nsf_mpm_set_profiling(nsf_mpm* h, int32_t enable);
 int32_t nsf_mpm_kernel_times(nsf_mpm* h, const char** names, double* total_ms,
                              int64_t* launches, int32_t max);
 
-/* Number of kernel launches per substep for the current configuration. */
+/* Number of kernel launches of the most recently enqueued substep. */
 int32_t nsf_mpm_launches_per_substep(nsf_mpm* h);
+
+/* Kernel launches enqueued by nsf_mpm_substep since the last load (the fused
+ * pipeline adds a re-binning every 32 substeps, so this is not n x a constant). */
+int64_t nsf_mpm_launch_count(const nsf_mpm* h);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,7 @@ EXPORTS = ["nsf_mpm_abi_version", "nsf_mpm_create", "nsf_mpm_set_stream", "nsf_m
            "nsf_mpm_substep", "nsf_mpm_eval_stress_field", "nsf_mpm_read_state", "nsf_mpm_sync",
            "nsf_mpm_step_count", "nsf_mpm_inverted_count", "nsf_mpm_last_error", "nsf_mpm_destroy",
            "nsf_mpm_debug_bins", "nsf_mpm_debug_grid", "nsf_mpm_set_profiling",
-           "nsf_mpm_kernel_times", "nsf_mpm_launches_per_substep"]
+           "nsf_mpm_kernel_times", "nsf_mpm_launches_per_substep", "nsf_mpm_launch_count"]
 
 
 class nsf_material(C.Structure):
@@ -90,6 +90,7 @@ def lib():
         "nsf_mpm_set_profiling": (i32, [vp, i32]),
         "nsf_mpm_kernel_times": (i32, [vp, dp(C.c_char_p), dp(C.c_double), dp(i64), i32]),
         "nsf_mpm_launches_per_substep": (i32, [vp]),
+        "nsf_mpm_launch_count": (i64, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -299,6 +300,10 @@ def nsf_mpm_kernel_times(h) -> dict:
 
 def nsf_mpm_launches_per_substep(h) -> int:
     return lib().nsf_mpm_launches_per_substep(h)
+
+
+def nsf_mpm_launch_count(h) -> int:
+    return lib().nsf_mpm_launch_count(h)
 
 
 # ---------------------------------------------------------------------------

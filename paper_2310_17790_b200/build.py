@@ -24,6 +24,8 @@ LIB = os.path.join(PKG, "libnsf_mpm.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                      "--expt-relaxed-constexpr", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+# tuning knobs for experiments, e.g. NSF_DEFINES="NSF_P2G_ROWS=8 NSF_FUSED_MIN_BLOCKS=4"
+NVCC_FLAGS += [f"-D{d}" for d in os.environ.get("NSF_DEFINES", "").split()]
 
 
 def nvcc() -> str:
@@ -53,6 +55,12 @@ def _compile(src: str, force: bool, log: list) -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    stamp = os.path.join(BUILD, "flags.txt")     # a change of flags (NSF_DEFINES) forces a rebuild
+    flags = " ".join(NVCC_FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+        if os.path.exists(stamp):
+            os.remove(stamp)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     log: list = []
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
@@ -62,6 +70,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    with open(stamp, "w") as f:
+        f.write(flags)
     with open(os.path.join(BUILD, "ptxas.log"), "w" if log else "a") as f:
         for src, out in log:
             f.write(f"==== {src}\n{out}\n")

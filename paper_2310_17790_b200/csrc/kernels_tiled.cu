@@ -51,7 +51,13 @@ __device__ __forceinline__ BlockCoord decode_block(int key, const DevParams& P) 
 // ---------------------------------------------------------------------------
 // P2G (MLS force form)
 constexpr int kP2GThreads = 192;   // 64 cells x 3 stencil planes (ox)
-constexpr int kRows = 12;          // particles per cell per round
+#ifndef NSF_P2G_ROWS
+#define NSF_P2G_ROWS 12
+#endif
+#ifndef NSF_FUSED_MIN_BLOCKS
+#define NSF_FUSED_MIN_BLOCKS 3
+#endif
+constexpr int kRows = NSF_P2G_ROWS;   // particles per cell per round
 constexpr int kSlotFields = 21;    // w(9), u0(3), q0(3), q1(3), q2(3)
 constexpr int kSlotStride = kRows * 64;   // floats per field
 constexpr int kSegment = 1024;     // particles of one block handled per segment (smem: 3 CTAs/SM)
@@ -121,6 +127,107 @@ __device__ __forceinline__ void p2g_stage_particle(const float* __restrict__ S, 
                                    P.dx * Q[2], P.dx * Q[5], P.dx * Q[8]};
 #pragma unroll
   for (int k = 0; k < kSlotFields; ++k) sl[k * kSlotStride + s] = vals[k];
+}
+
+// one particle's slot data from its state values (same arithmetic as above)
+__device__ __forceinline__ void p2g_stage_values(const float x[3], const float v[3], const float Cm[9], const float T[6],
+                                                 int s, float* sl, const DevParams& P) {
+  const float m = P.mass;
+  const Axis a0 = bspline_axis(x[0], P.inv_dx), a1 = bspline_axis(x[1], P.inv_dx), a2 = bspline_axis(x[2], P.inv_dx);
+  const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
+  float Q[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+  const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
+  const float u0x = m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2);
+  const float u0y = m * v[1] - P.dx * (Q[3] * f0 + Q[4] * f1 + Q[5] * f2);
+  const float u0z = m * v[2] - P.dx * (Q[6] * f0 + Q[7] * f1 + Q[8] * f2);
+  const float vals[kSlotFields] = {a0.w[0], a0.w[1], a0.w[2], a1.w[0], a1.w[1], a1.w[2], a2.w[0], a2.w[1], a2.w[2],
+                                   u0x, u0y, u0z,
+                                   P.dx * Q[0], P.dx * Q[3], P.dx * Q[6],
+                                   P.dx * Q[1], P.dx * Q[4], P.dx * Q[7],
+                                   P.dx * Q[2], P.dx * Q[5], P.dx * Q[8]};
+#pragma unroll
+  for (int k = 0; k < kSlotFields; ++k) sl[k * kSlotStride + s] = vals[k];
+}
+
+// MLS P2G of one particle straight to the global accumulator (27 x red.v4), marking
+// every touched grid block in `flags` (used for particles outside their segment's
+// block, and for cells with more than kRows particles)
+// mark grid block `b` as touched; the first marker appends it to the work list of
+// the next grid update
+__device__ __forceinline__ void touch_block(int* flags, int* list, int* list_count, int b) {
+  if (flags[b] == 0 && atomicExch(&flags[b], 1) == 0) list[atomicAdd(list_count, 1)] = b;
+}
+
+__device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float v[3], const float Cm[9],
+                                                   const float T[6], float4* gbase, int* flags, int* list,
+                                                   int* list_count, int64_t scene_block0, const DevParams& P) {
+  const float m = P.mass;
+  Axis ax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ax[a] = bspline_axis(x[a], P.inv_dx);
+    ax[a].base = min(max(ax[a].base, 0), P.N[a] - 3);
+  }
+  const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
+  float Q[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
+        const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
+        const float mv0 = W * (m * v[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
+        const float mv1 = W * (m * v[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
+        const float mv2 = W * (m * v[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
+        red_add_v4_t(gbase + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
+      }
+  // touched blocks: per axis the blocks of base and base+2
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int b0 = (ax[0].base + 2 * a) >> 2, b1 = (ax[1].base + 2 * b) >> 2, b2 = (ax[2].base + 2 * c) >> 2;
+        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+      }
+}
+
+// thread (my_cell, ox) accumulates its cell's staged rows for stencil plane ox
+__device__ __forceinline__ void p2g_accumulate(const float* sl, int my_cell, int ox, int rows, float accm[9],
+                                               float accp[9][3]) {
+  const float fox = (float)ox;
+  for (int r = 0; r < rows; ++r) {
+    const int s = r * 64 + my_cell;
+    const float wx = sl[ox * kSlotStride + s];
+    const float wyv[3] = {sl[3 * kSlotStride + s], sl[4 * kSlotStride + s], sl[5 * kSlotStride + s]};
+    const float wzv[3] = {sl[6 * kSlotStride + s], sl[7 * kSlotStride + s], sl[8 * kSlotStride + s]};
+    const float ux = fmaf(fox, sl[12 * kSlotStride + s], sl[9 * kSlotStride + s]);
+    const float uy = fmaf(fox, sl[13 * kSlotStride + s], sl[10 * kSlotStride + s]);
+    const float uz = fmaf(fox, sl[14 * kSlotStride + s], sl[11 * kSlotStride + s]);
+    const float q1x = sl[15 * kSlotStride + s], q1y = sl[16 * kSlotStride + s], q1z = sl[17 * kSlotStride + s];
+    const float q2x = sl[18 * kSlotStride + s], q2y = sl[19 * kSlotStride + s], q2z = sl[20 * kSlotStride + s];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) {
+      const float wxy = wx * wyv[oy];
+      const float uyx = fmaf((float)oy, q1x, ux), uyy = fmaf((float)oy, q1y, uy), uyz = fmaf((float)oy, q1z, uz);
+#pragma unroll
+      for (int oz = 0; oz < 3; ++oz) {
+        const float W = wxy * wzv[oz];
+        const int k = oy * 3 + oz;
+        accm[k] += W;
+        accp[k][0] = fmaf(W, fmaf((float)oz, q2x, uyx), accp[k][0]);
+        accp[k][1] = fmaf(W, fmaf((float)oz, q2y, uyy), accp[k][1]);
+        accp[k][2] = fmaf(W, fmaf((float)oz, q2z, uyz), accp[k][2]);
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ int cell_in_block(const float* __restrict__ S, int64_t pitch, int p, const BlockCoord& bc,
@@ -364,41 +471,23 @@ __device__ __forceinline__ void load_pstate(PState& s, const float* __restrict__
   s.id = __ldg(ids + p);
 }
 
-#ifndef NSF_G2P_FLAT_MIN_BLOCKS
-#define NSF_G2P_FLAT_MIN_BLOCKS 7
-#endif
+// G2P gather: v_p = sum w v_i, C_p = 4/dx^2 sum w v_i (x_i - x_p)^T and the
+// velocity gradient G for the F update (= C_p in MLS form, sum v_i grad(w)^T in GRADW
+// form), from the blocked grid velocities vb (read through L1).  Separable sums:
+// per stencil plane a, T = sum w_y w_z v, Ty = sum o_y w_y w_z v, Tz = sum o_z w_y w_z v;
+// then v = sum w_x T and B = dx (M - v f^T) with M_ij = sum W v_i o_j.
 template <int FORCE>
-__global__ void __launch_bounds__(128, NSF_G2P_FLAT_MIN_BLOCKS)
-k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
-           const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
-           const int32_t* __restrict__ perm, const float4* __restrict__ vel, const int64_t* __restrict__ scene_off,
-           int n_scenes, int32_t* __restrict__ keys, int32_t* __restrict__ counts, DevParams P, DevErr* err,
-           int64_t* d_step) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)d_step, 1ull);
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const unsigned active = __ballot_sync(0xffffffffu, j < n);
-  if (j >= n) return;
-  const int lane = threadIdx.x & 31;
-  const int p = perm[j];
-  PState st;
-  load_pstate(st, Sin, p, ids_in);
-  // scenes stay contiguous and in order in the sorted slot order
-  const int bps = (int)P.blocks_per_scene;
-  int scene = 0;
-  if (n_scenes > 1) {
-    int lo = 0, hi = n_scenes;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (scene_off[mid] <= j) lo = mid; else hi = mid;
-    }
-    scene = lo;
-  }
-  const float4* vb = vel + (int64_t)scene * P.nodes_per_scene;
-  const float cC = 4.0f * P.inv_dx;
+__device__ __forceinline__ void g2p_gather(const float x[3], const float4* __restrict__ vb, const DevParams& P,
+                                           float v[3], float Cn[9], float G[9]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) v[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) G[k] = 0.f;
+  const float cC = 4.0f * P.inv_dx;   // C = (4/dx) (M - v f^T) = 4/dx^2 B (b = 2)
   Axis ax[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    ax[a] = bspline_axis(st.x[a], P.inv_dx);
+    ax[a] = bspline_axis(x[a], P.inv_dx);
     ax[a].base = min(max(ax[a].base, 0), P.N[a] - 3);
   }
   int X[3], Y[3], Z[3];
@@ -417,9 +506,7 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
   for (int b = 0; b < 3; ++b)
 #pragma unroll
     for (int c = 0; c < 3; ++c) wyz[b * 3 + c] = ax[1].w[b] * ax[2].w[c];
-  float v[3] = {0.f, 0.f, 0.f};
   float M[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     float Tt[3] = {0.f, 0.f, 0.f}, Ty[3] = {0.f, 0.f, 0.f}, Tz[3] = {0.f, 0.f, 0.f};
@@ -459,7 +546,6 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
       }
     }
   }
-  float Cn[9];
   const float f[3] = {ax[0].f, ax[1].f, ax[2].f};
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -469,6 +555,40 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
 #pragma unroll
     for (int k = 0; k < 9; ++k) G[k] = Cn[k];
   }
+}
+
+#ifndef NSF_G2P_FLAT_MIN_BLOCKS
+#define NSF_G2P_FLAT_MIN_BLOCKS 7
+#endif
+template <int FORCE>
+__global__ void __launch_bounds__(128, NSF_G2P_FLAT_MIN_BLOCKS)
+k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
+           const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
+           const int32_t* __restrict__ perm, const float4* __restrict__ vel, const int64_t* __restrict__ scene_off,
+           int n_scenes, int32_t* __restrict__ keys, int32_t* __restrict__ counts, DevParams P, DevErr* err,
+           int64_t* d_step) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)d_step, 1ull);
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const unsigned active = __ballot_sync(0xffffffffu, j < n);
+  if (j >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int p = perm[j];
+  PState st;
+  load_pstate(st, Sin, p, ids_in);
+  // scenes stay contiguous and in order in the sorted slot order
+  const int bps = (int)P.blocks_per_scene;
+  int scene = 0;
+  if (n_scenes > 1) {
+    int lo = 0, hi = n_scenes;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= j) lo = mid; else hi = mid;
+    }
+    scene = lo;
+  }
+  const float4* vb = vel + (int64_t)scene * P.nodes_per_scene;
+  float v[3], Cn[9], G[9];
+  g2p_gather<FORCE>(st.x, vb, P, v, Cn, G);
   float xn[3];
   bool ok = true;
   float* ob = Sout + pbase(j);
@@ -570,5 +690,394 @@ void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n,
 }  // namespace nsf
 
 namespace nsf {
-static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / 3, "P2G shared memory must allow 3 CTAs per SM");
+static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shared memory must allow the CTAs per SM");
+// ===========================================================================
+// Fused pipeline (MLS, full-order models): G2P of substep n and P2G of substep
+// n+1 in one kernel, over storage segments.
+//
+// Storage is sorted by 4x4x4-cell block at the last re-binning (every
+// kRebinEvery substeps, or at load); segment k = the particles that were in
+// block k then.  For each segment one CTA
+//   1. runs G2P(n) + the constitutive update for its particles (grid velocities
+//      gathered through L1) and writes the new state in place;
+//   2. stages the new state's P2G data by cell for the particles still inside
+//      block k (register accumulation per (cell, stencil plane), then one
+//      red.global.add.v4 per touched tile node), and scatters particles that left
+//      the block (or overflow a cell) directly with 27 red.global.add.v4;
+//   3. marks every grid block it touched in `flags`.
+// The grid update then visits exactly the flagged blocks.  Re-binning only
+// restores locality; correctness does not depend on it.
+#ifndef NSF_FUSED_VTILE
+#define NSF_FUSED_VTILE 1                      // G2P reads a shared-memory velocity tile (else global gathers)
+#endif
+constexpr int kRowsF = NSF_FUSED_VTILE ? 11 : 12;   // staged rows per cell in the fused kernel
+constexpr int kSlotStrideF = kRowsF * 64;
+constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-1, 4b+7)
+
+struct __align__(16) FusedSmem {
+  float4 vt[NSF_FUSED_VTILE ? kVT * kVT * kVT : 1];   // G2P velocity tile (8 KB)
+  union {
+    float slot[kSlotFields * kSlotStrideF];    // [field][row][cell]
+    float part[27 * 4 * 64];                   // [(node*4 + comp)][cell]
+  } u;
+  int pop[64];
+  int next;
+  uint16_t tbl[1728];
+  uint16_t tbl_off[218];
+};
+static_assert(sizeof(FusedSmem) + 1024 <= 228 * 1024 / 3, "fused kernel: 3 CTAs per SM");
+
+__device__ __forceinline__ void cp_async16_f(void* smem, const void* gmem, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
+}
+
+// G2P gather (MLS) from the shared 8^3 velocity tile whose node (0,0,0) is grid
+// node o[]; the 27 reads are one shared base address plus immediate offsets.
+__device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* vt, const int o[3], const DevParams& P,
+                                                float v[3], float Cn[9]) {
+  Axis ax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) ax[a] = bspline_axis(x[a], P.inv_dx);
+  const float4* tp = vt + ((ax[0].base - o[0]) * kVT + (ax[1].base - o[1])) * kVT + (ax[2].base - o[2]);
+  float wyz[9];
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) wyz[b * 3 + c] = ax[1].w[b] * ax[2].w[c];
+  float M[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  v[0] = v[1] = v[2] = 0.f;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float Tt[3] = {0.f, 0.f, 0.f}, Ty[3] = {0.f, 0.f, 0.f}, Tz[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float4 vi = tp[(a * kVT + b) * kVT + c];
+        const float wgt = wyz[b * 3 + c];
+        Tt[0] = fmaf(wgt, vi.x, Tt[0]); Tt[1] = fmaf(wgt, vi.y, Tt[1]); Tt[2] = fmaf(wgt, vi.z, Tt[2]);
+        if (b) {
+          const float wb = (float)b * wgt;
+          Ty[0] = fmaf(wb, vi.x, Ty[0]); Ty[1] = fmaf(wb, vi.y, Ty[1]); Ty[2] = fmaf(wb, vi.z, Ty[2]);
+        }
+        if (c) {
+          const float wc = (float)c * wgt;
+          Tz[0] = fmaf(wc, vi.x, Tz[0]); Tz[1] = fmaf(wc, vi.y, Tz[1]); Tz[2] = fmaf(wc, vi.z, Tz[2]);
+        }
+      }
+    const float wx = ax[0].w[a];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      v[i] = fmaf(wx, Tt[i], v[i]);
+      if (a) M[i * 3 + 0] = fmaf((float)a * wx, Tt[i], M[i * 3 + 0]);
+      M[i * 3 + 1] = fmaf(wx, Ty[i], M[i * 3 + 1]);
+      M[i * 3 + 2] = fmaf(wx, Tz[i], M[i * 3 + 2]);
+    }
+  }
+  const float cC = 4.0f * P.inv_dx;
+  const float f[3] = {ax[0].f, ax[1].f, ax[2].f};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) Cn[i * 3 + jj] = cC * fmaf(-v[i], f[jj], M[i * 3 + jj]);
+}
+
+__device__ __forceinline__ void p2g_stage_values_f(const float x[3], const float v[3], const float Cm[9],
+                                                   const float T[6], int s, float* sl, const DevParams& P) {
+  const float m = P.mass;
+  const Axis a0 = bspline_axis(x[0], P.inv_dx), a1 = bspline_axis(x[1], P.inv_dx), a2 = bspline_axis(x[2], P.inv_dx);
+  const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
+  float Q[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+  const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
+  const float vals[kSlotFields] = {a0.w[0], a0.w[1], a0.w[2], a1.w[0], a1.w[1], a1.w[2], a2.w[0], a2.w[1], a2.w[2],
+                                   m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2),
+                                   m * v[1] - P.dx * (Q[3] * f0 + Q[4] * f1 + Q[5] * f2),
+                                   m * v[2] - P.dx * (Q[6] * f0 + Q[7] * f1 + Q[8] * f2),
+                                   P.dx * Q[0], P.dx * Q[3], P.dx * Q[6],
+                                   P.dx * Q[1], P.dx * Q[4], P.dx * Q[7],
+                                   P.dx * Q[2], P.dx * Q[5], P.dx * Q[8]};
+#pragma unroll
+  for (int k = 0; k < kSlotFields; ++k) sl[k * kSlotStrideF + s] = vals[k];
+}
+
+__device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, int ox, int rows, float accm[9],
+                                                 float accp[9][3]) {
+  const float fox = (float)ox;
+  for (int r = 0; r < rows; ++r) {
+    const int s = r * 64 + my_cell;
+    const float wx = sl[ox * kSlotStrideF + s];
+    const float wyv[3] = {sl[3 * kSlotStrideF + s], sl[4 * kSlotStrideF + s], sl[5 * kSlotStrideF + s]};
+    const float wzv[3] = {sl[6 * kSlotStrideF + s], sl[7 * kSlotStrideF + s], sl[8 * kSlotStrideF + s]};
+    const float ux = fmaf(fox, sl[12 * kSlotStrideF + s], sl[9 * kSlotStrideF + s]);
+    const float uy = fmaf(fox, sl[13 * kSlotStrideF + s], sl[10 * kSlotStrideF + s]);
+    const float uz = fmaf(fox, sl[14 * kSlotStrideF + s], sl[11 * kSlotStrideF + s]);
+    const float q1x = sl[15 * kSlotStrideF + s], q1y = sl[16 * kSlotStrideF + s], q1z = sl[17 * kSlotStrideF + s];
+    const float q2x = sl[18 * kSlotStrideF + s], q2y = sl[19 * kSlotStrideF + s], q2z = sl[20 * kSlotStrideF + s];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) {
+      const float wxy = wx * wyv[oy];
+      const float uyx = fmaf((float)oy, q1x, ux), uyy = fmaf((float)oy, q1y, uy), uyz = fmaf((float)oy, q1z, uz);
+#pragma unroll
+      for (int oz = 0; oz < 3; ++oz) {
+        const float W = wxy * wzv[oz];
+        const int k = oy * 3 + oz;
+        accm[k] += W;
+        accp[k][0] = fmaf(W, fmaf((float)oz, q2x, uyx), accp[k][0]);
+        accp[k][1] = fmaf(W, fmaf((float)oz, q2y, uyy), accp[k][1]);
+        accp[k][2] = fmaf(W, fmaf((float)oz, q2z, uyz), accp[k][2]);
+      }
+    }
+  }
+}
+
+template <bool DO_G2P>
+__global__ void __launch_bounds__(kP2GThreads, NSF_FUSED_MIN_BLOCKS)
+k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
+        int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
+        const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
+        int64_t* d_step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int my_cell = tid & 63;
+  const int ox = tid >> 6;
+  const int nblk = *(volatile int32_t*)&counters[0];
+  if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
+  for (int q = tid; q < 1728; q += kP2GThreads) sm.tbl[q] = g_p2g_tbl[q];
+  for (int q = tid; q < 217; q += kP2GThreads) sm.tbl_off[q] = g_p2g_tbl_off[q];
+  const float cC_unused = 0.0f;
+  (void)cC_unused;
+  while (true) {
+    if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
+    __syncthreads();   // also: previous segment's readers of part/slot are done
+    const int bi = sm.next;
+    if (bi >= nblk) break;
+    const int key = nonempty[bi];
+    const BlockCoord bc = decode_block(key, P);
+    const int s0 = block_start[key], s1 = block_start[key + 1];
+    const int64_t scene_block0 = (int64_t)bc.scene * P.blocks_per_scene;
+    float4* gacc = acc + (int64_t)bc.scene * P.nodes_per_scene;
+    const float4* gvel = vel + (int64_t)bc.scene * P.nodes_per_scene;
+    if (tid < 64) sm.pop[tid] = 0;
+    const int o[3] = {4 * bc.b[0] - 1, 4 * bc.b[1] - 1, 4 * bc.b[2] - 1};   // tile origin (grid node)
+    if (DO_G2P && NSF_FUSED_VTILE) {
+      for (int e = tid; e < kVT * kVT * kVT; e += kP2GThreads) {
+        const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
+        const bool in = i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2];
+        cp_async16_f(&sm.vt[e], in ? gvel + node_index(i, jn, k, P) : gvel, in ? 16 : 0);
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    // ---- phase 1: per particle ----
+    for (int j = s0 + tid; j < s1; j += kP2GThreads) {
+      float* base = S + pbase(j);
+      float xn[3], vn[3], Cn[9], tau[6];
+      if (DO_G2P) {
+        float x[3], F[9], G[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x[a] = base[(PX + a) * 32];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
+        // stencil inside the tile (drift <= 1 cell since the last re-binning)?
+        bool in_tile = NSF_FUSED_VTILE;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const int bb = (int)floorf(x[a] * P.inv_dx - 0.5f);
+          in_tile &= (bb >= o[a]) && (bb + 2 < o[a] + kVT);
+        }
+        if (in_tile) {
+          g2p_gather_tile(x, sm.vt, o, P, vn, Cn);
+#pragma unroll
+          for (int k = 0; k < 9; ++k) G[k] = Cn[k];
+        } else {
+          g2p_gather<0>(x, gvel, P, vn, Cn, G);
+        }
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          xn[a] = x[a] + P.dt * vn[a];
+          const float tt = xn[a] * P.inv_dx;
+          ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
+          base[(PX + a) * 32] = xn[a];
+          base[(PV + a) * 32] = vn[a];
+        }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) base[(PC + k) * 32] = Cn[k];
+        float Ft[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj)
+            Ft[i * 3 + jj] = F[i * 3 + jj] + P.dt * (G[i * 3 + 0] * F[0 * 3 + jj] + G[i * 3 + 1] * F[1 * 3 + jj] +
+                                                     G[i * 3 + 2] * F[2 * 3 + jj]);
+        float FE[9];
+        const float J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+        float chk = xn[0] + xn[1] + xn[2] + vn[0] + vn[1] + vn[2];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) { base[(PF + k) * 32] = FE[k]; chk += FE[k]; }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) { base[(PT + k) * 32] = tau[k]; chk += tau[k]; }
+        if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
+        if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, j); }
+        if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, j); }
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { xn[a] = base[(PX + a) * 32]; vn[a] = base[(PV + a) * 32]; }
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Cn[k] = base[(PC + k) * 32];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) tau[k] = base[(PT + k) * 32];
+      }
+      // ---- P2G of the new state: by cell if still inside this block, else direct ----
+      int c[3];
+      bool core = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        int b = (int)floorf(xn[a] * P.inv_dx - 0.5f);
+        b = min(max(b, 0), P.N[a] - 3);
+        c[a] = b - 4 * bc.b[a];
+        core &= (c[a] >= 0) && (c[a] < 4);
+      }
+      int rank = kRowsF;
+      int cell = 0;
+      if (core) {
+        cell = (c[0] << 4) | (c[1] << 2) | c[2];
+        rank = atomicAdd(&sm.pop[cell], 1);
+      }
+      if (rank < kRowsF) p2g_stage_values_f(xn, vn, Cn, tau, rank * 64 + cell, sm.u.slot, P);
+      else p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+    }
+    __syncthreads();
+    // ---- phase 2: per (cell, stencil plane) register accumulation ----
+    float accm[9], accp[9][3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) { accm[k] = 0.f; accp[k][0] = accp[k][1] = accp[k][2] = 0.f; }
+    p2g_accumulate_f(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], kRowsF), accm, accp);
+    __syncthreads();   // slot buffer becomes the partial buffer
+    float* part = sm.u.part;
+    const float m = P.mass;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const int node = ox * 9 + k;
+      part[(node * 4 + 0) * 64 + my_cell] = accm[k] * m;
+      part[(node * 4 + 1) * 64 + my_cell] = accp[k][0];
+      part[(node * 4 + 2) * 64 + my_cell] = accp[k][1];
+      part[(node * 4 + 3) * 64 + my_cell] = accp[k][2];
+    }
+    __syncthreads();
+    for (int t = tid; t < 216; t += kP2GThreads) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      const int q1 = sm.tbl_off[t + 1];
+      for (int q = sm.tbl_off[t]; q < q1; ++q) {
+        const int pr = sm.tbl[q];
+        const float* pp = part + (pr >> 6) * 256 + (pr & 63);
+        s0 += pp[0];
+        s1 += pp[64];
+        s2 += pp[128];
+        s3 += pp[192];
+      }
+      if (s0 > 0.0f) {
+        const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
+        const int gi = 4 * bc.b[0] + nx, gj = 4 * bc.b[1] + ny, gk = 4 * bc.b[2] + nz;
+        if (gi < P.N[0] && gj < P.N[1] && gk < P.N[2]) {
+          red_add_v4_t(gacc + node_index(gi, gj, gk, P), s0, s1, s2, s3);
+          touch_block(flags, list, list_count, (int)(scene_block0 + block_id(gi >> 2, gj >> 2, gk >> 2, P)));
+        }
+      }
+    }
+  }
+}
+
+// Grid update over the touched blocks: v = mv/m + dt g, walls, plate; the
+// accumulator and the block's flag are cleared.  One warp per listed block; the
+// last CTA to finish empties the list for the next G2P2G.
+__global__ void __launch_bounds__(128)
+k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* __restrict__ list_count,
+                   int* __restrict__ done_count, float4* __restrict__ acc, float4* __restrict__ vel, DevParams P,
+                   const int64_t* __restrict__ d_step, int32_t* __restrict__ counters) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[3] = 0;   // segment ticket of the next k_g2p2g
+  const int nl = *(volatile int*)list_count;
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  const float y_plate = (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)(*d_step) * (double)P.dt));
+  const int bps = (int)P.blocks_per_scene;
+  for (int e = warp; e < nl; e += nwarps) {
+    const int key = list[e];
+    const int scene = key / bps;
+    const BlockCoord bc = decode_block(key, P);
+    const int64_t gb = (int64_t)scene * P.nodes_per_scene + (int64_t)(key - scene * bps) * kBlockNodes;
+    float4 a[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) a[h] = acc[gb + lane + 32 * h];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int l = lane + 32 * h;
+      const int i = bc.b[0] * 4 + (l >> 4), j = bc.b[1] * 4 + ((l >> 2) & 3), k = bc.b[2] * 4 + (l & 3);
+      vel[gb + l] = grid_node_update_t(a[h], i, j, k, P, y_plate);
+      acc[gb + l] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (lane == 0) flags[key] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done_count, 1) == (int)gridDim.x - 1) {
+      *list_count = 0;
+      *done_count = 0;
+    }
+  }
+}
+
+// physical reorder into binned order: out[j] = in[perm[j]] (all 30 fields + id)
+__global__ void k_reorder(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
+                          const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
+                          const int32_t* __restrict__ perm) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int p = perm[j];
+  const float* src = Sin + pbase(p);
+  float* dst = Sout + pbase(j);
+#pragma unroll
+  for (int k = 0; k < kPlanes; ++k) dst[k * 32] = __ldg(src + k * 32);
+  ids_out[j] = __ldg(ids_in + p);
+}
+
+void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
+                  const DevParams& P, DevErr* err, int64_t* d_step) {
+  static bool attr = false;
+  const size_t smem = sizeof(FusedSmem);
+  if (!attr) {
+    cudaFuncSetAttribute(k_g2p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_g2p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int grid = num_sms() * NSF_FUSED_MIN_BLOCKS;
+  if (do_g2p)
+    k_g2p2g<true><<<grid, kP2GThreads, smem, st>>>(S, vel, acc, pb->flags, pb->touched,
+                                                  pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
+                                                  pb->n_nonempty, P, err, d_step);
+  else
+    k_g2p2g<false><<<grid, kP2GThreads, smem, st>>>(S, vel, acc, pb->flags, pb->touched,
+                                                   pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
+                                                   pb->n_nonempty, P, err, d_step);
+}
+
+void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
+                              const int64_t* d_step) {
+  const int grid = num_sms() * 8;
+  k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks,
+                                           pb->touched + pb->total_blocks + 1, acc, vel, P, d_step, pb->n_nonempty);
+}
+
+void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,
+                    const int32_t* perm) {
+  if (n == 0) return;
+  k_reorder<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Sin, Sout, n, ids_in, ids_out, perm);
+}
+
 }  // namespace nsf

@@ -1,6 +1,7 @@
 // Substep pipeline: the order of kernels for one MLS-MPM substep (PAPER.md
 // §3.3) and for the reduced variant.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <cstring>
 #include "pipeline.h"
 
@@ -35,6 +36,11 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   if (cudaMemsetAsync(pb->scan_status, 0, sizeof(unsigned long long) * pb->scan_tiles, v.stream) != cudaSuccess)
     return -1;
   if (cudaMemsetAsync(pb->scan_ticket, 0, sizeof(unsigned long long) * 4, v.stream) != cudaSuccess) return -1;
+  pb->flags = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
+  pb->touched = (int*)pipeline_alloc(h, sizeof(int) * (total_blocks + 4));
+  if (!pb->flags || !pb->touched) return -1;
+  if (cudaMemsetAsync(pb->flags, 0, sizeof(int) * total_blocks, v.stream) != cudaSuccess) return -1;
+  if (cudaMemsetAsync(pb->touched, 0, sizeof(int) * (total_blocks + 4), v.stream) != cudaSuccess) return -1;
   p2g_tables_init(v.stream);
   if (cudaGetLastError() != cudaSuccess) return -1;
   pb->tiled = false;
@@ -56,13 +62,54 @@ nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
 // Invariant of the dense (tiled) path between substeps: keys[] and counts[]
 // describe the particles of the current buffer (written by the last G2P, or
 // here after a load).
+// Re-binning with a physical reorder of buffer `cur` into 1 - cur (fused pipeline):
+// keys + histogram, scan (block_start, non-empty list), scatter (perm), reorder.
+static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
+  const int nxt = 1 - cur;
+  PLAUNCH(h, "bin_keys_hist",
+          launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
+  PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+  PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
+  PLAUNCH(h, "reorder", launch_reorder(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb->perm));
+  return nxt;
+}
+
+static bool fused_enabled() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_PIPELINE");
+    f = (e && strcmp(e, "split") == 0) ? 0 : 1;
+  }
+  return f == 1;
+}
+
+// Invariants between substeps.
+//  split path : keys[] and counts[] describe the particles of the current buffer
+//               (written by the last G2P, or here after a load).
+//  fused path : storage is sorted by block at the last re-binning (segments =
+//               block_start / non-empty list); the accumulator holds P2G of the
+//               current state and `flags` marks its touched blocks; counts = 0.
 nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
   HandleView v = view(h);
   pb->tiled = v.model != NSF_NEURAL_STRESS;
+  pb->fused = pb->tiled && v.P->force_mode == NSF_FORCE_MLS && fused_enabled();
+  pb->since_rebin = 0;
+  pb->launch_total = 0;
   if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess)
     return NSF_ERR_CUDA;
-  if (pb->tiled)
+  if (cudaMemsetAsync(v.acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return NSF_ERR_CUDA;
+  if (cudaMemsetAsync(pb->flags, 0, sizeof(int) * pb->total_blocks, v.stream) != cudaSuccess) return NSF_ERR_CUDA;
+  if (cudaMemsetAsync(pb->touched + pb->total_blocks, 0, sizeof(int) * 4, v.stream) != cudaSuccess)
+    return NSF_ERR_CUDA;
+  if (pb->fused) {
+    const int cur = enqueue_rebin(h, pb, v, 0);
+    set_cur(h, cur);
+    v = view(h);
+    if (cudaMemsetAsync(pb->n_nonempty + 3, 0, sizeof(int32_t), v.stream) != cudaSuccess) return NSF_ERR_CUDA;
+    launch_g2p2g(v.stream, false, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step);   // P2G of state 0
+  } else if (pb->tiled) {
     launch_keys_hist(v.stream, v.n, v.S[0], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
+  }
   if (cudaGetLastError() != cudaSuccess) return NSF_ERR_CUDA;
   return NSF_OK;
 }
@@ -86,15 +133,41 @@ static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v
   PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
 }
 
-// One substep.  Dense full-order path (tiled):
-//   scan -> scatter -> P2G (tiled MLS, or direct for GRADW) -> grid update over
-//   touched blocks -> G2P (sort-on-write into the other buffer, next keys+hist)
-// Reduced (NSF) path: keys+hist -> scan -> MLP -> direct P2G -> grid update over
-//   touched blocks -> direct G2P (points are ~0.1 per cell: tiles do not pay).
-int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur) {
+int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  return (pb->fused && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
+}
+
+void pipeline_advance(nsf_mpm* h, PipelineBuffers* pb, int variant, int launches) {
+  (void)h;
+  pb->since_rebin = variant ? 0 : pb->since_rebin + 1;
+  pb->launch_total += launches;
+}
+
+// One substep.
+//  fused (full-order, MLS): grid update of the flagged blocks -> G2P(n) + P2G(n+1)
+//    in place over storage segments -> (every rebin_every substeps) re-binning
+//    with a physical reorder.
+//  split (GRADW): scan -> scatter -> P2G (direct) -> grid update -> G2P
+//    (sort-on-write into the other buffer, next keys + histogram).
+//  reduced (NSF): keys + hist -> scan -> MLP -> direct P2G -> grid update -> direct G2P
+//    (points are ~0.1 per cell: tiles do not pay).
+int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
   HandleView v = view(h);
   const bool nsf_model = v.model == NSF_NEURAL_STRESS;
   int launches = 0;
+  if (pb->fused) {
+    PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
+    PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
+    launches = 2;
+    int next = cur;
+    if (variant) {
+      next = enqueue_rebin(h, pb, v, cur);
+      launches += v.n > 0 ? 4 : 1;
+    }
+    pb->launches = launches;
+    return next;
+  }
   if (!nsf_model) {
     const int nxt = 1 - cur;
     PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
@@ -109,7 +182,7 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur) {
       launches += (v.n > 0);
     }
     PLAUNCH(h, "grid_update", launch_grid_update_blocks(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
-    PLAUNCH(h, "g2p_tiled",
+    PLAUNCH(h, "g2p",
             launch_g2p_tiled(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb, v.vel, v.scene_off,
                              v.n_scenes, *v.P, v.err, v.d_step));
     launches += 2;
@@ -168,13 +241,24 @@ int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* count
     if (e != cudaSuccess) return -1;
   }
   if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess) return -1;
-  if (pb->tiled) launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
+  if (pb->fused) {
+    // segments must describe the storage order again: re-bin and reorder (the
+    // accumulator only depends on the state, which is unchanged)
+    set_cur(h, enqueue_rebin(h, pb, v, cur));
+    pb->since_rebin = 0;
+  } else if (pb->tiled) {
+    launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, float* out) {
   HandleView v = view(h);
-  (void)pb;
+  if (pb->fused) {
+    // the accumulator already holds P2G of the current state; keep it
+    launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   if (v.model == NSF_NEURAL_STRESS)
     launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
                    v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0);
@@ -187,6 +271,11 @@ int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, flo
 int pipeline_launches_per_substep(nsf_mpm* h, PipelineBuffers* pb) {
   (void)h;
   return pb->launches;
+}
+
+int64_t pipeline_launch_total(nsf_mpm* h, PipelineBuffers* pb) {
+  (void)h;
+  return pb->launch_total;
 }
 
 void pipeline_destroy(nsf_mpm* h, PipelineBuffers* pb) {

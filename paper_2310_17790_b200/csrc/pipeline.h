@@ -25,6 +25,12 @@ struct PipelineBuffers {
   int64_t total_blocks = 0;
   int64_t pitch = 0;
   bool tiled = false;               // dense tiled path (full-order models)
+  bool fused = false;               // fused G2P2G pipeline (full-order, MLS)
+  int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
+  int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
+  int rebin_every = 32;             // fused pipeline: substeps between re-binnings
+  int since_rebin = 0;              // host counter
+  int64_t launch_total = 0;         // kernel launches enqueued since load
   int launches = 0;                 // kernels per substep (last enqueued)
 };
 
@@ -64,7 +70,9 @@ nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch);
 nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb);
 void pipeline_on_mlp(nsf_mpm* h, PipelineBuffers* pb);
 bool pipeline_graphable(nsf_mpm* h, PipelineBuffers* pb);
-int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur);   // returns next buffer or -1
+int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb);             // graph variant of the next substep
+int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant);   // returns next buffer or -1
+void pipeline_advance(nsf_mpm* h, PipelineBuffers* pb, int variant, int launches);          // host bookkeeping after one substep
 void pipeline_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes,
                             int64_t pitch);
 void pipeline_eval_mlp(nsf_mpm* h, PipelineBuffers* pb, int64_t m, const float* planes, int64_t pitch,
@@ -73,6 +81,7 @@ int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* count
                         int on_device);
 int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, float* out);
 int pipeline_launches_per_substep(nsf_mpm* h, PipelineBuffers* pb);
+int64_t pipeline_launch_total(nsf_mpm* h, PipelineBuffers* pb);
 void pipeline_destroy(nsf_mpm* h, PipelineBuffers* pb);
 
 // kernels_bin.cu
@@ -89,6 +98,12 @@ void launch_p2g_tiled(cudaStream_t st, const float* S, int64_t pitch, const int3
 void launch_grid_update_blocks(cudaStream_t st, const PipelineBuffers* pb, float4* acc, float4* vel,
                                const DevParams& P, const int64_t* d_step);
 void p2g_tables_init(cudaStream_t st);
+void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
+                  const DevParams& P, DevErr* err, int64_t* d_step);
+void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
+                              const int64_t* d_step);
+void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,
+                    const int32_t* perm);
 void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                       int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const int64_t* scene_off,
                       int n_scenes, const DevParams& P, DevErr* err, int64_t* d_step);

@@ -66,8 +66,9 @@ struct nsf_mpm {
   size_t staging_bytes = 0;
   // graphs: one captured substep per source buffer (the pipeline may ping-pong
   // particle buffers, so the substep starting from buffer k is graph[k])
-  cudaGraphExec_t graph[2] = {nullptr, nullptr};
-  int graph_next[2] = {0, 1};
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [source buffer][variant]
+  int graph_next[2][2] = {{0, 0}, {1, 1}};
+  int graph_launches[2][2] = {{0, 0}, {0, 0}};   // kernels in each captured graph
   // profiling
   bool profiling = false;
   struct Pending { std::string name; cudaEvent_t a, b; };
@@ -156,10 +157,11 @@ nsf_status to_device(nsf_mpm* h, const void* src, size_t bytes, int on_device, v
 }
 
 void invalidate_graph(nsf_mpm* h) {
-  for (int k = 0; k < 2; ++k) {
-    if (h->graph[k]) cudaGraphExecDestroy(h->graph[k]);
-    h->graph[k] = nullptr;
-  }
+  for (int k = 0; k < 2; ++k)
+    for (int v = 0; v < 2; ++v) {
+      if (h->graph[k][v]) cudaGraphExecDestroy(h->graph[k][v]);
+      h->graph[k][v] = nullptr;
+    }
 }
 
 nsf_status check_device_errors(nsf_mpm* h) {
@@ -481,27 +483,31 @@ nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const floa
 static nsf_status enqueue_substeps(nsf_mpm* h, int32_t n) {
   const bool use_graph = !h->profiling && pipeline_graphable(h, &h->pb);
   for (int i = 0; i < n; ++i) {
+    const int variant = pipeline_variant(h, &h->pb);
     if (!use_graph) {
-      int next = pipeline_substep(h, &h->pb, h->cur);
+      int next = pipeline_substep(h, &h->pb, h->cur, variant);
       if (next < 0) return fail(h, NSF_ERR_CUDA, "substep launch failed");
       CK(cudaGetLastError());
       h->cur = next;
+      pipeline_advance(h, &h->pb, variant, pipeline_launches_per_substep(h, &h->pb));
       continue;
     }
-    int c = h->cur;
-    if (!h->graph[c]) {
+    const int c = h->cur;
+    if (!h->graph[c][variant]) {
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-      int next = pipeline_substep(h, &h->pb, c);
+      int next = pipeline_substep(h, &h->pb, c, variant);
       cudaError_t ec = cudaStreamEndCapture(h->stream, &g);
       if (next < 0 || ec != cudaSuccess)
         return cuda_fail(h, ec == cudaSuccess ? cudaErrorUnknown : ec, "graph capture");
-      CK(cudaGraphInstantiate(&h->graph[c], g, 0));
+      CK(cudaGraphInstantiate(&h->graph[c][variant], g, 0));
       cudaGraphDestroy(g);
-      h->graph_next[c] = next;
+      h->graph_next[c][variant] = next;
+      h->graph_launches[c][variant] = pipeline_launches_per_substep(h, &h->pb);
     }
-    CK(cudaGraphLaunch(h->graph[c], h->stream));
-    h->cur = h->graph_next[c];
+    CK(cudaGraphLaunch(h->graph[c][variant], h->stream));
+    h->cur = h->graph_next[c][variant];
+    pipeline_advance(h, &h->pb, variant, h->graph_launches[c][variant]);
   }
   return NSF_OK;
 }
@@ -671,6 +677,11 @@ int32_t nsf_mpm_kernel_times(nsf_mpm* h, const char** names, double* total_ms, i
 int32_t nsf_mpm_launches_per_substep(nsf_mpm* h) {
   if (!h) return -1;
   return pipeline_launches_per_substep(h, &h->pb);
+}
+
+int64_t nsf_mpm_launch_count(const nsf_mpm* h) {
+  if (!h) return -1;
+  return pipeline_launch_total(const_cast<nsf_mpm*>(h), const_cast<PipelineBuffers*>(&h->pb));
 }
 
 }  // extern "C"
