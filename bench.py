@@ -63,6 +63,7 @@ KERNEL_BYTES_PER_PARTICLE = {
     "bin_keys_hist": 12.0 + 4.0,
     "bin_scatter": 8.0,
 }
+L2_FLUSH_BYTES = 256 << 20              # > 2x the 126 MB L2
 B_ALG_PER_PARTICLE_SUBSTEP = 268.0   # 84 + 48 + 120 + 16
 
 
@@ -254,17 +255,23 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     # ---- timed region: K substeps, inputs resident in HBM ----
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    # L2 (126 MB) is flushed before every timed substep by a 256 MB write on the
+    # same stream, outside the substep's own event pair; the K per-substep device
+    # times are summed.
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     with ClockSampler(local) as clk:
         launches0 = nsf.nsf_mpm_launch_count(sim.h)
-        e0.record(stream)
-        sim.substep(args.steps)
-        e1.record(stream)
-        e1.synchronize()
+        for a, b in ev:
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            a.record(stream)
+            sim.substep(1)
+            b.record(stream)
+        ev[-1][1].synchronize()
     barrier()
-    ms = e0.elapsed_time(e1)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
     launches = nsf.nsf_mpm_launch_count(sim.h) - launches0
     sim.sync()   # surfaces deferred device errors
     if world > 1:
@@ -277,7 +284,10 @@ def run_ours(args):
 
     # ---- per-kernel timing pass (CUDA events around each launch, same stream) ----
     nsf.nsf_mpm_set_profiling(sim.h, True)
-    sim.substep(args.steps)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        sim.substep(1)
     sim.sync()
     kt = nsf.nsf_mpm_kernel_times(sim.h)
     nsf.nsf_mpm_set_profiling(sim.h, False)
@@ -351,8 +361,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenes/, seeded)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                        "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
-                       "replicas": world, "l2": ("inputs larger than L2 (particle state 120 B x n = 120 MB for C3, rewritten every substep)"
-                              if n * 120 > 126e6 else "inputs smaller than L2 (state L2-resident between substeps)"),
+                       "replicas": world, "l2": "flushed before every timed substep (256 MB write outside the per-substep CUDA events)",
                        "step": ("one full substep: binning, NSF MLP (tcgen05), P2G, grid update, G2P"
                                 if args.config == "C5" else
                                 "one full substep: binning, P2G, grid update, G2P + return map")},

@@ -199,6 +199,62 @@ __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float
       }
 }
 
+// Warp-cooperative form of p2g_scatter_direct: the lanes with `direct` set are
+// taken one at a time, their particle broadcast by shuffles, and the active
+// lanes of the warp each scatter some of its 27 nodes (and touch its 8 corner
+// blocks).  A few direct particles per warp then cost ~21 shuffles + one node
+// each instead of serialising 27 reductions while the other lanes idle.
+__device__ __forceinline__ void p2g_scatter_warp(bool direct, const float x[3], const float v[3], const float Cm[9],
+                                                 const float T[6], float4* gbase, int* flags, int* list,
+                                                 int* list_count, int64_t scene_block0, const DevParams& P) {
+  const unsigned act = __activemask();
+  unsigned pend = __ballot_sync(act, direct);
+  if (!pend) return;
+  const int lane = threadIdx.x & 31;
+  const int r = __popc(act & ((1u << lane) - 1u));
+  const int nact = __popc(act);
+  const float m = P.mass;
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    pend &= pend - 1;
+    float px[3], pv[3], pC[9], pT[6];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { px[a] = __shfl_sync(act, x[a], src); pv[a] = __shfl_sync(act, v[a], src); }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) pC[k] = __shfl_sync(act, Cm[k], src);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) pT[k] = __shfl_sync(act, T[k], src);
+    Axis ax[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      ax[a] = bspline_axis(px[a], P.inv_dx);
+      ax[a].base = min(max(ax[a].base, 0), P.N[a] - 3);
+    }
+    const float Tm[9] = {pT[0], pT[5], pT[4], pT[5], pT[1], pT[3], pT[4], pT[3], pT[2]};
+    float Q[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Q[k] = m * pC[k] - P.mls_coef * Tm[k];
+    for (int node = r; node < 27; node += nact) {
+      const int a = node / 9, b = (node / 3) % 3, c = node % 3;
+      const float wa = a == 0 ? ax[0].w[0] : (a == 1 ? ax[0].w[1] : ax[0].w[2]);
+      const float wb = b == 0 ? ax[1].w[0] : (b == 1 ? ax[1].w[1] : ax[1].w[2]);
+      const float wc = c == 0 ? ax[2].w[0] : (c == 1 ? ax[2].w[1] : ax[2].w[2]);
+      const float W = wa * wb * wc;
+      const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
+      const float mv0 = W * (m * pv[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
+      const float mv1 = W * (m * pv[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
+      const float mv2 = W * (m * pv[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
+      red_add_v4_t(gbase + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
+    }
+    // touched blocks: per axis the blocks of base and base+2
+    for (int k = r; k < 8; k += nact) {
+      const int b0 = (ax[0].base + 2 * (k >> 2)) >> 2, b1 = (ax[1].base + 2 * ((k >> 1) & 1)) >> 2,
+                b2 = (ax[2].base + 2 * (k & 1)) >> 2;
+      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+    }
+  }
+}
+
 // thread (my_cell, ox) accumulates its cell's staged rows for stencil plane ox
 __device__ __forceinline__ void p2g_accumulate(const float* sl, int my_cell, int ox, int rows, float accm[9],
                                                float accp[9][3]) {
@@ -710,7 +766,10 @@ static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shar
 #ifndef NSF_FUSED_VTILE
 #define NSF_FUSED_VTILE 1                      // G2P reads a shared-memory velocity tile (else global gathers)
 #endif
-constexpr int kRowsF = NSF_FUSED_VTILE ? 11 : 12;   // staged rows per cell in the fused kernel
+constexpr int kRowsF = NSF_FUSED_VTILE ? 11 : 12;
+#ifndef NSF_WARP_SCATTER
+#define NSF_WARP_SCATTER 1                     // direct scatters are done warp-cooperatively
+#endif   // staged rows per cell in the fused kernel
 constexpr int kSlotStrideF = kRowsF * 64;
 constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-1, 4b+7)
 
@@ -949,7 +1008,11 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
         rank = atomicAdd(&sm.pop[cell], 1);
       }
       if (rank < kRowsF) p2g_stage_values_f(xn, vn, Cn, tau, rank * 64 + cell, sm.u.slot, P);
+#if NSF_WARP_SCATTER
+      p2g_scatter_warp(rank >= kRowsF, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+#else
       else p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+#endif
     }
     __syncthreads();
     // ---- phase 2: per (cell, stencil plane) register accumulation ----

@@ -268,15 +268,18 @@ __device__ __forceinline__ float elastoplastic(const float Ft[9], int model, flo
 // (reading #21: inverted / degenerate F), so conventions stay identical.
 
 // Symmetric 3x3 eigen-decomposition by cyclic Jacobi: A = V diag(A_ii) V^T.
+// Stops once the off-diagonal mass is below 3e-7 of ||A||_F (fp32 round-off
+// level for the small-strain matrices it is applied to, see elastoplastic_fast).
 __device__ __forceinline__ void sym_eig3(float A[3][3], float V[3][3]) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0f : 0.0f;
+  const float off0 = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+  const float tol2 = 1e-13f * (A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2] + 2.0f * off0);
   for (int sweep = 0; sweep < 6; ++sweep) {
-    float off = fabsf(A[0][1]) + fabsf(A[0][2]) + fabsf(A[1][2]);
-    float dia = fabsf(A[0][0]) + fabsf(A[1][1]) + fabsf(A[2][2]);
-    if (off <= 1e-9f * dia) break;
+    const float off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+    if (off <= tol2) break;
     jacobi_pq(A, V, 0, 1);
     jacobi_pq(A, V, 0, 2);
     jacobi_pq(A, V, 1, 2);
@@ -342,23 +345,29 @@ __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model
     for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
     return J;
   }
-  // b = F F^T
+  // S = b - I = F F^T - I, formed as H + H^T + H H^T with H = F - I (exact for
+  // F near I) so that small strains keep their relative precision; b shares
+  // S's eigenvectors and lambda_i(b) = 1 + lambda_i(S).
+  float Hm[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Hm[k] = Ft[k] - ((k & 3) == 0 ? 1.0f : 0.0f);
   float Bm[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = i; j < 3; ++j) {
-      const float s = Ft[i * 3 + 0] * Ft[j * 3 + 0] + Ft[i * 3 + 1] * Ft[j * 3 + 1] + Ft[i * 3 + 2] * Ft[j * 3 + 2];
+      const float s = Hm[i * 3 + j] + Hm[j * 3 + i] +
+                      (Hm[i * 3 + 0] * Hm[j * 3 + 0] + Hm[i * 3 + 1] * Hm[j * 3 + 1] + Hm[i * 3 + 2] * Hm[j * 3 + 2]);
       Bm[i][j] = s;
       Bm[j][i] = s;
     }
   float U[3][3];
   sym_eig3(Bm, U);
-  const float l0 = Bm[0][0], l1 = Bm[1][1], l2 = Bm[2][2];
   const float kFloor2 = 1e-8f;   // sigma >= 1e-4
-  if (!(l0 > kFloor2 && l1 > kFloor2 && l2 > kFloor2)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+  if (!(1.0f + Bm[0][0] > kFloor2 && 1.0f + Bm[1][1] > kFloor2 && 1.0f + Bm[2][2] > kFloor2))
+    return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
   // eps = log sigma = log(lambda)/2
-  const float e[3] = {0.5f * logf(l0), 0.5f * logf(l1), 0.5f * logf(l2)};
+  const float e[3] = {0.5f * log1pf(Bm[0][0]), 0.5f * log1pf(Bm[1][1]), 0.5f * log1pf(Bm[2][2])};
   const float tr = e[0] + e[1] + e[2];
   const float eh[3] = {e[0] - tr * (1.0f / 3.0f), e[1] - tr * (1.0f / 3.0f), e[2] - tr * (1.0f / 3.0f)};
   const float nrm = sqrtf(eh[0] * eh[0] + eh[1] * eh[1] + eh[2] * eh[2]);
