@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnsf_mpm.so")
+LIB_PATH = os.environ.get("NSF_MPM_LIB") or os.path.join(_PKG, "libnsf_mpm.so")   # override: A/B of library builds
 
 NSF_OK, NSF_ERR_INVALID_ARGUMENT, NSF_ERR_OUT_OF_DOMAIN, NSF_ERR_NONFINITE, NSF_ERR_CUDA, \
     NSF_ERR_OUT_OF_MEMORY, NSF_ERR_BAD_STATE = range(7)
