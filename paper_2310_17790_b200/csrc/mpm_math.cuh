@@ -52,10 +52,16 @@ __device__ __forceinline__ float det3(const float A[9]) {
 // (Classic two-sided Jacobi eigenvalue step on S = A^T A.)
 __device__ __forceinline__ void jacobi_pq(float S[3][3], float V[3][3], int p, int q) {
   float apq = S[p][q];
-  if (apq == 0.0f) return;
+  if (!(fabsf(apq) > 1e-18f)) return;
   float app = S[p][p], aqq = S[q][q];
-  float theta = (aqq - app) / (2.0f * apq);
-  float t = copysignf(1.0f, theta) / (fabsf(theta) + sqrtf(fmaf(theta, theta, 1.0f)));
+  // t = tan(angle) = 2 apq sgn(d) / (|d| + sqrt(d^2 + 4 apq^2)), d = aqq - app (the
+  // smaller root of t^2 + 2 theta t - 1 = 0, theta = d / (2 apq); overflow-free).
+  // An approximate t still gives an exactly orthogonal (c, s); the sweep
+  // absorbs the difference.
+  const float d = aqq - app;
+  const float h = fmaf(d, d, 4.0f * apq * apq);
+  const float den = fabsf(d) + h * rsqrtf(h);
+  float t = __fdividef(copysignf(2.0f, d) * apq, den);
   float c = rsqrtf(fmaf(t, t, 1.0f));
   float s = t * c;
   S[p][p] = app - t * apq;
