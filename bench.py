@@ -134,6 +134,23 @@ def dist_env():
     return world, rank, local
 
 
+def max_over_ranks(x, world, device):
+    """Max of a per-rank scalar over all ranks (timings: the job takes as long as
+    its slowest rank).  Identity at world == 1."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_rate(world, units_per_rank, seconds):
+    """Whole-job throughput: every rank processes its own replica of the units."""
+    return world * units_per_rank / seconds
+
+
 def make_scene(name):
     import scenes
     return {"C1": scenes.c1, "C2": scenes.c2, "C3": scenes.c3, "C4": scenes.c4, "C5": scenes.c5}[name]()
@@ -274,13 +291,9 @@ def run_ours(args):
     ms = sum(a.elapsed_time(b) for a, b in ev)
     launches = nsf.nsf_mpm_launch_count(sim.h) - launches0
     sim.sync()   # surfaces deferred device errors
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, dev)
     per_sub = nsf.nsf_mpm_launches_per_substep(sim.h)
-    value = world * n * args.steps / (ms * 1e-3)
+    value = job_rate(world, n * args.steps, ms * 1e-3)
 
     # ---- per-kernel timing pass (CUDA events around each launch, same stream) ----
     nsf.nsf_mpm_set_profiling(sim.h, True)
@@ -331,7 +344,9 @@ def run_ours(args):
     sim.substep(2)
     sim.sync()
     barrier()
-    t0 = time.perf_counter()
+    ea = torch.cuda.Event(enable_timing=True)
+    eb = torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
     for _ in range(e2e_iters):
         nsf.nsf_mpm_load_particles(sim.h, pin["x"].numpy(), pin["v"].numpy(), pin["C"].numpy(), pin["F"].numpy(),
                                    sc.scene_offsets)
@@ -339,14 +354,11 @@ def run_ours(args):
         ptrs = (ctypes.c_void_p * 2)(out_x.data_ptr(), out_v.data_ptr())
         st = lib.nsf_mpm_read_state(sim.h, nsf.NSF_FIELD_X | nsf.NSF_FIELD_V, ptrs, 0)
         assert st == 0, nsf.nsf_mpm_last_error(sim.h)
+    eb.record(stream)
+    eb.synchronize()
     barrier()
-    e2e_s = (time.perf_counter() - t0) / e2e_iters
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * n * args.steps / e2e_s
+    e2e_s = max_over_ranks(ea.elapsed_time(eb) * 1e-3 / e2e_iters, world, dev)
+    e2e_value = job_rate(world, n * args.steps, e2e_s)
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:

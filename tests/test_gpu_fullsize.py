@@ -1,0 +1,85 @@
+"""Full-size GPU parity for C2, C3, C4 (BASELINE.json configs 2-4) in the launch
+configuration bench.py times (fused pipeline, CUDA graphs, re-binning every 32
+substeps), on sampled particles.
+
+One substep of a particle p depends only on the grid nodes of its stencil,
+base_p + {0,1,2}^3, and a node i receives mass only from particles q with
+base_q in [i-2, i] per axis.  So the oracle substep of the particles whose base
+lies within +-2 cells of a sampled particle's base gives that sampled
+particle's exact (fp64) result: a "local oracle" the CPU finishes in seconds at
+any problem size.  Samples are small clusters (27 cells) around seeded random
+particles plus the extremes of the scene (floor, top / plate, fastest).
+Bar: 1e-5 per field, the floors of tests/parity_util.py.
+"""
+import numpy as np
+import pytest
+
+import scenes
+from oracle import mpm
+from tests.parity_util import BAR_STEP, compare, voigt_to_mat
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("x", "v", "C", "F", "tau")
+
+
+@pytest.fixture(scope="module")
+def nsf():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2310_17790_b200 as m
+    return m
+
+
+def _keys(base, N):
+    base = base.astype(np.int64)
+    return (base[:, 0] * N + base[:, 1]) * N + base[:, 2]
+
+
+def _sample_and_support(x, inv_dx, N, rng, n_seeds=12):
+    """Sampled particle indices (clusters of 3^3 cells) and the index set of every
+    particle that can contribute to their stencil nodes."""
+    base = np.floor(x * inv_dx - 0.5).astype(np.int64)
+    keys = _keys(base, N)
+    seeds = list(rng.choice(len(x), n_seeds, replace=False))
+    seeds += [int(np.argmin(x[:, 1])), int(np.argmax(x[:, 1]))]
+    d3 = np.stack(np.meshgrid(*[np.arange(3)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    d5 = np.stack(np.meshgrid(*[np.arange(-2, 3)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    cluster_keys = np.unique(_keys((base[seeds][:, None, :] + d3[None] - 1).reshape(-1, 3), N))
+    samples = np.nonzero(np.isin(keys, cluster_keys))[0]
+    need = np.unique(_keys((base[samples][:, None, :] + d5[None]).reshape(-1, 3), N))
+    support = np.nonzero(np.isin(keys, need))[0]
+    return samples, support
+
+
+def _state(st, idx):
+    out = {k: np.asarray(st[k][idx], np.float64) for k in ("x", "v", "C", "F")}
+    out["C"] = out["C"].reshape(-1, 3, 3)
+    out["F"] = out["F"].reshape(-1, 3, 3)
+    out["tau"] = voigt_to_mat(st["tau"][idx])
+    return out
+
+
+@pytest.mark.parametrize("name,k", [("C2", 33), ("C3", 33), ("C4", 33)])
+def test_full_size_sampled_substep(nsf, name, k):
+    sc = scenes.by_name(name)
+    cfg = sc.cfg
+    sim = nsf.Simulator(cfg)
+    sim.load_scene(sc)
+    sim.substep(k)                     # crosses a re-binning (every 32 substeps)
+    s0 = sim.read()
+    sim.substep(1)
+    sim.sync()
+    s1 = sim.read()
+    sim.close()
+    rng = np.random.default_rng(20231027 + k)
+    samples, support = _sample_and_support(s0["x"], float(cfg.grid_res), cfg.grid_res, rng)
+    assert len(samples) >= 100 and len(support) < 400_000, (len(samples), len(support))
+    P = mpm.params_from_config(cfg)
+    ref = mpm.substep(_state(s0, support), P, k)
+    pos = np.searchsorted(support, samples)        # samples within the support subset
+    ref_s = {f: ref[f][pos] for f in FIELDS}
+    got = _state(s1, samples)
+    errs = compare(got, ref_s, cfg)
+    assert all(e <= BAR_STEP for e in errs.values()), (name, len(samples), errs)
