@@ -766,17 +766,24 @@ static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shar
 #ifndef NSF_FUSED_VTILE
 #define NSF_FUSED_VTILE 1                      // G2P reads a shared-memory velocity tile (else global gathers)
 #endif
-constexpr int kRowsF = NSF_FUSED_VTILE ? 11 : 12;
+constexpr int kRowsF = NSF_FUSED_VTILE ? 11 : 12;   // dense variant: staged rows per cell
+#ifndef NSF_SPARSE_ROWS
+#define NSF_SPARSE_ROWS 6                      // sparse variant (few particles per block)
+#endif
+#ifndef NSF_SPARSE_MIN_BLOCKS
+#define NSF_SPARSE_MIN_BLOCKS 4
+#endif
 #ifndef NSF_WARP_SCATTER
 #define NSF_WARP_SCATTER 1                     // direct scatters are done warp-cooperatively
 #endif   // staged rows per cell in the fused kernel
-constexpr int kSlotStrideF = kRowsF * 64;
+
 constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-1, 4b+7)
 
-struct __align__(16) FusedSmem {
+template <int ROWS>
+struct __align__(16) FusedSmemT {
   float4 vt[NSF_FUSED_VTILE ? kVT * kVT * kVT : 1];   // G2P velocity tile (8 KB)
   union {
-    float slot[kSlotFields * kSlotStrideF];    // [field][row][cell]
+    float slot[kSlotFields * ROWS * 64];       // [field][row][cell]
     float part[27 * 4 * 64];                   // [(node*4 + comp)][cell]
   } u;
   int pop[64];
@@ -784,7 +791,9 @@ struct __align__(16) FusedSmem {
   uint16_t tbl[1728];
   uint16_t tbl_off[218];
 };
-static_assert(sizeof(FusedSmem) + 1024 <= 228 * 1024 / 3, "fused kernel: 3 CTAs per SM");
+static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "fused kernel: CTAs per SM");
+static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPARSE_MIN_BLOCKS,
+              "fused kernel (sparse): CTAs per SM");
 
 __device__ __forceinline__ void cp_async16_f(void* smem, const void* gmem, int src_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -842,6 +851,7 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
     for (int jj = 0; jj < 3; ++jj) Cn[i * 3 + jj] = cC * fmaf(-v[i], f[jj], M[i * 3 + jj]);
 }
 
+template <int kSlotStrideF>
 __device__ __forceinline__ void p2g_stage_values_f(const float x[3], const float v[3], const float Cm[9],
                                                    const float T[6], int s, float* sl, const DevParams& P) {
   const float m = P.mass;
@@ -862,6 +872,7 @@ __device__ __forceinline__ void p2g_stage_values_f(const float x[3], const float
   for (int k = 0; k < kSlotFields; ++k) sl[k * kSlotStrideF + s] = vals[k];
 }
 
+template <int kSlotStrideF>
 __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, int ox, int rows, float accm[9],
                                                  float accp[9][3]) {
   const float fox = (float)ox;
@@ -892,14 +903,14 @@ __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, i
   }
 }
 
-template <bool DO_G2P>
-__global__ void __launch_bounds__(kP2GThreads, NSF_FUSED_MIN_BLOCKS)
+template <bool DO_G2P, int ROWS, int MINB>
+__global__ void __launch_bounds__(kP2GThreads, MINB)
 k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
         int64_t* d_step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
+  FusedSmemT<ROWS>& sm = *reinterpret_cast<FusedSmemT<ROWS>*>(smem_raw);
   const int tid = threadIdx.x;
   const int my_cell = tid & 63;
   const int ox = tid >> 6;
@@ -1001,15 +1012,15 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
         c[a] = b - 4 * bc.b[a];
         core &= (c[a] >= 0) && (c[a] < 4);
       }
-      int rank = kRowsF;
+      int rank = ROWS;
       int cell = 0;
       if (core) {
         cell = (c[0] << 4) | (c[1] << 2) | c[2];
         rank = atomicAdd(&sm.pop[cell], 1);
       }
-      if (rank < kRowsF) p2g_stage_values_f(xn, vn, Cn, tau, rank * 64 + cell, sm.u.slot, P);
+      if (rank < ROWS) p2g_stage_values_f<ROWS * 64>(xn, vn, Cn, tau, rank * 64 + cell, sm.u.slot, P);
 #if NSF_WARP_SCATTER
-      p2g_scatter_warp(rank >= kRowsF, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+      p2g_scatter_warp(rank >= ROWS, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
 #else
       else p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
 #endif
@@ -1019,7 +1030,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     float accm[9], accp[9][3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) { accm[k] = 0.f; accp[k][0] = accp[k][1] = accp[k][2] = 0.f; }
-    p2g_accumulate_f(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], kRowsF), accm, accp);
+    p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
     __syncthreads();   // slot buffer becomes the partial buffer
     float* part = sm.u.part;
     const float m = P.mass;
@@ -1110,24 +1121,29 @@ __global__ void k_reorder(const float* __restrict__ Sin, float* __restrict__ Sou
   ids_out[j] = __ldg(ids_in + p);
 }
 
-void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
-                  const DevParams& P, DevErr* err, int64_t* d_step) {
+template <bool DO_G2P, int ROWS, int MINB>
+static void launch_g2p2g_t(cudaStream_t st, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
+                           const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
-  const size_t smem = sizeof(FusedSmem);
+  const size_t smem = sizeof(FusedSmemT<ROWS>);
   if (!attr) {
-    cudaFuncSetAttribute(k_g2p2g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_g2p2g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const int grid = num_sms() * NSF_FUSED_MIN_BLOCKS;
-  if (do_g2p)
-    k_g2p2g<true><<<grid, kP2GThreads, smem, st>>>(S, vel, acc, pb->flags, pb->touched,
-                                                  pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
-                                                  pb->n_nonempty, P, err, d_step);
-  else
-    k_g2p2g<false><<<grid, kP2GThreads, smem, st>>>(S, vel, acc, pb->flags, pb->touched,
-                                                   pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
-                                                   pb->n_nonempty, P, err, d_step);
+  k_g2p2g<DO_G2P, ROWS, MINB><<<num_sms() * MINB, kP2GThreads, smem, st>>>(
+      S, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
+      pb->n_nonempty, P, err, d_step);
+}
+
+void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
+                  const DevParams& P, DevErr* err, int64_t* d_step) {
+  if (pb->sparse) {
+    if (do_g2p) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
+    else launch_g2p2g_t<false, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
+  } else {
+    if (do_g2p) launch_g2p2g_t<true, kRowsF, NSF_FUSED_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
+    else launch_g2p2g_t<false, kRowsF, NSF_FUSED_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
+  }
 }
 
 void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,

@@ -9,6 +9,9 @@
 
 namespace nsf {
 
+// fused kernel variant threshold: mean particles per non-empty 4^3-cell block
+constexpr int kSparseParticlesPerBlock = 256;
+
 struct PipelineBuffers {
   // binning: block key per particle slot, per-block counts,
   // start offsets (exclusive scan), scatter cursors, permutation, active list
@@ -26,6 +29,7 @@ struct PipelineBuffers {
   int64_t pitch = 0;
   bool tiled = false;               // dense tiled path (full-order models)
   bool fused = false;               // fused G2P2G pipeline (full-order, MLS)
+  bool sparse = false;              // fused kernel variant for few particles per block (chosen at load)
   int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
   int rebin_every = 32;             // fused pipeline: substeps between re-binnings
