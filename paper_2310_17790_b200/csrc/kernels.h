@@ -22,6 +22,13 @@ void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, cons
 void launch_grid_debug(cudaStream_t st, int stage, int64_t total_nodes, const float4* acc, float4* vel,
                        float* out, const DevParams& P, const int64_t* d_step);
 
+// reduced (NSF) substep pieces (point_ops.cuh, kernels_basic.cu)
+struct NsfP2G;
+void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_off, int n_scenes,
+                    const float4* acc0, const float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step,
+                    int* done);
+void launch_nsf_reset_base(cudaStream_t st, int64_t n, float* S);
+
 // kernels_nsf.cu -- neural stress field MLP
 struct MlpDev {
   const uint16_t* W;    // bf16 bits, layer-major [out][in]
@@ -34,12 +41,13 @@ struct MlpDev {
 bool nsf_mlp_tc_supported(const MlpDev& mlp);
 void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
                        int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
-                       const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out);
+                       const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out, const NsfP2G* q);
 // tau (AoSoA tau fields of the particle store, or AoS m x 6 if aos_out) = stress_scale * h(X, z_scene(p) + step*dz);
 // dispatches to the tensor-core kernel when supported (NSF_MLP_SIMT=1 forces the CUDA-core kernel)
 void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X /*3 planes, pitch*/, int64_t xpitch,
                     const int64_t* scene_off, int n_scenes, const float* z, const float* dz, int r,
                     const int64_t* d_step, const MlpDev& mlp, float stress_scale, float* tau_out,
-                    int64_t tau_pitch, int aos_out);
+                    int64_t tau_pitch, int aos_out, const NsfP2G* q = nullptr);
+// ... with q: the same kernel then runs the P2G of each point with its tau
 
 }  // namespace nsf

@@ -6,27 +6,9 @@
 #include <cstdint>
 #include "kernels.h"
 #include "mpm_math.cuh"
+#include "point_ops.cuh"
 
 namespace nsf {
-
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
-               "f"(c), "f"(d)
-               : "memory");
-}
-
-__device__ __forceinline__ void flag_error(DevErr* err, uint32_t bit, int idx) {
-  atomicOr(&err->bits, bit);
-  atomicMin(&err->first_index, idx);
-}
-
-__device__ __forceinline__ bool in_safe_region(float t, int N) {
-  return t >= 0.5f && t < (float)N - 1.5f;
-}
-
-// clamp a base index so that base..base+2 stays inside [0, N)
-__device__ __forceinline__ int clamp_base(int b, int N) { return min(max(b, 0), N - 3); }
 
 // ---------------------------------------------------------------------------
 // unpack AoS caller arrays into SoA planes; ids = load order; tau^0 = tau(F^0)
@@ -161,36 +143,6 @@ void launch_p2g_direct(cudaStream_t st, int64_t n, const float* S, int64_t pitch
   unsigned g = (unsigned)((n + bs - 1) / bs);
   if (P.force_mode == 0) k_p2g_direct<0><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, acc, P);
   else k_p2g_direct<1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, acc, P);
-}
-
-// ---------------------------------------------------------------------------
-// Grid update for one node: v = mv/m + dt g, walls, plate.  Returns (v, m).
-__device__ __forceinline__ float4 grid_node_update(float4 a, int i, int j, int k, const DevParams& P,
-                                                   float y_plate) {
-  float m = a.x;
-  if (!(m > 0.0f)) return make_float4(0.f, 0.f, 0.f, 0.f);
-  float v[3] = {a.y / m + P.dt * P.g[0], a.z / m + P.dt * P.g[1], a.w / m + P.dt * P.g[2]};
-  int idx[3] = {i, j, k};
-#pragma unroll
-  for (int face = 0; face < 6; ++face) {
-    int kind = P.bc[face];
-    if (kind == 0) continue;
-    int axis = face >> 1;
-    bool high = face & 1;
-    bool in = high ? (idx[axis] >= P.N[axis] - P.bc_width) : (idx[axis] < P.bc_width);
-    if (!in) continue;
-    if (kind == 1) { v[0] = v[1] = v[2] = 0.0f; }
-    else v[axis] = high ? fminf(v[axis], 0.0f) : fmaxf(v[axis], 0.0f);
-  }
-  if (P.plate_enabled && (float)j * P.dx >= y_plate) {
-    v[0] = P.plate_v[0]; v[1] = P.plate_v[1]; v[2] = P.plate_v[2];
-  }
-  return make_float4(v[0], v[1], v[2], m);
-}
-
-__device__ __forceinline__ float plate_y(const DevParams& P, int64_t step) {
-  // y_p(t_n) = y0 + v_y * n dt (reading #12); computed in double to keep t exact
-  return (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)step * (double)P.dt));
 }
 
 // dense update over every node of every scene: vel = update(acc); acc = 0
@@ -337,6 +289,93 @@ void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, cons
   } else {
     k_g2p_direct<0, 0><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Reduced (NSF) G2P (see point_ops.cuh): reads acc[step & 1], applies
+// the grid update to each of the 27 stencil nodes, updates x, v, C in place and
+// records the stencil base for the clear in the next P2G.  The last CTA
+// advances the step counter (every thread reads it first).
+__global__ void __launch_bounds__(128) k_g2p_nsf(int64_t n, float* S, const int64_t* __restrict__ scene_off,
+                                                 int n_scenes, const float4* __restrict__ acc0,
+                                                 const float4* __restrict__ acc1, DevParams P, DevErr* err,
+                                                 int64_t* d_step, int* done) {
+  const int64_t step = *(volatile const int64_t*)d_step;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) {
+    const int scene = scene_of(p, scene_off, n_scenes);
+    const float y_pl = plate_y(P, step);
+    float xp[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) xp[a] = S[pbase(p) + (PX + a) * 32];
+    Axis ax[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      ax[a] = bspline_axis(xp[a], P.inv_dx);
+      ax[a].base = clamp_base(ax[a].base, P.N[a]);
+    }
+    S[pbase(p) + PF * 32] = __int_as_float(pack_base(ax[0].base, ax[1].base, ax[2].base));
+    const float4* ab = ((step & 1) ? acc1 : acc0) + (int64_t)scene * P.nodes_per_scene;
+    float v[3] = {0.f, 0.f, 0.f};
+    float Bm[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int i = ax[0].base + a, j = ax[1].base + b, k = ax[2].base + c;
+          const float4 vi = grid_node_update(__ldg(ab + node_index(i, j, k, P)), i, j, k, P, y_pl);
+          const float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
+          const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
+          const float wv0 = W * vi.x, wv1 = W * vi.y, wv2 = W * vi.z;
+          v[0] += wv0; v[1] += wv1; v[2] += wv2;
+          Bm[0] += wv0 * d0; Bm[1] += wv0 * d1; Bm[2] += wv0 * d2;
+          Bm[3] += wv1 * d0; Bm[4] += wv1 * d1; Bm[5] += wv1 * d2;
+          Bm[6] += wv2 * d0; Bm[7] += wv2 * d1; Bm[8] += wv2 * d2;
+        }
+    const float cC = 4.0f * P.inv_dx * P.inv_dx;   // C = 4/dx^2 B (b = 2)
+    bool ok = true, finite = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float xn = xp[a] + P.dt * v[a];
+      ok &= in_safe_region(xn * P.inv_dx, P.N[a]);
+      finite &= isfinite(xn) && isfinite(v[a]);
+      S[pbase(p) + (PX + a) * 32] = xn;
+      S[pbase(p) + (PV + a) * 32] = v[a];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) S[pbase(p) + (PC + k) * 32] = cC * Bm[k];
+    if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
+    if (!finite) flag_error(err, ERR_NONFINITE, (int)p);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      *d_step = step + 1;
+      *done = 0;
+    }
+  }
+}
+
+void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_off, int n_scenes,
+                    const float4* acc0, const float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step,
+                    int* done) {
+  const int bs = 128;
+  unsigned g = (unsigned)((n + bs - 1) / bs);
+  if (g == 0) g = 1;   // still advances the step counter
+  k_g2p_nsf<<<g, bs, 0, st>>>(n, S, scene_off, n_scenes, acc0, acc1, P, err, d_step, done);
+}
+
+// Marks every point's previous stencil as absent (after a load).
+__global__ void k_nsf_reset_base(int64_t n, float* S) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) S[pbase(p) + PF * 32] = __int_as_float(kNoBase);
+}
+
+void launch_nsf_reset_base(cudaStream_t st, int64_t n, float* S) {
+  if (n > 0) k_nsf_reset_base<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, S);
 }
 
 // ---------------------------------------------------------------------------

@@ -215,6 +215,21 @@ void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const in
   k_gather_ids<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, perm, ids, out);
 }
 
+// X reference planes (load order, pitch) -> the AoSoA X planes of the store, slot j
+// holding particle ids[j]
+__global__ void k_gather_xref(int64_t n, const float* __restrict__ X, int64_t pitch, const int32_t* __restrict__ ids,
+                              float* S) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int32_t id = ids[j];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) S[pbase(j) + (PXR + a) * 32] = X[a * pitch + id];
+}
+
+void launch_gather_xref(cudaStream_t st, int64_t n, const float* X, int64_t pitch, const int32_t* ids, float* S) {
+  if (n > 0) k_gather_xref<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, X, pitch, ids, S);
+}
+
 __global__ void k_aos_to_planes(int64_t n, const float* __restrict__ aos, int ncomp, float* planes, int64_t pitch) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;

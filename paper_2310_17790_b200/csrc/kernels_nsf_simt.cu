@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include "kernels.h"
+#include "point_ops.cuh"
 
 namespace nsf {
 
@@ -25,7 +26,7 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
                                                         const float* __restrict__ z, const float* __restrict__ dz,
                                                         int r, const int64_t* __restrict__ d_step, MlpDev mlp,
                                                         float stress_scale, float* __restrict__ tau_out,
-                                                        int64_t tau_pitch, int aos_out) {
+                                                        int64_t tau_pitch, int aos_out, NsfP2G q) {
   extern __shared__ __align__(16) uint16_t sm[];
   const int L = mlp.n_hidden + 1;   // number of linear layers
   const int width = mlp.width;
@@ -49,21 +50,19 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
     int64_t p = tile0 + t;
     bool live = p < n;
     float u[16];
-    int scene = 0;
-    if (live && n_scenes > 1 && scene_off) {
-      int lo = 0, hi = n_scenes;
-      while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (scene_off[mid] <= p) lo = mid; else hi = mid;
-      }
-      scene = lo;
-    }
+    const int scene = live ? scene_of(p, scene_off, n_scenes) : 0;
 #pragma unroll
     for (int a = 0; a < 16; ++a) u[a] = 0.0f;
     if (live) {
-      u[0] = X[0 * xpitch + p];
-      u[1] = X[1 * xpitch + p];
-      u[2] = X[2 * xpitch + p];
+      if (xpitch >= 0) {
+        u[0] = X[0 * xpitch + p];
+        u[1] = X[1 * xpitch + p];
+        u[2] = X[2 * xpitch + p];
+      } else {   // AoSoA planes of the particle store
+        u[0] = X[pbase(p) + 0 * 32];
+        u[1] = X[pbase(p) + 1 * 32];
+        u[2] = X[pbase(p) + 2 * 32];
+      }
       for (int k = 0; k < r; ++k)
         u[3 + k] = z[scene * r + k] + (float)step * (dz ? dz[scene * r + k] : 0.0f);
     }
@@ -127,10 +126,14 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
           if (o < mlp.out_dim) y[o] = fmaf(bf16_bits_to_f32(Wt[k * mlp.out_dim + o]), hk, y[o]);
       }
       if (live) {
+        float tau[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) tau[o] = stress_scale * y[o];
         for (int o = 0; o < mlp.out_dim; ++o) {
-          if (aos_out) tau_out[p * mlp.out_dim + o] = stress_scale * y[o];
-          else tau_out[pbase(p) + o * 32] = stress_scale * y[o];   // AoSoA particle store
+          if (aos_out) tau_out[p * mlp.out_dim + o] = tau[o];
+          else tau_out[pbase(p) + o * 32] = tau[o];   // AoSoA particle store
         }
+        if (q.enabled) nsf_p2g_point(q, p, scene, tau, step);   // reduced P2G
       }
     }
     __syncthreads();
@@ -139,15 +142,19 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
 
 void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
                     int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
-                    const MlpDev& mlp, float stress_scale, float* tau_out, int64_t tau_pitch, int aos_out) {
+                    const MlpDev& mlp, float stress_scale, float* tau_out, int64_t tau_pitch, int aos_out,
+                    const NsfP2G* qp) {
   if (n == 0) return;
+  NsfP2G q{};
+  if (qp) q = *qp;
   static int force_simt = -1;
   if (force_simt < 0) {
     const char* e = getenv("NSF_MLP_SIMT");
     force_simt = (e && atoi(e) != 0) ? 1 : 0;
   }
   if (!force_simt && nsf_mlp_tc_supported(mlp)) {
-    launch_nsf_mlp_tc(st, n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp, stress_scale, tau_out, aos_out);
+    launch_nsf_mlp_tc(st, n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp, stress_scale, tau_out, aos_out,
+                      qp);
     return;
   }
   int L = mlp.n_hidden + 1;
@@ -161,7 +168,7 @@ void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, 
   int64_t tiles = (n + kTile - 1) / kTile;
   int grid = (int)(tiles < 148 ? tiles : 148);
   k_nsf_mlp_simt<<<grid, kTile, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp,
-                                            stress_scale, tau_out, tau_pitch, aos_out);
+                                            stress_scale, tau_out, tau_pitch, aos_out, q);
 }
 
 }  // namespace nsf

@@ -23,6 +23,7 @@
 #include <cstdint>
 #include "kernels.h"
 #include "params.cuh"
+#include "point_ops.cuh"
 
 namespace nsf {
 
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64_t* __restrict__ scene_off,
              int n_scenes, const float* __restrict__ z, const float* __restrict__ dz, int r,
              const int64_t* __restrict__ d_step, MlpDev mlp, float stress_scale, float* __restrict__ tau_out,
-             int aos_out) {
+             int aos_out, NsfP2G q) {
   extern __shared__ uint8_t smem_raw[];
   // align to 1024 B (SWIZZLE_128B atoms)
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -252,19 +253,17 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     float u[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) u[i] = 0.0f;
+    const int scene = live ? scene_of(p, scene_off, n_scenes) : 0;
     if (live) {
-      int scene = 0;
-      if (n_scenes > 1 && scene_off) {
-        int lo = 0, hi = n_scenes;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (scene_off[mid] <= p) lo = mid; else hi = mid;
-        }
-        scene = lo;
+      if (xpitch >= 0) {
+        u[0] = X[0 * xpitch + p];
+        u[1] = X[1 * xpitch + p];
+        u[2] = X[2 * xpitch + p];
+      } else {   // AoSoA planes of the particle store
+        u[0] = X[pbase(p) + 0 * 32];
+        u[1] = X[pbase(p) + 1 * 32];
+        u[2] = X[pbase(p) + 2 * 32];
       }
-      u[0] = X[0 * xpitch + p];
-      u[1] = X[1 * xpitch + p];
-      u[2] = X[2 * xpitch + p];
       for (int k = 0; k < r && k < 13; ++k)
         u[3 + k] = z[scene * r + k] + (float)step * (dz ? dz[scene * r + k] : 0.0f);
     }
@@ -348,11 +347,14 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     float y[8];
     tmem_ld8(o_col + lane_sel, y);
     if (live) {
+      float tau[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) tau[o] = stress_scale * (y[o] + sm.bout[o]);
       for (int o = 0; o < mlp.out_dim && o < 8; ++o) {
-        const float val = stress_scale * (y[o] + sm.bout[o]);
-        if (aos_out) tau_out[p * mlp.out_dim + o] = val;
-        else tau_out[pbase(p) + o * 32] = val;   // AoSoA particle store (tau fields)
+        if (aos_out) tau_out[p * mlp.out_dim + o] = tau[o];
+        else tau_out[pbase(p) + o * 32] = tau[o];   // AoSoA particle store (tau fields)
       }
+      if (q.enabled) nsf_p2g_point(q, p, scene, tau, step);   // reduced P2G, tau from registers
     }
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile
@@ -371,8 +373,10 @@ bool nsf_mlp_tc_supported(const MlpDev& mlp) {
 
 void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
                        int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
-                       const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out) {
+                       const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out, const NsfP2G* qp) {
   if (n == 0) return;
+  NsfP2G q{};
+  if (qp) q = *qp;
   static int n_sms = 0;
   static bool attr = false;
   const size_t smem = sizeof(Smem) + 1024;
@@ -387,7 +391,7 @@ void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitc
   int64_t grid = (tiles + kStreams - 1) / kStreams;
   if (grid > n_sms) grid = n_sms;
   k_nsf_mlp_tc<<<(unsigned)grid, kThreads, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp,
-                                                       stress_scale, tau_out, aos_out);
+                                                       stress_scale, tau_out, aos_out, q);
 }
 
 }  // namespace nsf

@@ -23,6 +23,9 @@ enum Plane : int {
   PC = 6,   // C00..C22 (row-major)
   PF = 15,  // F00..F22
   PT = 24,  // tau Voigt xx,yy,zz,yz,xz,xy
+  // reduced (NSF) model, which has no F: plane PF holds the packed stencil base of
+  // the last P2G, planes PXR..PXR+2 the reference position X (MLP input)
+  PXR = PF + 1,
   kPlanes = 30
 };
 

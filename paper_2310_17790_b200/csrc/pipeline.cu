@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include "pipeline.h"
+#include "point_ops.cuh"
 
 namespace nsf {
 
@@ -74,6 +75,15 @@ static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, i
   return nxt;
 }
 
+static bool nsf_sort_enabled() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_REDUCED_SORT");
+    f = (e && strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return f == 1;
+}
+
 static bool fused_enabled() {
   static int f = -1;
   if (f < 0) {
@@ -119,14 +129,36 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     launch_g2p2g(v.stream, false, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step);   // P2G of state 0
   } else if (pb->tiled) {
     launch_keys_hist(v.stream, v.n, v.S[0], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
+  } else {
+    // reduced path: acc and vel are the two P2G accumulators (point_ops.cuh)
+    if (!pb->nsf_done) {
+      pb->nsf_done = (int*)pipeline_alloc(h, sizeof(int) * 4);
+      if (!pb->nsf_done) return NSF_ERR_OUT_OF_MEMORY;
+    }
+    if (cudaMemsetAsync(pb->nsf_done, 0, sizeof(int) * 4, v.stream) != cudaSuccess ||
+        cudaMemsetAsync(v.vel, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess)
+      return NSF_ERR_CUDA;
+    launch_nsf_reset_base(v.stream, v.n, v.S[0]);
+    // keep the points in block order (periodic re-binning, as the fused path):
+    // neighbouring threads then share stencil nodes in the P2G reductions and
+    // the G2P gathers.  X moves with them (planes PXR..).
+    if (v.X) launch_gather_xref(v.stream, v.n, v.X, v.pitch, v.ids[0], v.S[0]);
+    pb->nsf_sorted = nsf_sort_enabled();
+    pb->since_rebin = 0;
+    if (pb->nsf_sorted && v.n > 0) {
+      const int cur = enqueue_rebin(h, pb, v, 0);
+      set_cur(h, cur);
+    }
   }
   if (cudaGetLastError() != cudaSuccess) return NSF_ERR_CUDA;
   return NSF_OK;
 }
 
 void pipeline_on_mlp(nsf_mpm* h, PipelineBuffers* pb) {
-  (void)h;
   (void)pb;
+  HandleView v = view(h);
+  if (v.model == NSF_NEURAL_STRESS && v.X && v.n > 0)   // X planes of the store follow the points
+    launch_gather_xref(v.stream, v.n, v.X, v.pitch, v.ids[v.cur], v.S[v.cur]);
 }
 
 bool pipeline_graphable(nsf_mpm* h, PipelineBuffers* pb) {
@@ -145,7 +177,7 @@ static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v
 
 int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb) {
   (void)h;
-  return (pb->fused && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
+  return ((pb->fused || pb->nsf_sorted) && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
 }
 
 void pipeline_advance(nsf_mpm* h, PipelineBuffers* pb, int variant, int launches) {
@@ -199,17 +231,25 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
     pb->launches = launches;
     return nxt;
   }
-  PLAUNCH(h, "bin_keys_hist",
-          launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
-  PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+  // reduced: MLP with the P2G of each point in its epilogue ->
+  // G2P with the grid update applied per gathered node
+  NsfP2G q;
+  q.S = v.S[cur];
+  q.acc0 = v.acc;
+  q.acc1 = v.vel;
+  q.P = *v.P;
+  q.enabled = 1;
+  // MLP input X from the store's X planes (xpitch < 0: AoSoA addressing)
   PLAUNCH(h, "nsf_mlp",
-          launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
-                         v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0));
-  PLAUNCH(h, "p2g_direct", launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P));
-  PLAUNCH(h, "grid_update", launch_grid_update_blocks(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
-  PLAUNCH(h, "g2p_direct",
-          launch_g2p_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.vel, *v.P, v.err, v.d_step, 0));
-  launches += (v.n > 0 ? 6 : 3);
+          launch_nsf_mlp(v.stream, v.n, v.S[cur] + PXR * kTileP, -1, v.scene_off, v.n_scenes, v.z, v.dz, v.r,
+                         v.d_step, *v.mlp, v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0, &q));
+  PLAUNCH(h, "g2p_nsf", launch_g2p_nsf(v.stream, v.n, v.S[cur], v.scene_off, v.n_scenes, v.acc, v.vel, *v.P, v.err,
+                                       v.d_step, pb->nsf_done));
+  launches += (v.n > 0 ? 2 : 1);
+  if (variant && v.n > 0) {
+    pb->launches = launches + 4;
+    return enqueue_rebin(h, pb, v, cur);
+  }
   pb->launches = launches;
   return cur;
 }
@@ -269,12 +309,24 @@ int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, flo
     launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
-  if (v.model == NSF_NEURAL_STRESS)
-    launch_nsf_mlp(v.stream, v.n, v.X, v.pitch, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step, *v.mlp,
-                   v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0);
-  launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.acc, *v.P);
-  launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
-  if (cudaMemsetAsync(v.acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return -1;
+  float4* acc = v.acc;
+  float4* vel = v.vel;
+  if (v.model == NSF_NEURAL_STRESS) {
+    // acc / vel hold the reduced path's accumulators: use scratch grids
+    if (!pb->dbg_acc) {
+      pb->dbg_acc = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
+      pb->dbg_vel = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
+      if (!pb->dbg_acc || !pb->dbg_vel) return -1;
+    }
+    acc = pb->dbg_acc;
+    vel = pb->dbg_vel;
+    if (cudaMemsetAsync(acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return -1;
+    launch_nsf_mlp(v.stream, v.n, v.S[cur] + PXR * kTileP, -1, v.scene_off, v.n_scenes, v.z, v.dz, v.r, v.d_step,
+                   *v.mlp, v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0);
+  }
+  launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, acc, *v.P);
+  launch_grid_debug(v.stream, stage, v.total_nodes, acc, vel, out, *v.P, v.d_step);
+  if (cudaMemsetAsync(acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return -1;
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

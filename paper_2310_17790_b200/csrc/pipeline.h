@@ -29,9 +29,13 @@ struct PipelineBuffers {
   int64_t pitch = 0;
   bool tiled = false;               // dense tiled path (full-order models)
   bool fused = false;               // fused G2P2G pipeline (full-order, MLS)
-  bool sparse = false;              // fused kernel variant for few particles per block (chosen at load)
+  bool sparse = false;
+  bool nsf_sorted = false;          // reduced path: points kept in block order (periodic re-binning)              // fused kernel variant for few particles per block (chosen at load)
   int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
+  int* nsf_done = nullptr;          // reduced path: CTA completion counter of the G2P kernel
+  float4* dbg_acc = nullptr;        // reduced path: scratch grids for debug_grid
+  float4* dbg_vel = nullptr;
   int rebin_every = 32;             // fused pipeline: substeps between re-binnings
   int since_rebin = 0;              // host counter
   int64_t launch_total = 0;         // kernel launches enqueued since load
@@ -52,6 +56,7 @@ struct HandleView {
   int64_t total_nodes, total_blocks;
   DevErr* err;
   int64_t* d_step;
+  int cur;                          // current particle buffer
   const MlpDev* mlp;
   const float* X;
   const float* z;
@@ -94,6 +99,7 @@ void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
 void launch_scan(cudaStream_t st, PipelineBuffers* pb);
 void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cursor, int32_t* perm);
 void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out);
+void launch_gather_xref(cudaStream_t st, int64_t n, const float* X, int64_t pitch, const int32_t* ids, float* S);
 void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch);
 
 // kernels_tiled.cu

@@ -1,0 +1,141 @@
+// Per-point device helpers shared by the particle-parallel kernels
+// (kernels_basic.cu) and the reduced-variant MLP kernels (P2G epilogue).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "mpm_math.cuh"
+#include "params.cuh"
+
+namespace nsf {
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void flag_error(DevErr* err, uint32_t bit, int idx) {
+  atomicOr(&err->bits, bit);
+  atomicMin(&err->first_index, idx);
+}
+
+__device__ __forceinline__ bool in_safe_region(float t, int N) {
+  return t >= 0.5f && t < (float)N - 1.5f;
+}
+
+// clamp a base index so that base..base+2 stays inside [0, N)
+__device__ __forceinline__ int clamp_base(int b, int N) { return min(max(b, 0), N - 3); }
+
+// ---------------------------------------------------------------------------
+// Grid update for one node: v = mv/m + dt g, walls, plate.  Returns (v, m).
+__device__ __forceinline__ float4 grid_node_update(float4 a, int i, int j, int k, const DevParams& P,
+                                                   float y_plate) {
+  float m = a.x;
+  if (!(m > 0.0f)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  float v[3] = {a.y / m + P.dt * P.g[0], a.z / m + P.dt * P.g[1], a.w / m + P.dt * P.g[2]};
+  int idx[3] = {i, j, k};
+#pragma unroll
+  for (int face = 0; face < 6; ++face) {
+    int kind = P.bc[face];
+    if (kind == 0) continue;
+    int axis = face >> 1;
+    bool high = face & 1;
+    bool in = high ? (idx[axis] >= P.N[axis] - P.bc_width) : (idx[axis] < P.bc_width);
+    if (!in) continue;
+    if (kind == 1) { v[0] = v[1] = v[2] = 0.0f; }
+    else v[axis] = high ? fminf(v[axis], 0.0f) : fmaxf(v[axis], 0.0f);
+  }
+  if (P.plate_enabled && (float)j * P.dx >= y_plate) {
+    v[0] = P.plate_v[0]; v[1] = P.plate_v[1]; v[2] = P.plate_v[2];
+  }
+  return make_float4(v[0], v[1], v[2], m);
+}
+
+__device__ __forceinline__ float plate_y(const DevParams& P, int64_t step) {
+  // y_p(t_n) = y0 + v_y * n dt (reading #12); computed in double to keep t exact
+  return (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)step * (double)P.dt));
+}
+
+// ---------------------------------------------------------------------------
+// Reduced (NSF) substep: points carry x, v, C; tau comes from
+// the MLP.  Two accumulators alternate by step parity: P2G(n) reduces into
+// acc[n & 1]; G2P(n) reads acc[n & 1] and applies the grid update node by
+// node; P2G(n+1) clears, in acc[n & 1], the 27 nodes of each point's stencil at
+// x_n (its base, packed into the otherwise unused F plane by G2P(n)).
+struct NsfP2G {
+  float* S;            // particle store (AoSoA)
+  float4* acc0;
+  float4* acc1;
+  DevParams P;
+  int enabled;         // 0: MLP only (tau to the store / AoS output)
+};
+
+constexpr int kNoBase = -1;
+
+__device__ __forceinline__ int pack_base(int b0, int b1, int b2) { return (b0 << 20) | (b1 << 10) | b2; }
+
+// P2G of point p of `scene` with Kirchhoff stress tau (Voigt), MLS force
+// (reading #1), and the clear of its previous stencil.
+__device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int64_t p, int scene, const float tp[6],
+                                              int64_t step) {
+  const DevParams& P = q.P;
+  float* S = q.S;
+  const int64_t so = (int64_t)scene * P.nodes_per_scene;
+  float4* out = ((step & 1) ? q.acc1 : q.acc0) + so;
+  float4* clr = ((step & 1) ? q.acc0 : q.acc1) + so;
+  const int packed = __float_as_int(S[pbase(p) + PF * 32]);
+  if (packed != kNoBase) {
+    const int c0 = packed >> 20, c1 = (packed >> 10) & 1023, c2 = packed & 1023;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) clr[node_index(c0 + a, c1 + b, c2 + c, P)] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float xp[3], vp[3], Cp[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { xp[a] = S[pbase(p) + (PX + a) * 32]; vp[a] = S[pbase(p) + (PV + a) * 32]; }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Cp[k] = S[pbase(p) + (PC + k) * 32];
+  Axis ax[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    ax[a] = bspline_axis(xp[a], P.inv_dx);
+    ax[a].base = clamp_base(ax[a].base, P.N[a]);
+  }
+  const float m = P.mass;
+  const float T[9] = {tp[0], tp[5], tp[4], tp[5], tp[1], tp[3], tp[4], tp[3], tp[2]};
+  float Q[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Q[k] = m * Cp[k] - P.mls_coef * T[k];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
+        const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
+        const float mv0 = W * (m * vp[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
+        const float mv1 = W * (m * vp[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
+        const float mv2 = W * (m * vp[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
+        red_add_v4(out + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
+      }
+}
+
+// scene of point p (binary search over the scene offsets)
+__device__ __forceinline__ int scene_of(int64_t p, const int64_t* scene_off, int n_scenes) {
+  int lo = 0;
+  if (n_scenes > 1 && scene_off) {
+    int hi = n_scenes;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= p) lo = mid; else hi = mid;
+    }
+  }
+  return lo;
+}
+
+}  // namespace nsf

@@ -705,6 +705,7 @@ HandleView view(nsf_mpm* h) {
   v.total_blocks = h->total_blocks;
   v.err = h->err;
   v.d_step = h->d_step;
+  v.cur = h->cur;
   v.mlp = &h->mlp;
   v.X = h->X;
   v.z = h->z;
