@@ -25,8 +25,7 @@ void launch_grid_debug(cudaStream_t st, int stage, int64_t total_nodes, const fl
 // reduced (NSF) substep pieces (point_ops.cuh, kernels_basic.cu)
 struct NsfP2G;
 void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_off, int n_scenes,
-                    const float4* acc0, const float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step,
-                    int* done);
+                    float4* acc0, float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step, int* done);
 void launch_nsf_reset_base(cudaStream_t st, int64_t n, float* S);
 
 // kernels_nsf.cu -- neural stress field MLP

@@ -293,47 +293,92 @@ void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, cons
 
 // ---------------------------------------------------------------------------
 // Reduced (NSF) G2P (see point_ops.cuh): reads acc[step & 1], applies
-// the grid update to each of the 27 stencil nodes, updates x, v, C in place and
-// records the stencil base for the clear in the next P2G.  The last CTA
-// advances the step counter (every thread reads it first).
+// the grid update to each of the 27 stencil nodes, updates x, v, C in place,
+// clears the point's previous stencil in acc[(step + 1) & 1] and records the
+// current base.  The last CTA advances the step counter (every thread reads it
+// first).
 __global__ void __launch_bounds__(128) k_g2p_nsf(int64_t n, float* S, const int64_t* __restrict__ scene_off,
-                                                 int n_scenes, const float4* __restrict__ acc0,
-                                                 const float4* __restrict__ acc1, DevParams P, DevErr* err,
+                                                 int n_scenes, float4* acc0, float4* acc1, DevParams P, DevErr* err,
                                                  int64_t* d_step, int* done) {
   const int64_t step = *(volatile const int64_t*)d_step;
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p < n) {
+  // reverse sweep: the MLP/P2G kernel just reduced into the accumulator in
+  // forward point order, so its most recent (L2-resident) lines come first
+  const int64_t p = n - 1 - (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  if (p >= 0) {
     const int scene = scene_of(p, scene_off, n_scenes);
     const float y_pl = plate_y(P, step);
+    const int64_t so = (int64_t)scene * P.nodes_per_scene;
     float xp[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) xp[a] = S[pbase(p) + (PX + a) * 32];
+    const int packed = __float_as_int(S[pbase(p) + PF * 32]);
     Axis ax[3];
+    int base[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       ax[a] = bspline_axis(xp[a], P.inv_dx);
-      ax[a].base = clamp_base(ax[a].base, P.N[a]);
+      base[a] = ax[a].base = clamp_base(ax[a].base, P.N[a]);
     }
-    S[pbase(p) + PF * 32] = __int_as_float(pack_base(ax[0].base, ax[1].base, ax[2].base));
-    const float4* ab = ((step & 1) ? acc1 : acc0) + (int64_t)scene * P.nodes_per_scene;
+    S[pbase(p) + PF * 32] = __int_as_float(pack_base(base[0], base[1], base[2]));
+    int X[3], Y[3], Z[3];
+    if (packed != kNoBase) {   // previous stencil, in the accumulator P2G(step + 1) will use
+      const int pb_[3] = {packed >> 20, (packed >> 10) & 1023, packed & 1023};
+      stencil_offsets(pb_, P, X, Y, Z);
+      float4* clr = ((step & 1) ? acc0 : acc1) + so;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) clr[X[a] + Y[b] + Z[c]] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    stencil_offsets(base, P, X, Y, Z);
+    const float4* ab = ((step & 1) ? acc1 : acc0) + so;
+    // interior stencil (no wall band, no plate): the node update is v = mv/m + dt g
+    bool simple = !(P.plate_enabled && (float)(base[1] + 2) * P.dx >= y_pl);
+#pragma unroll
+    for (int face = 0; face < 6; ++face) {
+      const int axis = face >> 1;
+      const bool hit = (face & 1) ? (base[axis] + 2 >= P.N[axis] - P.bc_width) : (base[axis] < P.bc_width);
+      simple &= !(P.bc[face] != 0 && hit);
+    }
     float v[3] = {0.f, 0.f, 0.f};
     float Bm[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    auto accumulate = [&](int a, int b, int c, float4 vi) {
+      const float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
+      const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
+      const float wv0 = W * vi.x, wv1 = W * vi.y, wv2 = W * vi.z;
+      v[0] += wv0; v[1] += wv1; v[2] += wv2;
+      Bm[0] += wv0 * d0; Bm[1] += wv0 * d1; Bm[2] += wv0 * d2;
+      Bm[3] += wv1 * d0; Bm[4] += wv1 * d1; Bm[5] += wv1 * d2;
+      Bm[6] += wv2 * d0; Bm[7] += wv2 * d1; Bm[8] += wv2 * d2;
+    };
+    if (simple) {
+      const float gx = P.dt * P.g[0], gy = P.dt * P.g[1], gz = P.dt * P.g[2];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a) {
+        float4 an[9];
 #pragma unroll
-      for (int b = 0; b < 3; ++b)
+        for (int q = 0; q < 9; ++q) an[q] = __ldg(ab + (X[a] + Y[q / 3] + Z[q % 3]));   // 9 loads in flight
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int i = ax[0].base + a, j = ax[1].base + b, k = ax[2].base + c;
-          const float4 vi = grid_node_update(__ldg(ab + node_index(i, j, k, P)), i, j, k, P, y_pl);
-          const float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
-          const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
-          const float wv0 = W * vi.x, wv1 = W * vi.y, wv2 = W * vi.z;
-          v[0] += wv0; v[1] += wv1; v[2] += wv2;
-          Bm[0] += wv0 * d0; Bm[1] += wv0 * d1; Bm[2] += wv0 * d2;
-          Bm[3] += wv1 * d0; Bm[4] += wv1 * d1; Bm[5] += wv1 * d2;
-          Bm[6] += wv2 * d0; Bm[7] += wv2 * d1; Bm[8] += wv2 * d2;
+        for (int q = 0; q < 9; ++q) {
+          const float rm = an[q].x > 0.0f ? __frcp_rn(an[q].x) : 0.0f;
+          const float4 vi = an[q].x > 0.0f ? make_float4(fmaf(an[q].y, rm, gx), fmaf(an[q].z, rm, gy),
+                                                         fmaf(an[q].w, rm, gz), an[q].x)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          accumulate(a, q / 3, q % 3, vi);
         }
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            accumulate(a, b, c, grid_node_update(__ldg(ab + (X[a] + Y[b] + Z[c])), base[0] + a, base[1] + b,
+                                                 base[2] + c, P, y_pl));
+    }
     const float cC = 4.0f * P.inv_dx * P.inv_dx;   // C = 4/dx^2 B (b = 2)
     bool ok = true, finite = true;
 #pragma unroll
@@ -360,8 +405,7 @@ __global__ void __launch_bounds__(128) k_g2p_nsf(int64_t n, float* S, const int6
 }
 
 void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_off, int n_scenes,
-                    const float4* acc0, const float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step,
-                    int* done) {
+                    float4* acc0, float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step, int* done) {
   const int bs = 128;
   unsigned g = (unsigned)((n + bs - 1) / bs);
   if (g == 0) g = 1;   // still advances the step counter

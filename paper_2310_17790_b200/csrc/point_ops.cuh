@@ -33,7 +33,8 @@ __device__ __forceinline__ float4 grid_node_update(float4 a, int i, int j, int k
                                                    float y_plate) {
   float m = a.x;
   if (!(m > 0.0f)) return make_float4(0.f, 0.f, 0.f, 0.f);
-  float v[3] = {a.y / m + P.dt * P.g[0], a.z / m + P.dt * P.g[1], a.w / m + P.dt * P.g[2]};
+  const float rm = __frcp_rn(m);   // v = (m v) (1/m) + dt g: the form every reduced-path gather uses
+  float v[3] = {fmaf(a.y, rm, P.dt * P.g[0]), fmaf(a.z, rm, P.dt * P.g[1]), fmaf(a.w, rm, P.dt * P.g[2])};
   int idx[3] = {i, j, k};
 #pragma unroll
   for (int face = 0; face < 6; ++face) {
@@ -61,8 +62,9 @@ __device__ __forceinline__ float plate_y(const DevParams& P, int64_t step) {
 // Reduced (NSF) substep: points carry x, v, C; tau comes from
 // the MLP.  Two accumulators alternate by step parity: P2G(n) reduces into
 // acc[n & 1]; G2P(n) reads acc[n & 1] and applies the grid update node by
-// node; P2G(n+1) clears, in acc[n & 1], the 27 nodes of each point's stencil at
-// x_n (its base, packed into the otherwise unused F plane by G2P(n)).
+// node, and clears in acc[(n+1) & 1] (read by G2P(n-1), next written by P2G(n+1))
+// the 27 nodes of each point's stencil at x_{n-1}: the base G2P(n-1) packed into
+// the otherwise unused F plane.
 struct NsfP2G {
   float* S;            // particle store (AoSoA)
   float4* acc0;
@@ -83,17 +85,6 @@ __device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int64_t p, int sc
   float* S = q.S;
   const int64_t so = (int64_t)scene * P.nodes_per_scene;
   float4* out = ((step & 1) ? q.acc1 : q.acc0) + so;
-  float4* clr = ((step & 1) ? q.acc0 : q.acc1) + so;
-  const int packed = __float_as_int(S[pbase(p) + PF * 32]);
-  if (packed != kNoBase) {
-    const int c0 = packed >> 20, c1 = (packed >> 10) & 1023, c2 = packed & 1023;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) clr[node_index(c0 + a, c1 + b, c2 + c, P)] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
   float xp[3], vp[3], Cp[9];
 #pragma unroll
   for (int a = 0; a < 3; ++a) { xp[a] = S[pbase(p) + (PX + a) * 32]; vp[a] = S[pbase(p) + (PV + a) * 32]; }
@@ -123,6 +114,19 @@ __device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int64_t p, int sc
         const float mv2 = W * (m * vp[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
         red_add_v4(out + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
       }
+}
+
+// Blocked-layout offsets of the 3 stencil nodes per axis (node_index split per
+// axis, 32-bit: one scene's grid has < 2^31 nodes)
+__device__ __forceinline__ void stencil_offsets(const int base[3], const DevParams& P, int X[3], int Y[3], int Z[3]) {
+  const int plane = P.NB[1] * P.NB[2] * kBlockNodes;
+#pragma unroll
+  for (int o = 0; o < 3; ++o) {
+    const int i = base[0] + o, j = base[1] + o, k = base[2] + o;
+    X[o] = (i >> 2) * plane + ((i & 3) << 4);
+    Y[o] = (j >> 2) * (P.NB[2] * kBlockNodes) + ((j & 3) << 2);
+    Z[o] = (k >> 2) * kBlockNodes + (k & 3);
+  }
 }
 
 // scene of point p (binary search over the scene offsets)
