@@ -766,7 +766,16 @@ static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shar
 #ifndef NSF_FUSED_VTILE
 #define NSF_FUSED_VTILE 1                      // G2P reads a shared-memory velocity tile (else global gathers)
 #endif
-constexpr int kRowsF = NSF_FUSED_VTILE ? 11 : 12;   // dense variant: staged rows per cell
+#ifndef NSF_DENSE_THREADS
+#define NSF_DENSE_THREADS 192                  // dense variant: threads per CTA (>= 192)
+#endif
+#ifndef NSF_DENSE_MIN_BLOCKS
+#define NSF_DENSE_MIN_BLOCKS NSF_FUSED_MIN_BLOCKS   // dense variant: CTAs per SM
+#endif
+#ifndef NSF_DENSE_ROWS
+#define NSF_DENSE_ROWS (NSF_FUSED_VTILE ? 11 : 12)
+#endif
+constexpr int kRowsF = NSF_DENSE_ROWS;         // dense variant: staged rows per cell
 #ifndef NSF_SPARSE_ROWS
 #define NSF_SPARSE_ROWS 6                      // sparse variant (few particles per block)
 #endif
@@ -791,7 +800,7 @@ struct __align__(16) FusedSmemT {
   uint16_t tbl[1728];
   uint16_t tbl_off[218];
 };
-static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "fused kernel: CTAs per SM");
+static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_DENSE_MIN_BLOCKS, "fused kernel: CTAs per SM");
 static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPARSE_MIN_BLOCKS,
               "fused kernel (sparse): CTAs per SM");
 
@@ -903,8 +912,8 @@ __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, i
   }
 }
 
-template <bool DO_G2P, int ROWS, int MINB>
-__global__ void __launch_bounds__(kP2GThreads, MINB)
+template <bool DO_G2P, int ROWS, int MINB, int NT>
+__global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
@@ -916,8 +925,8 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
   const int ox = tid >> 6;
   const int nblk = *(volatile int32_t*)&counters[0];
   if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
-  for (int q = tid; q < 1728; q += kP2GThreads) sm.tbl[q] = g_p2g_tbl[q];
-  for (int q = tid; q < 217; q += kP2GThreads) sm.tbl_off[q] = g_p2g_tbl_off[q];
+  for (int q = tid; q < 1728; q += NT) sm.tbl[q] = g_p2g_tbl[q];
+  for (int q = tid; q < 217; q += NT) sm.tbl_off[q] = g_p2g_tbl_off[q];
   const float cC_unused = 0.0f;
   (void)cC_unused;
   while (true) {
@@ -934,7 +943,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     if (tid < 64) sm.pop[tid] = 0;
     const int o[3] = {4 * bc.b[0] - 1, 4 * bc.b[1] - 1, 4 * bc.b[2] - 1};   // tile origin (grid node)
     if (DO_G2P && NSF_FUSED_VTILE) {
-      for (int e = tid; e < kVT * kVT * kVT; e += kP2GThreads) {
+      for (int e = tid; e < kVT * kVT * kVT; e += NT) {
         const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
         const bool in = i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2];
         cp_async16_f(&sm.vt[e], in ? gvel + node_index(i, jn, k, P) : gvel, in ? 16 : 0);
@@ -943,7 +952,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     }
     __syncthreads();
     // ---- phase 1: per particle ----
-    for (int j = s0 + tid; j < s1; j += kP2GThreads) {
+    for (int j = s0 + tid; j < s1; j += NT) {
       float* base = S + pbase(j);
       float xn[3], vn[3], Cn[9], tau[6];
       if (DO_G2P) {
@@ -1030,12 +1039,13 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     float accm[9], accp[9][3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) { accm[k] = 0.f; accp[k][0] = accp[k][1] = accp[k][2] = 0.f; }
-    p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
+    if (ox < 3) p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
     __syncthreads();   // slot buffer becomes the partial buffer
     float* part = sm.u.part;
     const float m = P.mass;
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
+      if (ox >= 3) break;   // threads beyond 64 cells x 3 planes (NT > 192) only stage and reduce
       const int node = ox * 9 + k;
       part[(node * 4 + 0) * 64 + my_cell] = accm[k] * m;
       part[(node * 4 + 1) * 64 + my_cell] = accp[k][0];
@@ -1043,7 +1053,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
       part[(node * 4 + 3) * 64 + my_cell] = accp[k][2];
     }
     __syncthreads();
-    for (int t = tid; t < 216; t += kP2GThreads) {
+    for (int t = tid; t < 216; t += NT) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       const int q1 = sm.tbl_off[t + 1];
       for (int q = sm.tbl_off[t]; q < q1; ++q) {
@@ -1121,16 +1131,16 @@ __global__ void k_reorder(const float* __restrict__ Sin, float* __restrict__ Sou
   ids_out[j] = __ldg(ids_in + p);
 }
 
-template <bool DO_G2P, int ROWS, int MINB>
+template <bool DO_G2P, int ROWS, int MINB, int NT>
 static void launch_g2p2g_t(cudaStream_t st, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
   const size_t smem = sizeof(FusedSmemT<ROWS>);
   if (!attr) {
-    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_g2p2g<DO_G2P, ROWS, MINB><<<num_sms() * MINB, kP2GThreads, smem, st>>>(
+  k_g2p2g<DO_G2P, ROWS, MINB, NT><<<num_sms() * MINB, NT, smem, st>>>(
       S, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
       pb->n_nonempty, P, err, d_step);
 }
@@ -1138,11 +1148,11 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const float4* vel, float4*
 void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
                   const DevParams& P, DevErr* err, int64_t* d_step) {
   if (pb->sparse) {
-    if (do_g2p) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
-    else launch_g2p2g_t<false, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
+    if (do_g2p) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192>(st, S, vel, acc, pb, P, err, d_step);
+    else launch_g2p2g_t<false, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192>(st, S, vel, acc, pb, P, err, d_step);
   } else {
-    if (do_g2p) launch_g2p2g_t<true, kRowsF, NSF_FUSED_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
-    else launch_g2p2g_t<false, kRowsF, NSF_FUSED_MIN_BLOCKS>(st, S, vel, acc, pb, P, err, d_step);
+    if (do_g2p) launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS>(st, S, vel, acc, pb, P, err, d_step);
+    else launch_g2p2g_t<false, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS>(st, S, vel, acc, pb, P, err, d_step);
   }
 }
 
