@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(128) k_g2p_nsf(int64_t n, float* S, const int6
   // forward point order, so its most recent (L2-resident) lines come first
   const int64_t p = n - 1 - (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
   if (p >= 0) {
-    const int scene = scene_of(p, scene_off, n_scenes);
+    const int scene = scene_of(p, scene_off, n_scenes, n);
     const float y_pl = plate_y(P, step);
     const int64_t so = (int64_t)scene * P.nodes_per_scene;
     float xp[3];

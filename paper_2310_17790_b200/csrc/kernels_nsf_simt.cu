@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
     int64_t p = tile0 + t;
     bool live = p < n;
     float u[16];
-    const int scene = live ? scene_of(p, scene_off, n_scenes) : 0;
+    const int scene = live ? scene_of(p, scene_off, n_scenes, n) : 0;
 #pragma unroll
     for (int a = 0; a < 16; ++a) u[a] = 0.0f;
     if (live) {
@@ -133,7 +133,11 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
           if (aos_out) tau_out[p * mlp.out_dim + o] = tau[o];
           else tau_out[pbase(p) + o * 32] = tau[o];   // AoSoA particle store
         }
-        if (q.enabled) nsf_p2g_point(q, p, scene, tau, step);   // reduced P2G
+        if (q.enabled) {   // reduced P2G
+          float xp[3], vp[3], Cp[9];
+          nsf_load_point(q.S, p, xp, vp, Cp);
+          nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);
+        }
       }
     }
     __syncthreads();

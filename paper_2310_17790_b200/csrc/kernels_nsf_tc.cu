@@ -159,17 +159,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// write 32 activations (columns c0..c0+31) of row `row` into the swizzled A tile at shared address `tile`
+// write 32 activations (columns c0..c0+31, c0 % 32 == 0) of row `row` into the swizzled A tile at shared
+// address `tile`: 16-byte chunk (c0 % 64) / 8 + q of the row's 128-byte line, XORed with row % 8
 __device__ __forceinline__ void store_act32(uint32_t tile, int row, int c0, const float* h) {
+  const uint32_t rbase = tile + (uint32_t)((c0 >> 6) * (kM * 128) + row * 128);
+  const uint32_t sw = (uint32_t)(row & 7), cb = (uint32_t)((c0 & 63) >> 3);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int k = c0 + 8 * q;
     uint4 u;
     u.x = pack_bf16(h[8 * q + 0], h[8 * q + 1]);
     u.y = pack_bf16(h[8 * q + 2], h[8 * q + 3]);
     u.z = pack_bf16(h[8 * q + 4], h[8 * q + 5]);
     u.w = pack_bf16(h[8 * q + 6], h[8 * q + 7]);
-    sts_u4(tile + sw128_offset(row, k, kM), u);
+    sts_u4(rbase + (((cb + (uint32_t)q) ^ sw) << 4), u);
   }
 }
 
@@ -253,7 +255,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     float u[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) u[i] = 0.0f;
-    const int scene = live ? scene_of(p, scene_off, n_scenes) : 0;
+    const int scene = live ? scene_of(p, scene_off, n_scenes, n) : 0;
     if (live) {
       if (xpitch >= 0) {
         u[0] = X[0 * xpitch + p];
@@ -341,6 +343,9 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       }
       mma_commit(&sm.bar[s]);
     }
+    // the point's P2G inputs load while the output MMA runs
+    float xp[3], vp[3], Cp[9];
+    if (q.enabled && live) nsf_load_point(q.S, p, xp, vp, Cp);
     mbar_wait(&sm.bar[s], phase);
     phase ^= 1;
     fence_after();
@@ -354,7 +359,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
         if (aos_out) tau_out[p * mlp.out_dim + o] = tau[o];
         else tau_out[pbase(p) + o * 32] = tau[o];   // AoSoA particle store (tau fields)
       }
-      if (q.enabled) nsf_p2g_point(q, p, scene, tau, step);   // reduced P2G, tau from registers
+      if (q.enabled) nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);   // reduced P2G, tau from registers
     }
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile

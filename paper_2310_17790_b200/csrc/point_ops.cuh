@@ -58,6 +58,35 @@ __device__ __forceinline__ float plate_y(const DevParams& P, int64_t step) {
   return (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)step * (double)P.dt));
 }
 
+// Blocked-layout offsets of the 3 stencil nodes per axis (node_index split per
+// axis, 32-bit: one scene's grid has < 2^31 nodes)
+__device__ __forceinline__ void stencil_offsets(const int base[3], const DevParams& P, int X[3], int Y[3], int Z[3]) {
+  const int plane = P.NB[1] * P.NB[2] * kBlockNodes;
+#pragma unroll
+  for (int o = 0; o < 3; ++o) {
+    const int i = base[0] + o, j = base[1] + o, k = base[2] + o;
+    X[o] = (i >> 2) * plane + ((i & 3) << 4);
+    Y[o] = (j >> 2) * (P.NB[2] * kBlockNodes) + ((j & 3) << 2);
+    Z[o] = (k >> 2) * kBlockNodes + (k & 3);
+  }
+}
+
+// scene of point p among n: first the guess of equal-size scenes (two
+// independent loads), else a binary search over the scene offsets
+__device__ __forceinline__ int scene_of(int64_t p, const int64_t* scene_off, int n_scenes, int64_t n) {
+  int lo = 0;
+  if (n_scenes > 1 && scene_off) {
+    const int g = (int)min((int64_t)n_scenes - 1, p * n_scenes / (n > 0 ? n : 1));
+    if (__ldg(scene_off + g) <= p && p < __ldg(scene_off + g + 1)) return g;
+    int hi = n_scenes;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (scene_off[mid] <= p) lo = mid; else hi = mid;
+    }
+  }
+  return lo;
+}
+
 // ---------------------------------------------------------------------------
 // Reduced (NSF) substep: points carry x, v, C; tau comes from
 // the MLP.  Two accumulators alternate by step parity: P2G(n) reduces into
@@ -77,25 +106,21 @@ constexpr int kNoBase = -1;
 
 __device__ __forceinline__ int pack_base(int b0, int b1, int b2) { return (b0 << 20) | (b1 << 10) | b2; }
 
-// P2G of point p of `scene` with Kirchhoff stress tau (Voigt), MLS force
-// (reading #1), and the clear of its previous stencil.
-__device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int64_t p, int scene, const float tp[6],
-                                              int64_t step) {
+// P2G of one point (state x, v, C, Kirchhoff stress tau in Voigt order) of
+// `scene`, MLS force (reading #1): 27 vector reductions into acc[step & 1].
+__device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int scene, const float xp[3], const float vp[3],
+                                              const float Cp[9], const float tp[6], int64_t step) {
   const DevParams& P = q.P;
-  float* S = q.S;
-  const int64_t so = (int64_t)scene * P.nodes_per_scene;
-  float4* out = ((step & 1) ? q.acc1 : q.acc0) + so;
-  float xp[3], vp[3], Cp[9];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) { xp[a] = S[pbase(p) + (PX + a) * 32]; vp[a] = S[pbase(p) + (PV + a) * 32]; }
-#pragma unroll
-  for (int k = 0; k < 9; ++k) Cp[k] = S[pbase(p) + (PC + k) * 32];
+  float4* out = ((step & 1) ? q.acc1 : q.acc0) + (int64_t)scene * P.nodes_per_scene;
   Axis ax[3];
+  int base[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     ax[a] = bspline_axis(xp[a], P.inv_dx);
-    ax[a].base = clamp_base(ax[a].base, P.N[a]);
+    base[a] = ax[a].base = clamp_base(ax[a].base, P.N[a]);
   }
+  int X[3], Y[3], Z[3];
+  stencil_offsets(base, P, X, Y, Z);
   const float m = P.mass;
   const float T[9] = {tp[0], tp[5], tp[4], tp[5], tp[1], tp[3], tp[4], tp[3], tp[2]};
   float Q[9];
@@ -112,34 +137,16 @@ __device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int64_t p, int sc
         const float mv0 = W * (m * vp[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
         const float mv1 = W * (m * vp[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
         const float mv2 = W * (m * vp[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
-        red_add_v4(out + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
+        red_add_v4(out + (X[a] + Y[b] + Z[c]), W * m, mv0, mv1, mv2);
       }
 }
 
-// Blocked-layout offsets of the 3 stencil nodes per axis (node_index split per
-// axis, 32-bit: one scene's grid has < 2^31 nodes)
-__device__ __forceinline__ void stencil_offsets(const int base[3], const DevParams& P, int X[3], int Y[3], int Z[3]) {
-  const int plane = P.NB[1] * P.NB[2] * kBlockNodes;
+// the point's x, v, C from the particle store
+__device__ __forceinline__ void nsf_load_point(const float* S, int64_t p, float xp[3], float vp[3], float Cp[9]) {
 #pragma unroll
-  for (int o = 0; o < 3; ++o) {
-    const int i = base[0] + o, j = base[1] + o, k = base[2] + o;
-    X[o] = (i >> 2) * plane + ((i & 3) << 4);
-    Y[o] = (j >> 2) * (P.NB[2] * kBlockNodes) + ((j & 3) << 2);
-    Z[o] = (k >> 2) * kBlockNodes + (k & 3);
-  }
-}
-
-// scene of point p (binary search over the scene offsets)
-__device__ __forceinline__ int scene_of(int64_t p, const int64_t* scene_off, int n_scenes) {
-  int lo = 0;
-  if (n_scenes > 1 && scene_off) {
-    int hi = n_scenes;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (scene_off[mid] <= p) lo = mid; else hi = mid;
-    }
-  }
-  return lo;
+  for (int a = 0; a < 3; ++a) { xp[a] = S[pbase(p) + (PX + a) * 32]; vp[a] = S[pbase(p) + (PV + a) * 32]; }
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Cp[k] = S[pbase(p) + (PC + k) * 32];
 }
 
 }  // namespace nsf
