@@ -8,9 +8,11 @@
 // One persistent CTA per SM, 384 threads = three independent "streams" of 128
 // points (one warpgroup each), so that the streams' CUDA-core epilogues (bias,
 // ELU, bf16 rounding) overlap each other's MMAs.  Per stream and tile:
-//   layer 1 (K = in_dim <= 16): fp32 FMA on CUDA cores, one thread per point,
-//     result rounded to bf16 into the stream's A tile (128 x 128, K-major,
-//     128B-swizzled, the canonical UMMA layout);
+//   layer 1 (K = in_dim <= 16): tcgen05.mma kind::tf32 with the fp32 input split
+//     as hi + lo (hi = tf32(u), lo = tf32(u - hi)) against W_1 stacked twice
+//     (bf16 weights are exact in tf32), K = 32: the sum is u W_1 to fp32 accuracy,
+//     as reading #20 requires; then bias + ELU, rounded to bf16 into the stream's
+//     A tile (128 x 128, K-major, 128B-swizzled, the canonical UMMA layout);
 //   hidden layers 2..L: tcgen05.mma.cta_group::1.kind::f16, M = N = 128,
 //     K = 8 x 16, A = activations (smem), B = W_l (smem, resident for the whole
 //     kernel), D = fp32 in TMEM (128 lanes x 128 columns); the epilogue reads D
@@ -42,8 +44,8 @@ constexpr int kOutBBytes = kOutN * kW * 2;     // 4 KB
 struct __align__(1024) Smem {
   uint8_t wB[kMaxHiddenMMA][kTileBytes];   // W_2..W_L as B operands (N x K, K-major, SW128)
   uint8_t wOut[kOutBBytes];                 // W_out padded to 16 rows
-  uint8_t a[kStreams][kTileBytes];          // per-stream activation tile
-  float w1[16][kW];                         // layer-1 weights, fp32, [in][out]
+  uint8_t a[kStreams][kTileBytes];          // per-stream activation tile (layer 1: tf32 [hi | lo] inputs)
+  uint8_t w1t[kW * 128];                     // layer-1 B operand: 128 rows x [W_1 | W_1] tf32, SW128
   float bias[kMaxHiddenMMA + 1][kW];        // b_1 .. b_L
   float bout[kOutN];
   unsigned long long bar[kStreams];          // per-stream MMA-completion mbarriers
@@ -70,9 +72,23 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   return d;
 }
 
-// instruction descriptor: D f32, A/B bf16, both K-major, M x N
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// instruction descriptor: D f32, A/B bf16 (fmt 1) or tf32 (fmt 2), both K-major, M x N
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, uint32_t fmt = 1u) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
 }
 
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -213,9 +229,12 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       *reinterpret_cast<uint4*>(sm.wOut + sw128_offset(nrow, kc * 8, kOutN)) = v;
     }
   }
-  for (int e = tid; e < 16 * kW; e += kThreads) {
-    const int i = e / kW, j = e % kW;
-    sm.w1[i][j] = i < in_dim ? __uint_as_float(((uint32_t)mlp.W[mlp.w_off[0] + j * in_dim + i]) << 16) : 0.0f;
+  // layer-1 B: row j = [W_1[j][0..15] | W_1[j][0..15]] (zero beyond in_dim), 16-byte chunk c of row j at
+  // j*128 + ((c ^ (j & 7)) << 4)
+  for (int e = tid; e < kW * 32; e += kThreads) {
+    const int j = e >> 5, k = e & 31, i = k & 15;
+    const float w = i < in_dim ? __uint_as_float(((uint32_t)mlp.W[mlp.w_off[0] + j * in_dim + i]) << 16) : 0.0f;
+    *reinterpret_cast<float*>(sm.w1t + j * 128 + ((((k >> 2) ^ (j & 7))) << 4) + (k & 3) * 4) = w;
   }
   for (int e = tid; e < (kMaxHiddenMMA + 1) * kW; e += kThreads) {
     const int l = e / kW, j = e % kW;
@@ -241,8 +260,9 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   const uint32_t lane_sel = ((uint32_t)(32 * (warp & 3))) << 16;
   const int64_t step = d_step ? *d_step : 0;
   const uint32_t a_saddr = smem_u32(sm.a[s]);
-  const uint32_t w1_saddr = smem_u32(&sm.w1[0][0]);
+  const uint32_t w1_saddr = smem_u32(sm.w1t);
   const uint32_t bias_saddr = smem_u32(&sm.bias[0][0]);
+  constexpr uint32_t kIdesc1 = make_idesc(kM, kW, 2u);
   constexpr uint32_t kIdescH = make_idesc(kM, kW);
   constexpr uint32_t kIdescO = make_idesc(kM, kOutN);
   uint32_t phase = 0;
@@ -251,7 +271,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   for (int64_t tile = (int64_t)blockIdx.x * kStreams + s; tile < n_tiles; tile += (int64_t)gridDim.x * kStreams) {
     const int64_t p = tile * kM + t;
     const bool live = p < n;
-    // ---- layer 1 on CUDA cores (fp32 input, reading #20) ----
+    // ---- layer 1 inputs u = (X, z(n)), fp32 (reading #20) ----
     float u[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) u[i] = 0.0f;
@@ -269,32 +289,53 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       for (int k = 0; k < r && k < 13; ++k)
         u[3 + k] = z[scene * r + k] + (float)step * (dz ? dz[scene * r + k] : 0.0f);
     }
+    // A row t = [hi(u) | lo(u)], 32 tf32 = one 128-byte swizzled line
+    {
+      const uint32_t row = a_saddr + (uint32_t)t * 128u;
+      const uint32_t sw = (uint32_t)(t & 7);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 hi, lo;
+        uint32_t* ph = &hi.x;
+        uint32_t* pl = &lo.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x = u[4 * c + e];
+          const uint32_t xh = to_tf32(x);
+          ph[e] = xh;
+          pl[e] = to_tf32(x - __uint_as_float(xh));
+        }
+        sts_u4(row + (((uint32_t)c ^ sw) << 4), hi);
+        sts_u4(row + (((uint32_t)(c + 4) ^ sw) << 4), lo);
+      }
+    }
+    fence_async_smem();
+    stream_barrier(s);
+    if (t == 0) {
+      fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)   // K = 32 in steps of 8 (32 bytes)
+        mma_tf32(d_col, make_desc(a_saddr + kk * 32), make_desc(w1_saddr + kk * 32), kIdesc1, kk > 0 ? 1u : 0u);
+      mma_commit(&sm.bar[s]);
+    }
+    mbar_wait(&sm.bar[s], phase);
+    phase ^= 1;
+    fence_after();
 #pragma unroll 1
     for (int c0 = 0; c0 < kW; c0 += 32) {
       float h[32];
+      tmem_ld32(d_col + lane_sel + c0, h);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float4 b = lds_f4(bias_saddr + (uint32_t)(c0 + 4 * q) * 4u);
-        h[4 * q] = b.x; h[4 * q + 1] = b.y; h[4 * q + 2] = b.z; h[4 * q + 3] = b.w;
+        h[4 * q] = elu(h[4 * q] + b.x);
+        h[4 * q + 1] = elu(h[4 * q + 1] + b.y);
+        h[4 * q + 2] = elu(h[4 * q + 2] + b.z);
+        h[4 * q + 3] = elu(h[4 * q + 3] + b.w);
       }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (i < in_dim) {   // warp-uniform
-          const float ui = u[i];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {   // broadcast reads of W_1[i][c0..c0+31]
-            const float4 wv = lds_f4(w1_saddr + (uint32_t)(i * kW + c0 + 4 * q) * 4u);
-            h[4 * q] = fmaf(wv.x, ui, h[4 * q]);
-            h[4 * q + 1] = fmaf(wv.y, ui, h[4 * q + 1]);
-            h[4 * q + 2] = fmaf(wv.z, ui, h[4 * q + 2]);
-            h[4 * q + 3] = fmaf(wv.w, ui, h[4 * q + 3]);
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) h[j] = elu(h[j]);
       store_act32(a_saddr, t, c0, h);
     }
+    fence_before();
     fence_async_smem();
     stream_barrier(s);
     // ---- hidden layers on tensor cores ----
