@@ -160,6 +160,10 @@ __device__ __forceinline__ float elu(float a) {
   return a > 0.0f ? a : e - 1.0f;
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes) : "memory");
+}
+
 __device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
@@ -212,23 +216,23 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   const int in_dim = mlp.in_dim;
 
   // ---- one-time setup: weights into smem (swizzled B operands), biases, TMEM, barriers
+  // (16-byte cp.async chunks, all in flight at once; the weights are L2-resident after the first CTA)
   for (int l = 0; l < n_mma_hidden; ++l) {
     const uint16_t* W = mlp.W + mlp.w_off[l + 1];   // [128 out][128 in]
     for (int c = tid; c < kW * (kW / 8); c += kThreads) {
       const int nrow = c >> 4, kc = c & 15;
-      const uint4 v = *reinterpret_cast<const uint4*>(W + nrow * kW + kc * 8);
-      *reinterpret_cast<uint4*>(sm.wB[l] + sw128_offset(nrow, kc * 8, kW)) = v;
+      cp_async16(smem_u32(sm.wB[l] + sw128_offset(nrow, kc * 8, kW)), W + nrow * kW + kc * 8, 16);
     }
   }
   {
-    const uint16_t* W = mlp.W + mlp.w_off[L - 1];   // [out_dim][128]
+    const uint16_t* W = mlp.W + mlp.w_off[L - 1];   // [out_dim][128], rows >= out_dim zero-filled
     for (int c = tid; c < kOutN * (kW / 8); c += kThreads) {
       const int nrow = c >> 4, kc = c & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (nrow < mlp.out_dim) v = *reinterpret_cast<const uint4*>(W + nrow * kW + kc * 8);
-      *reinterpret_cast<uint4*>(sm.wOut + sw128_offset(nrow, kc * 8, kOutN)) = v;
+      const bool in = nrow < mlp.out_dim;
+      cp_async16(smem_u32(sm.wOut + sw128_offset(nrow, kc * 8, kOutN)), in ? W + nrow * kW + kc * 8 : W, in ? 16 : 0);
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // layer-1 B: row j = [W_1[j][0..15] | W_1[j][0..15]] (zero beyond in_dim), 16-byte chunk c of row j at
   // j*128 + ((c ^ (j & 7)) << 4)
   for (int e = tid; e < kW * 32; e += kThreads) {
@@ -250,6 +254,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   fence_async_smem();
   fence_before();
   __syncthreads();
@@ -268,27 +273,33 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   uint32_t phase = 0;
 
   const int64_t n_tiles = (n + kM - 1) / kM;
-  for (int64_t tile = (int64_t)blockIdx.x * kStreams + s; tile < n_tiles; tile += (int64_t)gridDim.x * kStreams) {
+  const int64_t tile_stride = (int64_t)gridDim.x * kStreams;
+  // layer-1 inputs u = (X, z(n)) of point `tile * 128 + t`, fp32 (reading #20); loaded one tile ahead
+  auto load_inputs = [&](int64_t tile_, float* u_, int& scene_) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) u_[i] = 0.0f;
+    const int64_t p_ = tile_ * kM + t;
+    scene_ = 0;
+    if (tile_ >= n_tiles || p_ >= n) return;
+    scene_ = scene_of(p_, scene_off, n_scenes, n);
+    if (xpitch >= 0) {
+      u_[0] = X[0 * xpitch + p_];
+      u_[1] = X[1 * xpitch + p_];
+      u_[2] = X[2 * xpitch + p_];
+    } else {   // AoSoA planes of the particle store
+      u_[0] = X[pbase(p_) + 0 * 32];
+      u_[1] = X[pbase(p_) + 1 * 32];
+      u_[2] = X[pbase(p_) + 2 * 32];
+    }
+    for (int k = 0; k < r && k < 13; ++k)
+      u_[3 + k] = z[scene_ * r + k] + (float)step * (dz ? dz[scene_ * r + k] : 0.0f);
+  };
+  float u[16];
+  int scene = 0;
+  load_inputs((int64_t)blockIdx.x * kStreams + s, u, scene);
+  for (int64_t tile = (int64_t)blockIdx.x * kStreams + s; tile < n_tiles; tile += tile_stride) {
     const int64_t p = tile * kM + t;
     const bool live = p < n;
-    // ---- layer 1 inputs u = (X, z(n)), fp32 (reading #20) ----
-    float u[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) u[i] = 0.0f;
-    const int scene = live ? scene_of(p, scene_off, n_scenes, n) : 0;
-    if (live) {
-      if (xpitch >= 0) {
-        u[0] = X[0 * xpitch + p];
-        u[1] = X[1 * xpitch + p];
-        u[2] = X[2 * xpitch + p];
-      } else {   // AoSoA planes of the particle store
-        u[0] = X[pbase(p) + 0 * 32];
-        u[1] = X[pbase(p) + 1 * 32];
-        u[2] = X[pbase(p) + 2 * 32];
-      }
-      for (int k = 0; k < r && k < 13; ++k)
-        u[3 + k] = z[scene * r + k] + (float)step * (dz ? dz[scene * r + k] : 0.0f);
-    }
     // A row t = [hi(u) | lo(u)], 32 tf32 = one 128-byte swizzled line
     {
       const uint32_t row = a_saddr + (uint32_t)t * 128u;
@@ -402,6 +413,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       }
       if (q.enabled) nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);   // reduced P2G, tau from registers
     }
+    load_inputs(tile + tile_stride, u, scene);   // next tile's inputs (latency overlaps the barrier)
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile
   }
