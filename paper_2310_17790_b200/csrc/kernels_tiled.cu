@@ -912,6 +912,73 @@ __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, i
   }
 }
 
+// Phase 1 of the fused kernels for storage slot j: G2P from the
+// segment's velocity tile (global gather if the stencil left it), x/v/C/F/tau
+// updated in place, and the new state returned for the next substep's P2G.
+// P2G-only launches (DO_G2P = false) just read the state.
+template <bool DO_G2P>
+__device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const int o[3], const float4* vt,
+                                                   const float4* __restrict__ gvel, const DevParams& P, DevErr* err,
+                                                   float xn[3], float vn[3], float Cn[9], float tau[6]) {
+  float* base = S + pbase(j);
+      if (DO_G2P) {
+    float x[3], F[9], G[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x[a] = base[(PX + a) * 32];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
+    // stencil inside the tile (drift <= 1 cell since the last re-binning)?
+    bool in_tile = NSF_FUSED_VTILE;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int bb = (int)floorf(x[a] * P.inv_dx - 0.5f);
+      in_tile &= (bb >= o[a]) && (bb + 2 < o[a] + kVT);
+    }
+    if (in_tile) {
+      g2p_gather_tile(x, vt, o, P, vn, Cn);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) G[k] = Cn[k];
+    } else {
+      g2p_gather<0>(x, gvel, P, vn, Cn, G);
+    }
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      xn[a] = x[a] + P.dt * vn[a];
+      const float tt = xn[a] * P.inv_dx;
+      ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
+      base[(PX + a) * 32] = xn[a];
+      base[(PV + a) * 32] = vn[a];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) base[(PC + k) * 32] = Cn[k];
+    float Ft[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj)
+        Ft[i * 3 + jj] = F[i * 3 + jj] + P.dt * (G[i * 3 + 0] * F[0 * 3 + jj] + G[i * 3 + 1] * F[1 * 3 + jj] +
+                                                 G[i * 3 + 2] * F[2 * 3 + jj]);
+    float FE[9];
+    const float J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    float chk = xn[0] + xn[1] + xn[2] + vn[0] + vn[1] + vn[2];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) { base[(PF + k) * 32] = FE[k]; chk += FE[k]; }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) { base[(PT + k) * 32] = tau[k]; chk += tau[k]; }
+    if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
+    if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, j); }
+    if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, j); }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { xn[a] = base[(PX + a) * 32]; vn[a] = base[(PV + a) * 32]; }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Cn[k] = base[(PC + k) * 32];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) tau[k] = base[(PT + k) * 32];
+  }
+}
+
 template <bool DO_G2P, int ROWS, int MINB, int NT>
 __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
@@ -953,64 +1020,8 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     __syncthreads();
     // ---- phase 1: per particle ----
     for (int j = s0 + tid; j < s1; j += NT) {
-      float* base = S + pbase(j);
       float xn[3], vn[3], Cn[9], tau[6];
-      if (DO_G2P) {
-        float x[3], F[9], G[9];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) x[a] = base[(PX + a) * 32];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
-        // stencil inside the tile (drift <= 1 cell since the last re-binning)?
-        bool in_tile = NSF_FUSED_VTILE;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const int bb = (int)floorf(x[a] * P.inv_dx - 0.5f);
-          in_tile &= (bb >= o[a]) && (bb + 2 < o[a] + kVT);
-        }
-        if (in_tile) {
-          g2p_gather_tile(x, sm.vt, o, P, vn, Cn);
-#pragma unroll
-          for (int k = 0; k < 9; ++k) G[k] = Cn[k];
-        } else {
-          g2p_gather<0>(x, gvel, P, vn, Cn, G);
-        }
-        bool ok = true;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          xn[a] = x[a] + P.dt * vn[a];
-          const float tt = xn[a] * P.inv_dx;
-          ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
-          base[(PX + a) * 32] = xn[a];
-          base[(PV + a) * 32] = vn[a];
-        }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) base[(PC + k) * 32] = Cn[k];
-        float Ft[9];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 3; ++jj)
-            Ft[i * 3 + jj] = F[i * 3 + jj] + P.dt * (G[i * 3 + 0] * F[0 * 3 + jj] + G[i * 3 + 1] * F[1 * 3 + jj] +
-                                                     G[i * 3 + 2] * F[2 * 3 + jj]);
-        float FE[9];
-        const float J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
-        float chk = xn[0] + xn[1] + xn[2] + vn[0] + vn[1] + vn[2];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) { base[(PF + k) * 32] = FE[k]; chk += FE[k]; }
-#pragma unroll
-        for (int k = 0; k < 6; ++k) { base[(PT + k) * 32] = tau[k]; chk += tau[k]; }
-        if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
-        if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, j); }
-        if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, j); }
-      } else {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) { xn[a] = base[(PX + a) * 32]; vn[a] = base[(PV + a) * 32]; }
-#pragma unroll
-        for (int k = 0; k < 9; ++k) Cn[k] = base[(PC + k) * 32];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) tau[k] = base[(PT + k) * 32];
-      }
+      fused_g2p_particle<DO_G2P>(S, j, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
       // ---- P2G of the new state: by cell if still inside this block, else direct ----
       int c[3];
       bool core = true;
