@@ -63,6 +63,11 @@ KERNEL_BYTES_PER_PARTICLE = {
     "bin_keys_hist": 12.0 + 4.0,
     "bin_scatter": 8.0,
 }
+STEP_DESC = {
+    False: "one full substep: G2P + return map fused with the next P2G, grid update (+ re-binning every 32)",
+    True: "one reduced substep: NSF MLP (tcgen05) with P2G in its epilogue, G2P with the grid update "
+          "(+ re-binning every 32)",
+}
 L2_FLUSH_BYTES = 256 << 20              # > 2x the 126 MB L2
 B_ALG_PER_PARTICLE_SUBSTEP = 268.0   # 84 + 48 + 120 + 16
 
@@ -195,6 +200,8 @@ def run_reference(args):
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (scenes/, seeded)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
+                       "particles_per_gpu": sc.n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt, "replicas": 1,
+                       "step": STEP_DESC[args.config == "C5"],
                        "sample": f"first {S} particles (cell order) of the workload, one oracle substep per step"},
             "cpu_baseline": {"value": value, "unit": "particle-substeps/s", "cores": 1, "kind": "oracle",
                              "sample": f"{S} particles x {args.steps} substeps"},
@@ -374,9 +381,7 @@ def run_ours(args):
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                        "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
                        "replicas": world, "l2": "flushed before every timed substep (256 MB write outside the per-substep CUDA events)",
-                       "step": ("one full substep: binning, NSF MLP (tcgen05), P2G, grid update, G2P"
-                                if args.config == "C5" else
-                                "one full substep: binning, P2G, grid update, G2P + return map")},
+                       "step": STEP_DESC[args.config == "C5"]},
             "hbm_alg_gbs_whole_step": step_gbs,
             "hbm_alg_frac_whole_step": step_gbs / peak,
             "roofline": roof,
