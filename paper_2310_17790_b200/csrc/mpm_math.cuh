@@ -273,6 +273,12 @@ __device__ __forceinline__ float elastoplastic(const float Ft[9], int model, flo
 // Both fall back to the rotation-safe SVD when det F <= 1e-6 or sigma < 1e-4
 // (reading #21: inverted / degenerate F), so conventions stay identical.
 
+#ifndef NSF_LOGSTRAIN_SERIES
+#define NSF_LOGSTRAIN_SERIES 1   // eigen-free Hencky / return maps for ||F F^T - I||_F <= 0.3
+#endif
+#ifndef NSF_JACOBI_TOL2
+#define NSF_JACOBI_TOL2 1e-13f   // (off-diagonal / ||A||)^2 stopping level of sym_eig3
+#endif
 // Symmetric 3x3 eigen-decomposition by cyclic Jacobi: A = V diag(A_ii) V^T.
 // Stops once the off-diagonal mass is below 3e-7 of ||A||_F (fp32 round-off
 // level for the small-strain matrices it is applied to, see elastoplastic_fast).
@@ -282,7 +288,7 @@ __device__ __forceinline__ void sym_eig3(float A[3][3], float V[3][3]) {
 #pragma unroll
     for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0f : 0.0f;
   const float off0 = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
-  const float tol2 = 1e-13f * (A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2] + 2.0f * off0);
+  const float tol2 = NSF_JACOBI_TOL2 * (A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2] + 2.0f * off0);
   for (int sweep = 0; sweep < 6; ++sweep) {
     const float off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
     if (off <= tol2) break;
@@ -321,6 +327,118 @@ __device__ __forceinline__ bool polar_newton(const float F[9], float R[9]) {
     }
     if (diff < 2e-7f) break;
   }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Eigen-free log-strain models for moderate strains.  All matrices below are
+// functions of S = F F^T - I, hence symmetric and mutually commuting, so a
+// product is stored by its 6 independent entries (xx, yy, zz, yz, xz, xy).
+//   eps = 1/2 log(I + S) = atanh(Y) = Y + Y^3/3 + Y^5/5 + ..., Y = S (2I + S)^-1
+// (|Y| <= 0.18 for ||S||_F <= 0.3: five terms leave < 1e-9 relative).  With
+// F = V R and V = exp(eps): F_E = exp(eps_E - eps) F and
+// tau = 2 mu eps_E + lambda tr(eps_E) I -- the same Hencky model and return
+// maps as the eigen path (readings #3-#6), written as matrix
+// functions.
+struct Sym6 { float xx, yy, zz, yz, xz, xy; };
+
+__device__ __forceinline__ Sym6 sym_mul(const Sym6& A, const Sym6& B) {
+  Sym6 C;
+  C.xx = fmaf(A.xx, B.xx, fmaf(A.xy, B.xy, A.xz * B.xz));
+  C.yy = fmaf(A.xy, B.xy, fmaf(A.yy, B.yy, A.yz * B.yz));
+  C.zz = fmaf(A.xz, B.xz, fmaf(A.yz, B.yz, A.zz * B.zz));
+  C.yz = fmaf(A.xy, B.xz, fmaf(A.yy, B.yz, A.yz * B.zz));
+  C.xz = fmaf(A.xx, B.xz, fmaf(A.xy, B.yz, A.xz * B.zz));
+  C.xy = fmaf(A.xx, B.xy, fmaf(A.xy, B.yy, A.xz * B.yz));
+  return C;
+}
+
+// C = A * B + c I
+__device__ __forceinline__ Sym6 sym_mul_add_diag(const Sym6& A, const Sym6& B, float c) {
+  Sym6 C = sym_mul(A, B);
+  C.xx += c; C.yy += c; C.zz += c;
+  return C;
+}
+
+__device__ __forceinline__ float sym_fro2(const Sym6& A) {
+  return A.xx * A.xx + A.yy * A.yy + A.zz * A.zz + 2.0f * (A.yz * A.yz + A.xz * A.xz + A.xy * A.xy);
+}
+
+// exp(A) for ||A||_F <= 0.2 (Taylor to degree 6, Horner form; error < 3e-9)
+__device__ __forceinline__ Sym6 sym_exp_small(const Sym6& A) {
+  const float inv[6] = {1.0f, 0.5f, 1.0f / 3.0f, 0.25f, 0.2f, 1.0f / 6.0f};
+  Sym6 E{1.0f, 1.0f, 1.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 5; k >= 1; --k) {   // E <- I + A E / (k+1) ... evaluated innermost first
+    Sym6 As{A.xx * inv[k], A.yy * inv[k], A.zz * inv[k], A.yz * inv[k], A.xz * inv[k], A.xy * inv[k]};
+    E = sym_mul_add_diag(As, E, 1.0f);
+  }
+  return sym_mul_add_diag(A, E, 1.0f);
+}
+
+// Returns false (caller falls back to the eigen path) outside the series' range.
+__device__ __forceinline__ bool elastoplastic_series(const float Ft[9], const Sym6& S, int model, float mu,
+                                                     float lam, float alpha, float tau_Y, float FE[9], float tau[6],
+                                                     float& detFE) {
+  if (!(sym_fro2(S) <= 0.09f)) return false;
+  // Y = S (2I + S)^-1
+  const Sym6 M{2.0f + S.xx, 2.0f + S.yy, 2.0f + S.zz, S.yz, S.xz, S.xy};
+  const float cxx = M.yy * M.zz - M.yz * M.yz, cyy = M.xx * M.zz - M.xz * M.xz, czz = M.xx * M.yy - M.xy * M.xy;
+  const float cyz = M.xy * M.xz - M.xx * M.yz, cxz = M.xy * M.yz - M.yy * M.xz, cxy = M.xz * M.yz - M.zz * M.xy;
+  const float rdet = 1.0f / (M.xx * cxx + M.xy * cxy + M.xz * cxz);
+  const Sym6 Minv{cxx * rdet, cyy * rdet, czz * rdet, cyz * rdet, cxz * rdet, cxy * rdet};
+  const Sym6 Y = sym_mul(S, Minv);
+  const Sym6 Y2 = sym_mul(Y, Y);
+  // P = I + Y2/3 + Y2^2/5 + Y2^3/7 + Y2^4/9 (Horner), eps = Y P
+  Sym6 Pm{1.0f / 9.0f, 1.0f / 9.0f, 1.0f / 9.0f, 0.0f, 0.0f, 0.0f};
+  Pm = sym_mul_add_diag(Y2, Pm, 1.0f / 7.0f);
+  Pm = sym_mul_add_diag(Y2, Pm, 1.0f / 5.0f);
+  Pm = sym_mul_add_diag(Y2, Pm, 1.0f / 3.0f);
+  Pm = sym_mul_add_diag(Y2, Pm, 1.0f);
+  const Sym6 E = sym_mul(Y, Pm);
+  const float tr = E.xx + E.yy + E.zz;
+  const Sym6 Eh{E.xx - tr * (1.0f / 3.0f), E.yy - tr * (1.0f / 3.0f), E.zz - tr * (1.0f / 3.0f), E.yz, E.xz, E.xy};
+  const float nrm = sqrtf(sym_fro2(Eh));
+  float dg;
+  bool expand = false;
+  if (model == 1) {   // Drucker-Prager
+    expand = tr > 0.0f;
+    dg = nrm + alpha * (3.0f * lam + 2.0f * mu) * tr / (2.0f * mu);
+  } else {            // von Mises
+    dg = nrm - tau_Y / (2.0f * mu);
+  }
+  Sym6 Ee = E;   // eps_E
+  if (expand || dg > 0.0f) {
+    // A = eps_E - eps: -eps (DP tip) or -(dg / |eps_hat|) eps_hat
+    Sym6 A;
+    if (expand) {
+      A = Sym6{-E.xx, -E.yy, -E.zz, -E.yz, -E.xz, -E.xy};
+    } else {
+      const float k = dg / nrm;
+      A = Sym6{-k * Eh.xx, -k * Eh.yy, -k * Eh.zz, -k * Eh.yz, -k * Eh.xz, -k * Eh.xy};
+    }
+    if (!(sym_fro2(A) <= 0.04f)) return false;
+    const Sym6 X = sym_exp_small(A);
+    const float Xm[9] = {X.xx, X.xy, X.xz, X.xy, X.yy, X.yz, X.xz, X.yz, X.zz};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        FE[i * 3 + j] = Xm[i * 3 + 0] * Ft[0 * 3 + j] + Xm[i * 3 + 1] * Ft[1 * 3 + j] + Xm[i * 3 + 2] * Ft[2 * 3 + j];
+    Ee = Sym6{E.xx + A.xx, E.yy + A.yy, E.zz + A.zz, E.yz + A.yz, E.xz + A.xz, E.xy + A.xy};
+    detFE = det3(FE);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+    detFE = det3(Ft);
+  }
+  const float lt = lam * (Ee.xx + Ee.yy + Ee.zz);
+  tau[0] = 2.0f * mu * Ee.xx + lt;
+  tau[1] = 2.0f * mu * Ee.yy + lt;
+  tau[2] = 2.0f * mu * Ee.zz + lt;
+  tau[3] = 2.0f * mu * Ee.yz;
+  tau[4] = 2.0f * mu * Ee.xz;
+  tau[5] = 2.0f * mu * Ee.xy;
   return true;
 }
 
@@ -367,6 +485,13 @@ __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model
       Bm[i][j] = s;
       Bm[j][i] = s;
     }
+#if NSF_LOGSTRAIN_SERIES
+  {
+    float detS;
+    const Sym6 S6{Bm[0][0], Bm[1][1], Bm[2][2], Bm[1][2], Bm[0][2], Bm[0][1]};
+    if (elastoplastic_series(Ft, S6, model, mu, lam, alpha, tau_Y, FE, tau, detS)) return detS;
+  }
+#endif
   float U[3][3];
   sym_eig3(Bm, U);
   const float kFloor2 = 1e-8f;   // sigma >= 1e-4

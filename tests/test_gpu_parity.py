@@ -47,6 +47,12 @@ def small_scenes():
         # von Mises with the moving plate, states beyond yield
         "VM": S.block_scene("VM", 32, (9, 3, 8), (21, 13, 22), S.VON_MISES, 13,
                             keep=9000, vnoise=0.2, Fnoise=0.08, Cnoise=2.0),
+        # F noise 0.05: ||F F^T - I||_F straddles 0.3, so both the eigen-free series path and the
+        # Jacobi path of the log-strain models run, elastic and plastic
+        "VM_mix": S.block_scene("VMm", 32, (9, 3, 8), (21, 13, 22), S.VON_MISES, 16,
+                                keep=6000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0),
+        "DP_mix": S.block_scene("DPm", 32, (8, 3, 9), (20, 16, 21), S.DRUCKER_PRAGER, 17,
+                                keep=6000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0),
         "FC_gradw": S.block_scene("FCg", 32, (9, 6, 10), (20, 15, 19), S.FIXED_COROTATED, 14,
                                   keep=3333, vnoise=0.3, Fnoise=0.02, Cnoise=3.0,
                                   force_mode=S.FORCE_GRADW),
