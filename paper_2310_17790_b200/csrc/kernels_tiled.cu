@@ -76,8 +76,8 @@ struct __align__(16) P2GSmem {
 };
 
 // (cell, stencil-offset) pairs feeding each of the 216 tile nodes, built once
-__device__ uint16_t g_p2g_tbl[1728];
-__device__ uint16_t g_p2g_tbl_off[218];
+__device__ __align__(16) uint16_t g_p2g_tbl[1728];
+__device__ __align__(16) uint16_t g_p2g_tbl_off[224];   // 217 used; padded to 16-byte chunks
 
 __global__ void k_p2g_tables() {
   const int t = threadIdx.x;   // tile node 0..215
@@ -797,8 +797,8 @@ struct __align__(16) FusedSmemT {
   } u;
   int pop[64];
   int next;
-  uint16_t tbl[1728];
-  uint16_t tbl_off[218];
+  __align__(16) uint16_t tbl[1728];
+  __align__(16) uint16_t tbl_off[224];
 };
 static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_DENSE_MIN_BLOCKS, "fused kernel: CTAs per SM");
 static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPARSE_MIN_BLOCKS,
@@ -916,17 +916,26 @@ __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, i
 // segment's velocity tile (global gather if the stencil left it), x/v/C/F/tau
 // updated in place, and the new state returned for the next substep's P2G.
 // P2G-only launches (DO_G2P = false) just read the state.
+__device__ __forceinline__ void load_xF(const float* __restrict__ S, int j, float x[3], float F[9]) {
+  const float* base = S + pbase(j);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) x[a] = base[(PX + a) * 32];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
+}
+
 template <bool DO_G2P>
-__device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const int o[3], const float4* vt,
-                                                   const float4* __restrict__ gvel, const DevParams& P, DevErr* err,
-                                                   float xn[3], float vn[3], float Cn[9], float tau[6]) {
+__device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const float xin[3], const float Fin[9],
+                                                   const int o[3], const float4* vt, const float4* __restrict__ gvel,
+                                                   const DevParams& P, DevErr* err, float xn[3], float vn[3],
+                                                   float Cn[9], float tau[6]) {
   float* base = S + pbase(j);
       if (DO_G2P) {
     float x[3], F[9], G[9];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) x[a] = base[(PX + a) * 32];
+    for (int a = 0; a < 3; ++a) x[a] = xin[a];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
+    for (int k = 0; k < 9; ++k) F[k] = Fin[k];
     // stencil inside the tile (drift <= 1 cell since the last re-binning)?
     bool in_tile = NSF_FUSED_VTILE;
 #pragma unroll
@@ -992,8 +1001,11 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
   const int ox = tid >> 6;
   const int nblk = *(volatile int32_t*)&counters[0];
   if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
-  for (int q = tid; q < 1728; q += NT) sm.tbl[q] = g_p2g_tbl[q];
-  for (int q = tid; q < 217; q += NT) sm.tbl_off[q] = g_p2g_tbl_off[q];
+  for (int q = tid; q < 1728 / 8 + 224 / 8; q += NT) {   // 16-byte chunks of both tables, asynchronously
+    if (q < 1728 / 8) cp_async16_f(&sm.tbl[8 * q], &g_p2g_tbl[8 * q], 16);
+    else cp_async16_f(&sm.tbl_off[8 * (q - 1728 / 8)], &g_p2g_tbl_off[8 * (q - 1728 / 8)], 16);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   const float cC_unused = 0.0f;
   (void)cC_unused;
   while (true) {
@@ -1015,13 +1027,18 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
         const bool in = i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2];
         cp_async16_f(&sm.vt[e], in ? gvel + node_index(i, jn, k, P) : gvel, in ? 16 : 0);
       }
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    // the first particle's x, F load under the tile copy
+    float x0[3], F0[9];
+    if (DO_G2P && s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // ---- phase 1: per particle ----
     for (int j = s0 + tid; j < s1; j += NT) {
       float xn[3], vn[3], Cn[9], tau[6];
-      fused_g2p_particle<DO_G2P>(S, j, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
+      if (DO_G2P && j != s0 + tid) load_xF(S, j, x0, F0);
+      fused_g2p_particle<DO_G2P>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
       // ---- P2G of the new state: by cell if still inside this block, else direct ----
       int c[3];
       bool core = true;
@@ -1064,23 +1081,45 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
       part[(node * 4 + 3) * 64 + my_cell] = accp[k][2];
     }
     __syncthreads();
-    for (int t = tid; t < 216; t += NT) {
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    // node t = tid sums its 4 components; the 216 - NT remaining nodes are summed
+    // per component by threads 0 .. 4 (216 - NT) - 1, so no thread does two nodes
+    if (tid < 216) {
+      const int t = tid;
+      float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
       const int q1 = sm.tbl_off[t + 1];
       for (int q = sm.tbl_off[t]; q < q1; ++q) {
         const int pr = sm.tbl[q];
         const float* pp = part + (pr >> 6) * 256 + (pr & 63);
-        s0 += pp[0];
-        s1 += pp[64];
-        s2 += pp[128];
-        s3 += pp[192];
+        r0 += pp[0];
+        r1 += pp[64];
+        r2 += pp[128];
+        r3 += pp[192];
       }
-      if (s0 > 0.0f) {
+      if (r0 > 0.0f) {
         const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
         const int gi = 4 * bc.b[0] + nx, gj = 4 * bc.b[1] + ny, gk = 4 * bc.b[2] + nz;
         if (gi < P.N[0] && gj < P.N[1] && gk < P.N[2]) {
-          red_add_v4_t(gacc + node_index(gi, gj, gk, P), s0, s1, s2, s3);
+          red_add_v4_t(gacc + node_index(gi, gj, gk, P), r0, r1, r2, r3);
           touch_block(flags, list, list_count, (int)(scene_block0 + block_id(gi >> 2, gj >> 2, gk >> 2, P)));
+        }
+      }
+    }
+    if (NT < 216 && tid < 4 * (216 - NT)) {
+      const int t = NT + (tid >> 2), comp = tid & 3;
+      float r = 0.f;
+      const int q1 = sm.tbl_off[t + 1];
+      for (int q = sm.tbl_off[t]; q < q1; ++q) {
+        const int pr = sm.tbl[q];
+        r += part[(pr >> 6) * 256 + (pr & 63) + 64 * comp];
+      }
+      if (r != 0.0f) {
+        const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
+        const int gi = 4 * bc.b[0] + nx, gj = 4 * bc.b[1] + ny, gk = 4 * bc.b[2] + nz;
+        if (gi < P.N[0] && gj < P.N[1] && gk < P.N[2]) {
+          float* g = reinterpret_cast<float*>(gacc + node_index(gi, gj, gk, P)) + comp;
+          atomicAdd(g, r);
+          if (comp == 0 && r > 0.0f)
+            touch_block(flags, list, list_count, (int)(scene_block0 + block_id(gi >> 2, gj >> 2, gk >> 2, P)));
         }
       }
     }
