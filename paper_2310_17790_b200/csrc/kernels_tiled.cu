@@ -787,10 +787,16 @@ constexpr int kRowsF = NSF_DENSE_ROWS;         // dense variant: staged rows per
 #endif   // staged rows per cell in the fused kernel
 
 constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-1, 4b+7)
+// padded strides of the tile (in float4): a warp's lanes differ mostly within one
+// 4-cell block, so with 8-float4 rows the 16-byte bank group (index mod 8) would
+// take only 4 values; strides 9 (y) and 74 (x) spread (x, y, z) over all 8
+// (simulated: 13.2 -> 9.5 shared wavefronts per warp-wide LDS.128)
+constexpr int kVTy = 9, kVTx = 74;
+constexpr int kVTSize = (kVT - 1) * (kVTx + kVTy + 1) + 1;   // 589
 
 template <int ROWS>
 struct __align__(16) FusedSmemT {
-  float4 vt[NSF_FUSED_VTILE ? kVT * kVT * kVT : 1];   // G2P velocity tile (8 KB)
+  float4 vt[NSF_FUSED_VTILE ? kVTSize : 1];   // G2P velocity tile (9.4 KB, padded strides)
   union {
     float slot[kSlotFields * ROWS * 64];       // [field][row][cell]
     float part[27 * 4 * 64];                   // [(node*4 + comp)][cell]
@@ -816,7 +822,7 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
   Axis ax[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) ax[a] = bspline_axis(x[a], P.inv_dx);
-  const float4* tp = vt + ((ax[0].base - o[0]) * kVT + (ax[1].base - o[1])) * kVT + (ax[2].base - o[2]);
+  const float4* tp = vt + (ax[0].base - o[0]) * kVTx + (ax[1].base - o[1]) * kVTy + (ax[2].base - o[2]);
   float wyz[9];
 #pragma unroll
   for (int b = 0; b < 3; ++b)
@@ -831,7 +837,7 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
     for (int b = 0; b < 3; ++b)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const float4 vi = tp[(a * kVT + b) * kVT + c];
+        const float4 vi = tp[a * kVTx + b * kVTy + c];
         const float wgt = wyz[b * 3 + c];
         Tt[0] = fmaf(wgt, vi.x, Tt[0]); Tt[1] = fmaf(wgt, vi.y, Tt[1]); Tt[2] = fmaf(wgt, vi.z, Tt[2]);
         if (b) {
@@ -1025,7 +1031,8 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
       for (int e = tid; e < kVT * kVT * kVT; e += NT) {
         const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
         const bool in = i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2];
-        cp_async16_f(&sm.vt[e], in ? gvel + node_index(i, jn, k, P) : gvel, in ? 16 : 0);
+        cp_async16_f(&sm.vt[(e >> 6) * kVTx + ((e >> 3) & 7) * kVTy + (e & 7)], in ? gvel + node_index(i, jn, k, P) : gvel,
+                     in ? 16 : 0);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
