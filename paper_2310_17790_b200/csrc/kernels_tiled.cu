@@ -798,7 +798,7 @@ template <int ROWS>
 struct __align__(16) FusedSmemT {
   float4 vt[NSF_FUSED_VTILE ? kVTSize : 1];   // G2P velocity tile (9.4 KB, padded strides)
   union {
-    float slot[kSlotFields * ROWS * 64];       // [field][row][cell]
+    float slot[kSlotFields * ROWS * 64];       // [field][cell][row]
     float part[27 * 4 * 64];                   // [(node*4 + comp)][cell]
   } u;
   int pop[64];
@@ -892,7 +892,7 @@ __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, i
                                                  float accp[9][3]) {
   const float fox = (float)ox;
   for (int r = 0; r < rows; ++r) {
-    const int s = r * 64 + my_cell;
+    const int s = my_cell * (kSlotStrideF / 64) + r;   // [field][cell][row]
     const float wx = sl[ox * kSlotStrideF + s];
     const float wyv[3] = {sl[3 * kSlotStrideF + s], sl[4 * kSlotStrideF + s], sl[5 * kSlotStrideF + s]};
     const float wzv[3] = {sl[6 * kSlotStrideF + s], sl[7 * kSlotStrideF + s], sl[8 * kSlotStrideF + s]};
@@ -1062,7 +1062,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
         cell = (c[0] << 4) | (c[1] << 2) | c[2];
         rank = atomicAdd(&sm.pop[cell], 1);
       }
-      if (rank < ROWS) p2g_stage_values_f<ROWS * 64>(xn, vn, Cn, tau, rank * 64 + cell, sm.u.slot, P);
+      if (rank < ROWS) p2g_stage_values_f<ROWS * 64>(xn, vn, Cn, tau, cell * ROWS + rank, sm.u.slot, P);
 #if NSF_WARP_SCATTER
       p2g_scatter_warp(rank >= ROWS, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
 #else
@@ -1186,6 +1186,75 @@ __global__ void k_reorder(const float* __restrict__ Sin, float* __restrict__ Sou
 #pragma unroll
   for (int k = 0; k < kPlanes; ++k) dst[k * 32] = __ldg(src + k * 32);
   ids_out[j] = __ldg(ids_in + p);
+}
+
+// Physical reorder of the re-binning with each block's particles sorted by cell
+// (counting sort over the block's 64 cells): consecutive particles of a segment
+// then share a stencil, so the fused kernel's velocity-tile reads are mostly
+// broadcasts.  Persistent CTAs claim blocks by ticket (counters[1], reset by the
+// scan).  The order within a cell is not specified.
+__global__ void __launch_bounds__(256) k_reorder_cells(const float* __restrict__ Sin, float* __restrict__ Sout,
+                                                      const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
+                                                      const int32_t* __restrict__ perm,
+                                                      const int32_t* __restrict__ block_start,
+                                                      const int32_t* __restrict__ nonempty, int32_t* counters,
+                                                      DevParams P) {
+  __shared__ int cnt[64];
+  __shared__ int next;
+  const int tid = threadIdx.x;
+  const int nblk = *(volatile int32_t*)&counters[0];
+  auto cell_of = [&](int src, const BlockCoord& bc) {
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int b = (int)floorf(__ldg(Sin + pbase(src) + (PX + a) * 32) * P.inv_dx - 0.5f);
+      b = min(max(b, 0), P.N[a] - 3);
+      c[a] = min(max(b - 4 * bc.b[a], 0), 3);
+    }
+    return (c[0] << 4) | (c[1] << 2) | c[2];
+  };
+  while (true) {
+    if (tid == 0) next = atomicAdd(&counters[1], 1);
+    if (tid < 64) cnt[tid] = 0;
+    __syncthreads();
+    const int bi = next;
+    if (bi >= nblk) break;
+    const int key = nonempty[bi];
+    const BlockCoord bc = decode_block(key, P);
+    const int s0 = block_start[key], s1 = block_start[key + 1];
+    for (int j = s0 + tid; j < s1; j += 256) atomicAdd(&cnt[cell_of(perm[j], bc)], 1);
+    __syncthreads();
+    if (tid < 32) {   // exclusive scan of the 64 counts, two per lane
+      const int v0 = cnt[2 * tid], v1 = cnt[2 * tid + 1];
+      int incl = v0 + v1;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (tid >= d) incl += t;
+      }
+      const int excl = incl - v0 - v1;
+      cnt[2 * tid] = excl;
+      cnt[2 * tid + 1] = excl + v0;
+    }
+    __syncthreads();
+    for (int j = s0 + tid; j < s1; j += 256) {
+      const int src = perm[j];
+      const int dst = s0 + atomicAdd(&cnt[cell_of(src, bc)], 1);
+      const float* sp = Sin + pbase(src);
+      float* dp = Sout + pbase(dst);
+#pragma unroll
+      for (int k = 0; k < kPlanes; ++k) dp[k * 32] = __ldg(sp + k * 32);
+      ids_out[dst] = __ldg(ids_in + src);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
+                          int32_t* ids_out, const PipelineBuffers* pb, const DevParams& P) {
+  if (n == 0) return;
+  k_reorder_cells<<<num_sms() * 6, 256, 0, st>>>(Sin, Sout, ids_in, ids_out, pb->perm, pb->block_start, pb->nonempty,
+                                                 pb->n_nonempty, P);
 }
 
 template <bool DO_G2P, int ROWS, int MINB, int NT>

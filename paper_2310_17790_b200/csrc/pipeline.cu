@@ -63,6 +63,16 @@ nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
 // Invariant of the dense (tiled) path between substeps: keys[] and counts[]
 // describe the particles of the current buffer (written by the last G2P, or
 // here after a load).
+// particles of a block stored in cell order (NSF_REORDER_CELLS=0: block order only)
+static bool reorder_by_cell() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_REORDER_CELLS");
+    f = (e && e[0] == '0') ? 0 : 1;
+  }
+  return f == 1;
+}
+
 // Re-binning with a physical reorder of buffer `cur` into 1 - cur (fused pipeline):
 // keys + histogram, scan (block_start, non-empty list), scatter (perm), reorder.
 static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
@@ -71,7 +81,11 @@ static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, i
           launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
   PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
   PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
-  PLAUNCH(h, "reorder", launch_reorder(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb->perm));
+  if (reorder_by_cell())
+    PLAUNCH(h, "reorder",
+            launch_reorder_cells(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb, *v.P));
+  else
+    PLAUNCH(h, "reorder", launch_reorder(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb->perm));
   return nxt;
 }
 

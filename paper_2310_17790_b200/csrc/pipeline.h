@@ -114,6 +114,8 @@ void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc,
                               const int64_t* d_step);
 void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,
                     const int32_t* perm);
+void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
+                          int32_t* ids_out, const PipelineBuffers* pb, const DevParams& P);
 void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                       int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const int64_t* scene_off,
                       int n_scenes, const DevParams& P, DevErr* err, int64_t* d_step);
