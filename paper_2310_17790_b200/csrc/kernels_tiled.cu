@@ -37,6 +37,13 @@ struct BlockCoord {
 
 __device__ __forceinline__ BlockCoord decode_block(int key, const DevParams& P) {
   BlockCoord bc;
+  if (P.n_scenes == 1 && P.nb_shift[1] >= 0 && P.nb_shift[2] >= 0) {   // power-of-two grids: shifts
+    bc.scene = 0;
+    bc.b[0] = key >> (P.nb_shift[1] + P.nb_shift[2]);
+    bc.b[1] = (key >> P.nb_shift[2]) & (P.NB[1] - 1);
+    bc.b[2] = key & (P.NB[2] - 1);
+    return bc;
+  }
   const int bps = (int)P.blocks_per_scene;
   bc.scene = key / bps;
   const int local = key - bc.scene * bps;

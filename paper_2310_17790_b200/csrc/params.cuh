@@ -45,6 +45,7 @@ struct DevErr {
 struct DevParams {
   int N[3];          // nodes per axis
   int NB[3];         // blocks per axis
+  int nb_shift[3];   // log2 NB[a] when NB[a] is a power of two, else -1 (fast block decoding)
   int n_scenes;
   long long nodes_per_scene;
   long long blocks_per_scene;

@@ -275,6 +275,11 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   P.n_scenes = m->n_scenes;
   P.nodes_per_scene = (long long)grid_res[0] * grid_res[1] * grid_res[2];
   P.blocks_per_scene = (long long)P.NB[0] * P.NB[1] * P.NB[2];
+  for (int a = 0; a < 3; ++a) {
+    P.nb_shift[a] = -1;
+    for (int k = 0; k < 31; ++k)
+      if ((1 << k) == P.NB[a]) P.nb_shift[a] = k;
+  }
   P.dx = (float)dx;
   P.inv_dx = (float)(1.0 / dx);
   P.dt = (float)dt;
