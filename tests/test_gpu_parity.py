@@ -125,6 +125,22 @@ def test_c1_spin_200_substeps(nsf):
     assert ex <= BAR_TRAJ and disp <= 1e-3, (ex, disp)
 
 
+@pytest.mark.parametrize("name", [k for k in small_scenes().keys() if k != "dense_cluster"])
+def test_trajectory_100_substeps(nsf, name):
+    """Every model / force form over 100 substeps (three re-binnings with the cell-
+    ordered reorder): positions and velocities within the trajectory bar (1e-3)."""
+    sc = small_scenes()[name]
+    sim = make(nsf, sc)
+    sim.substep(100)
+    sim.sync()
+    g = gpu_state(sim)
+    sim.close()
+    P = mpm.params_from_config(sc.cfg)
+    ref = mpm.run({"x": sc.x, "v": sc.v, "C": sc.C, "F": sc.F, "tau": mpm.initial_tau(sc.F, P)}, P, 100)
+    ex, ev = rel_err(g["x"], ref["x"]), rel_err(g["v"], ref["v"])
+    assert ex <= BAR_TRAJ and ev <= BAR_TRAJ, (ex, ev)
+
+
 def test_binning_bit_exact(nsf):
     sc = small_scenes()["DP"]
     sim = make(nsf, sc)
