@@ -263,6 +263,7 @@ def run_ours(args):
     import paper_2310_17790_b200 as nsf
 
     sc = make_scene(args.config)
+    sc.cfg.deterministic = 1 if getattr(args, "deterministic", False) else 0
     n = sc.n
     stream = torch.cuda.Stream(device=dev)
     sim = nsf.Simulator(sc.cfg, stream=stream.cuda_stream)
@@ -380,7 +381,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenes/, seeded)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                        "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
-                       "replicas": world, "l2": "flushed before every timed substep (256 MB write outside the per-substep CUDA events)",
+                       "replicas": world, "deterministic": bool(sc.cfg.deterministic), "l2": "flushed before every timed substep (256 MB write outside the per-substep CUDA events)",
                        "step": STEP_DESC[args.config == "C5"]},
             "hbm_alg_gbs_whole_step": step_gbs,
             "hbm_alg_frac_whole_step": step_gbs / peak,
@@ -412,6 +413,8 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=2)
     ap.add_argument("--ref-sample", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="fixed-point (bitwise reproducible) P2G; reported in config")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

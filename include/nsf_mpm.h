@@ -105,7 +105,11 @@ typedef struct {
   double plate_y0;              /*   y_p(t_n) = plate_y0 + plate_velocity[1] n dt   */
   double plate_velocity[3];     /*   get v_i = plate_velocity, after the walls (#12)*/
   int32_t force_mode;           /* nsf_force_mode                                   */
-  int32_t deterministic;        /* reserved (1 = atomic-free ordered P2G); must be 0 */
+  int32_t deterministic;        /* 0: fastest (P2G float reductions in scheduling order);
+                                   1: P2G reduced in 64-bit fixed point with integer atomics
+                                   (units 2^-32 particle masses), so every substep is bitwise
+                                   reproducible, independent of particle order and launch
+                                   configuration; slower.  Other values: INVALID_ARGUMENT. */
   int32_t n_scenes;             /* >= 1; each scene owns a grid_res^3 grid          */
   double particle_volume;       /* V_p^0 (m^3); <= 0 -> dx^3/8 (8 ppc, #16); m = rho V0 */
   double stress_scale;          /* sigma_tau (Pa) multiplying the NSF output (#20)   */

@@ -153,7 +153,7 @@ def make_material(cfg) -> nsf_material:
     m.plate_y0 = cfg.plate_y0
     m.plate_velocity = (C.c_double * 3)(*cfg.plate_velocity)
     m.force_mode = cfg.force_mode
-    m.deterministic = 0
+    m.deterministic = int(getattr(cfg, "deterministic", 0))
     m.n_scenes = cfg.n_scenes
     m.particle_volume = cfg.particle_volume
     m.stress_scale = cfg.stress_scale

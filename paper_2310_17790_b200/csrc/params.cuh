@@ -63,6 +63,7 @@ struct DevParams {
   float mls_coef;    // dt V0 4/dx^2
   float gradw_coef;  // dt V0
   float stress_scale;
+  int deterministic;  // 1: fixed-point P2G (kernels_det.cu), bitwise reproducible
 };
 
 __host__ __device__ inline long long block_id(int b0, int b1, int b2, const DevParams& P) {

@@ -115,17 +115,29 @@ static bool fused_enabled() {
 //               current state and `flags` marks its touched blocks; counts = 0.
 nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
   HandleView v = view(h);
-  pb->tiled = v.model != NSF_NEURAL_STRESS;
+  const bool det = v.P->deterministic != 0;
+  pb->tiled = v.model != NSF_NEURAL_STRESS && !det;
   pb->fused = pb->tiled && v.P->force_mode == NSF_FORCE_MLS && fused_enabled();
   pb->since_rebin = 0;
   pb->launch_total = 0;
+  pb->nsf_sorted = false;
   if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess)
     return NSF_ERR_CUDA;
   if (cudaMemsetAsync(v.acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return NSF_ERR_CUDA;
   if (cudaMemsetAsync(pb->flags, 0, sizeof(int) * pb->total_blocks, v.stream) != cudaSuccess) return NSF_ERR_CUDA;
   if (cudaMemsetAsync(pb->touched + pb->total_blocks, 0, sizeof(int) * 4, v.stream) != cudaSuccess)
     return NSF_ERR_CUDA;
-  if (pb->fused) {
+  if (det) {
+    // fixed-point accumulator (deterministic P2G); nothing is sorted
+    if (!pb->fx) {
+      pb->fx = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * 4 * v.total_nodes);
+      if (!pb->fx) return NSF_ERR_OUT_OF_MEMORY;
+    }
+    if (cudaMemsetAsync(pb->fx, 0, sizeof(unsigned long long) * 4 * v.total_nodes, v.stream) != cudaSuccess)
+      return NSF_ERR_CUDA;
+    if (v.model == NSF_NEURAL_STRESS && v.X)
+      launch_gather_xref(v.stream, v.n, v.X, v.pitch, v.ids[0], v.S[0]);
+  } else if (pb->fused) {
     const int cur = enqueue_rebin(h, pb, v, 0);
     set_cur(h, cur);
     v = view(h);
@@ -212,6 +224,22 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
   HandleView v = view(h);
   const bool nsf_model = v.model == NSF_NEURAL_STRESS;
   int launches = 0;
+  if (v.P->deterministic) {
+    // deterministic: [MLP ->] fixed-point P2G -> grid update of the touched blocks -> G2P (in place)
+    if (nsf_model) {
+      PLAUNCH(h, "nsf_mlp",
+              launch_nsf_mlp(v.stream, v.n, v.S[cur] + PXR * kTileP, -1, v.scene_off, v.n_scenes, v.z, v.dz, v.r,
+                             v.d_step, *v.mlp, v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0));
+      launches += (v.n > 0);
+    }
+    PLAUNCH(h, "p2g_fixed", launch_p2g_fixed(v.stream, v.n, v.S[cur], v.scene_off, v.n_scenes, pb->fx, pb, *v.P));
+    PLAUNCH(h, "grid_update", launch_grid_update_fixed(v.stream, pb, pb->fx, v.vel, *v.P, v.d_step));
+    PLAUNCH(h, "g2p_direct", launch_g2p_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.vel, *v.P,
+                                               v.err, v.d_step, nsf_model ? 0 : 1));
+    launches += (v.n > 0) + 2;
+    pb->launches = launches;
+    return cur;
+  }
   if (pb->fused) {
     PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
     PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));

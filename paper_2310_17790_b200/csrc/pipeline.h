@@ -35,6 +35,7 @@ struct PipelineBuffers {
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
   int* nsf_done = nullptr;          // reduced path: CTA completion counter of the G2P kernel
   float4* dbg_acc = nullptr;        // reduced path: scratch grids for debug_grid
+  unsigned long long* fx = nullptr; // deterministic mode: fixed-point P2G accumulator [total_nodes][4]
   float4* dbg_vel = nullptr;
   int rebin_every = 32;             // fused pipeline: substeps between re-binnings
   int since_rebin = 0;              // host counter
@@ -114,6 +115,11 @@ void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc,
                               const int64_t* d_step);
 void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,
                     const int32_t* perm);
+// kernels_det.cu (deterministic mode)
+void launch_p2g_fixed(cudaStream_t st, int64_t n, const float* S, const int64_t* scene_off, int n_scenes,
+                      unsigned long long* fx, PipelineBuffers* pb, const DevParams& P);
+void launch_grid_update_fixed(cudaStream_t st, PipelineBuffers* pb, unsigned long long* fx, float4* vel,
+                              const DevParams& P, const int64_t* d_step);
 void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                           int32_t* ids_out, const PipelineBuffers* pb, const DevParams& P);
 void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,

@@ -248,7 +248,7 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
     if (grid_res[a] < 4 || grid_res[a] % 4 != 0 || grid_res[a] < 2 * m->bc_width + 3)
       return NSF_ERR_INVALID_ARGUMENT;
   if (m->force_mode < 0 || m->force_mode > 1) return NSF_ERR_INVALID_ARGUMENT;
-  if (m->deterministic != 0) return NSF_ERR_INVALID_ARGUMENT;
+  if (m->deterministic != 0 && m->deterministic != 1) return NSF_ERR_INVALID_ARGUMENT;
   if (m->n_scenes < 1) return NSF_ERR_INVALID_ARGUMENT;
   if (m->model == NSF_NEURAL_STRESS && !std::isfinite(m->stress_scale)) return NSF_ERR_INVALID_ARGUMENT;
   int device = 0;
@@ -299,6 +299,7 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   P.mls_coef = (float)(dt * V0 * 4.0 / (dx * dx));
   P.gradw_coef = (float)(dt * V0);
   P.stress_scale = (float)m->stress_scale;
+  P.deterministic = m->deterministic;
   h->total_nodes = P.nodes_per_scene * m->n_scenes;
   h->total_blocks = P.blocks_per_scene * m->n_scenes;
 

@@ -58,6 +58,7 @@ class Config:
     plate_y0: float = 0.0
     plate_velocity: tuple = (0.0, 0.0, 0.0)
     force_mode: int = FORCE_MLS
+    deterministic: int = 0         # 1: fixed-point (bitwise reproducible) P2G on the GPU
     particle_volume: float = 0.0   # <=0 -> dx^3/8
     n_scenes: int = 1
     stress_scale: float = 100.0    # sigma_tau for the NSF output (reading #20)
