@@ -1021,8 +1021,10 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
   asm volatile("cp.async.commit_group;" ::: "memory");
   const float cC_unused = 0.0f;
   (void)cC_unused;
+  // segment tickets: the first here, each next one claimed after phase 1 of the
+  // current segment (its round trip overlaps phase 2)
+  if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
   while (true) {
-    if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
     __syncthreads();   // also: previous segment's readers of part/slot are done
     const int bi = sm.next;
     if (bi >= nblk) break;
@@ -1077,6 +1079,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
 #endif
     }
     __syncthreads();
+    if (tid == 0) sm.next = atomicAdd(&counters[3], 1);   // the next segment (bi is in registers)
     // ---- phase 2: per (cell, stencil plane) register accumulation ----
     float accm[9], accp[9][3];
 #pragma unroll
