@@ -774,8 +774,8 @@ static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shar
 #define NSF_FUSED_VTILE 1                      // G2P reads a shared-memory velocity tile (else global gathers)
 #endif
 #ifndef NSF_DENSE_THREADS
-#define NSF_DENSE_THREADS 192                  // dense variant: threads per CTA (>= 192)
-#endif
+#define NSF_DENSE_THREADS 256                  // dense variant: threads per CTA (>= 192): a full 512-particle
+#endif                                         // block is exactly two phase-1 passes
 #ifndef NSF_DENSE_MIN_BLOCKS
 #define NSF_DENSE_MIN_BLOCKS NSF_FUSED_MIN_BLOCKS   // dense variant: CTAs per SM
 #endif
