@@ -89,3 +89,53 @@ def test_deterministic_reduced(nsf):
                                  step=0, tau_override=outs[0]["tau"])
     e = np.linalg.norm(outs[0]["x"] - ref["x"]) / np.linalg.norm(ref["x"])
     assert e <= BAR_STEP, e
+
+
+def test_two_scenes_equal_one_scene_bitwise(nsf):
+    """Full-order model with n_scenes = 2 (block keys carry the scene): two copies
+    of a scene on one handle reproduce the single-scene run bit for bit
+    (deterministic mode), each copy on its own grid."""
+    base = det(small_scenes()["FC_ragged"])
+    one = _run(nsf, base, np.arange(base.n), 20)
+    two = copy.deepcopy(base)
+    two.cfg.n_scenes = 2
+    two.x = np.concatenate([base.x, base.x])
+    two.v = np.concatenate([base.v, base.v])
+    two.C = np.concatenate([base.C, base.C])
+    two.F = np.concatenate([base.F, base.F])
+    two.scene_offsets = np.array([0, base.n, 2 * base.n], np.int64)
+    both = _run(nsf, two, np.arange(two.n), 20)
+    for f in one:
+        for s in range(2):
+            part = both[f][s * base.n:(s + 1) * base.n]
+            assert np.array_equal(part.view(np.uint32), one[f].view(np.uint32)), (f, s)
+
+
+def test_two_scenes_fused_parity(nsf):
+    """The fused (default) pipeline with two scenes: each scene matches the oracle
+    of its own particles."""
+    from tests.parity_util import compare, voigt_to_mat
+    base = small_scenes()["VM"]
+    two = copy.deepcopy(base)
+    two.cfg.n_scenes = 2
+    rng = np.random.default_rng(3)
+    keep = np.sort(rng.choice(base.n, base.n // 2, replace=False))
+    two.x = np.concatenate([base.x, base.x[keep]])
+    two.v = np.concatenate([base.v, -base.v[keep]])
+    two.C = np.concatenate([base.C, base.C[keep]])
+    two.F = np.concatenate([base.F, base.F[keep]])
+    two.scene_offsets = np.array([0, base.n, base.n + len(keep)], np.int64)
+    sim = nsf.Simulator(two.cfg)
+    sim.load_scene(two)
+    sim.substep(5)
+    s0 = gpu_state(sim)
+    sim.substep(1)
+    sim.sync()
+    s1 = gpu_state(sim)
+    sim.close()
+    P = mpm.params_from_config(base.cfg)
+    for a, b in zip(two.scene_offsets[:-1], two.scene_offsets[1:]):
+        ref = mpm.substep({k: s0[k][a:b] for k in ("x", "v", "C", "F", "tau")}, P, 5)
+        got = {k: s1[k][a:b] for k in ("x", "v", "C", "F", "tau")}
+        errs = compare(got, ref, base.cfg)
+        assert all(e <= BAR_STEP for e in errs.values()), errs
