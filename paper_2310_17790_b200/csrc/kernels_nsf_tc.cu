@@ -233,11 +233,17 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  // layer-1 B: row j = [W_1[j][0..15] | W_1[j][0..15]] (zero beyond in_dim), 16-byte chunk c of row j at
-  // j*128 + ((c ^ (j & 7)) << 4)
+  // layer-1 B: row j = [W_1[j][0..in) b_hi b_lo 0.. | the same] (the inputs carry 1, 1 at columns in_dim,
+  // in_dim + 1, so the MMA adds the fp32 bias b_1 = b_hi + b_lo, split in two tf32 parts); 16-byte chunk c of
+  // row j at j*128 + ((c ^ (j & 7)) << 4)
   for (int e = tid; e < kW * 32; e += kThreads) {
     const int j = e >> 5, k = e & 31, i = k & 15;
-    const float w = i < in_dim ? __uint_as_float(((uint32_t)mlp.W[mlp.w_off[0] + j * in_dim + i]) << 16) : 0.0f;
+    const float bj = mlp.b[mlp.b_off[0] + j];
+    const float b_hi = __uint_as_float(to_tf32(bj));
+    float w = 0.0f;
+    if (i < in_dim) w = __uint_as_float(((uint32_t)mlp.W[mlp.w_off[0] + j * in_dim + i]) << 16);
+    else if (i == in_dim) w = b_hi;
+    else if (i == in_dim + 1) w = __uint_as_float(to_tf32(bj - b_hi));
     *reinterpret_cast<float*>(sm.w1t + j * 128 + ((((k >> 2) ^ (j & 7))) << 4) + (k & 3) * 4) = w;
   }
   for (int e = tid; e < (kMaxHiddenMMA + 1) * kW; e += kThreads) {
@@ -293,6 +299,8 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     }
     for (int k = 0; k < r && k < 13; ++k)
       u_[3 + k] = z[scene_ * r + k] + (float)step * (dz ? dz[scene_ * r + k] : 0.0f);
+    u_[in_dim] = 1.0f;       // bias columns of the layer-1 B operand
+    u_[in_dim + 1] = 1.0f;
   };
   float u[16];
   int scene = 0;
@@ -335,15 +343,9 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
 #pragma unroll 1
     for (int c0 = 0; c0 < kW; c0 += 32) {
       float h[32];
-      tmem_ld32(d_col + lane_sel + c0, h);
+      tmem_ld32(d_col + lane_sel + c0, h);   // bias already added by the MMA
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 b = lds_f4(bias_saddr + (uint32_t)(c0 + 4 * q) * 4u);
-        h[4 * q] = elu(h[4 * q] + b.x);
-        h[4 * q + 1] = elu(h[4 * q + 1] + b.y);
-        h[4 * q + 2] = elu(h[4 * q + 2] + b.z);
-        h[4 * q + 3] = elu(h[4 * q + 3] + b.w);
-      }
+      for (int q = 0; q < 32; ++q) h[q] = elu(h[q]);
       store_act32(a_saddr, t, c0, h);
     }
     fence_before();
@@ -425,7 +427,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
 }
 
 bool nsf_mlp_tc_supported(const MlpDev& mlp) {
-  return mlp.width == kW && mlp.n_hidden >= 2 && mlp.n_hidden - 1 <= kMaxHiddenMMA && mlp.in_dim <= 16 &&
+  return mlp.width == kW && mlp.n_hidden >= 2 && mlp.n_hidden - 1 <= kMaxHiddenMMA && mlp.in_dim <= 14 &&
          mlp.out_dim <= 8;
 }
 
