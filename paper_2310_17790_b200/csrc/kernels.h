@@ -35,6 +35,8 @@ struct MlpDev {
   int in_dim, width, n_hidden, out_dim;
   int64_t w_off[10];    // element offsets of each layer's weights
   int64_t b_off[10];
+  unsigned int* ctr;    // [2] tile ticket + CTA completion counter of the tensor-core kernel (zero between
+                        // launches), or nullptr for a static tile assignment
 };
 // tcgen05 tensor-core MLP (kernels_nsf_tc.cu): width 128, 2..4 hidden layers
 bool nsf_mlp_tc_supported(const MlpDev& mlp);

@@ -49,6 +49,7 @@ struct __align__(1024) Smem {
   float bias[kMaxHiddenMMA + 1][kW];        // b_1 .. b_L
   float bout[kOutN];
   unsigned long long bar[kStreams];          // per-stream MMA-completion mbarriers
+  unsigned int tk[kStreams];                 // per-stream next tile (dynamic tickets)
   uint32_t tmem_base;
 };
 
@@ -302,10 +303,18 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     u_[in_dim] = 1.0f;       // bias columns of the layer-1 B operand
     u_[in_dim + 1] = 1.0f;
   };
+  // tiles: dynamic tickets (each stream claims its next tile while working on
+  // the current one) or, without a counter, round robin
+  int64_t tile = (int64_t)blockIdx.x * kStreams + s;
+  if (mlp.ctr) {
+    if (t == 0) sm.tk[s] = atomicAdd(mlp.ctr, 1u);
+    stream_barrier(s);
+    tile = sm.tk[s];
+  }
   float u[16];
   int scene = 0;
-  load_inputs((int64_t)blockIdx.x * kStreams + s, u, scene);
-  for (int64_t tile = (int64_t)blockIdx.x * kStreams + s; tile < n_tiles; tile += tile_stride) {
+  load_inputs(tile, u, scene);
+  while (tile < n_tiles) {
     const int64_t p = tile * kM + t;
     const bool live = p < n;
     // A row t = [hi(u) | lo(u)], 32 tf32 = one 128-byte swizzled line
@@ -328,6 +337,7 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
         sts_u4(row + (((uint32_t)(c + 4) ^ sw) << 4), lo);
       }
     }
+    if (mlp.ctr && t == 0) sm.tk[s] = atomicAdd(mlp.ctr, 1u);   // read after the tile's last barrier
     fence_async_smem();
     stream_barrier(s);
     if (t == 0) {
@@ -415,14 +425,23 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       }
       if (q.enabled) nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);   // reduced P2G, tau from registers
     }
-    load_inputs(tile + tile_stride, u, scene);   // next tile's inputs (latency overlaps the barrier)
+    const int64_t next = mlp.ctr ? (int64_t)sm.tk[s] : tile + tile_stride;
+    load_inputs(next, u, scene);   // next tile's inputs (latency overlaps the barrier)
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile
+    tile = next;
   }
   __syncthreads();
   if (warp == 0) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+  if (mlp.ctr && tid == 0) {   // the last CTA resets the counters for the next launch
+    __threadfence();
+    if (atomicAdd(mlp.ctr + 1, 1u) == gridDim.x - 1) {
+      mlp.ctr[0] = 0u;
+      mlp.ctr[1] = 0u;
+    }
   }
 }
 

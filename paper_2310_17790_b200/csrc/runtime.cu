@@ -54,6 +54,7 @@ struct nsf_mpm {
   // NSF
   uint16_t* W = nullptr;
   float* b = nullptr;
+  unsigned int* mlp_ctr = nullptr;   // MLP tile ticket + completion counter (kernels_nsf_tc.cu)
   MlpDev mlp{};
   bool mlp_loaded = false;
   float* X = nullptr;            // 3 planes, pitch
@@ -449,6 +450,11 @@ nsf_status nsf_mpm_load_stress_field(nsf_mpm* h, int32_t in_dim, int32_t width, 
   if ((s = to_device(h, b, sizeof(float) * bo, on_device, h->b)) != NSF_OK) return s;
   M.W = h->W;
   M.b = h->b;
+  if (!h->mlp_ctr) {
+    if ((s = alloc_into(h, &h->mlp_ctr, sizeof(unsigned int) * 4)) != NSF_OK) return s;
+    CK(cudaMemsetAsync(h->mlp_ctr, 0, sizeof(unsigned int) * 4, h->stream));
+  }
+  M.ctr = h->mlp_ctr;
   if (X_ref) {
     int64_t n = h->n;
     if ((s = alloc_into(h, &h->X, sizeof(float) * 3 * h->pitch)) != NSF_OK) return s;
