@@ -14,8 +14,6 @@ void launch_pack(cudaStream_t st, int64_t n, const float* S, int64_t pitch, cons
                  int plane0, int ncomp, float* out);
 void launch_p2g_direct(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
                        const int64_t* scene_off, int n_scenes, float4* acc, const DevParams& P);
-void launch_grid_update_dense(cudaStream_t st, int64_t total_nodes, float4* acc, float4* vel,
-                              const DevParams& P, const int64_t* d_step);
 void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, const int64_t* scene_off,
                        int n_scenes, const float4* vel, const DevParams& P, DevErr* err, int64_t* d_step,
                        int with_F);

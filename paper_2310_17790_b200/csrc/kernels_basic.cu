@@ -145,32 +145,6 @@ void launch_p2g_direct(cudaStream_t st, int64_t n, const float* S, int64_t pitch
   else k_p2g_direct<1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, acc, P);
 }
 
-// dense update over every node of every scene: vel = update(acc); acc = 0
-__global__ void k_grid_update_dense(int64_t total_nodes, float4* acc, float4* vel, DevParams P,
-                                    const int64_t* d_step) {
-  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= total_nodes) return;
-  float4 a = acc[g];
-  if (a.x == 0.0f && a.y == 0.0f && a.z == 0.0f && a.w == 0.0f) {
-    vel[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
-  int64_t local = g % P.nodes_per_scene;
-  int64_t blk = local >> 6;
-  int l = (int)(local & 63);
-  int b2 = (int)(blk % P.NB[2]);
-  int b1 = (int)((blk / P.NB[2]) % P.NB[1]);
-  int b0 = (int)(blk / ((int64_t)P.NB[2] * P.NB[1]));
-  int i = b0 * 4 + (l >> 4), j = b1 * 4 + ((l >> 2) & 3), k = b2 * 4 + (l & 3);
-  vel[g] = grid_node_update(a, i, j, k, P, plate_y(P, *d_step));
-  acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
-void launch_grid_update_dense(cudaStream_t st, int64_t total_nodes, float4* acc, float4* vel,
-                              const DevParams& P, const int64_t* d_step) {
-  int bs = 256;
-  k_grid_update_dense<<<(unsigned)((total_nodes + bs - 1) / bs), bs, 0, st>>>(total_nodes, acc, vel, P, d_step);
-}
 
 // ---------------------------------------------------------------------------
 // G2P + constitutive, one thread per particle, in place (reads and writes index p).
