@@ -129,13 +129,17 @@ def return_map_von_mises(sigma, mu, tau_Y):
 def elastoplastic_update(F_trial, model, mu, lam, alpha=0.0, tau_Y=0.0):
     """F^E = returnMap(F_trial), tau = tau(F^E).
 
-    model 0 fixed-corotated (F^E = F_trial), 1 Drucker-Prager, 2 von Mises.
+    model 0 fixed-corotated (F^E = F_trial), 1 Drucker-Prager, 2 von Mises,
+    4 the appendix's "StVK elasticity": tau = U (2 mu eps + lambda sum(eps) 1) U^T with
+    eps = log(Sigma) and F^E = F_trial, i.e. Hencky elasticity without a return map (reading #3 for U^T).
     Returns (F_E, tau).
     """
     F_trial = np.asarray(F_trial, dtype=np.float64)
     if model == 0:
         return F_trial.copy(), tau_fixed_corotated(F_trial, mu, lam)
     U, s, V = svd_rotation_safe(F_trial)
+    if model == 4:
+        return F_trial.copy(), tau_hencky(U, s, mu, lam)
     if model == 1:
         Z = return_map_drucker_prager(s, mu, lam, alpha)
     elif model == 2:

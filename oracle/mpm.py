@@ -65,6 +65,7 @@ class Params:
     plate_y0: float = 0.0
     plate_velocity: tuple = (0.0, 0.0, 0.0)
     force_mode: int = 0        # 0 MLS, 1 GRADW
+    transfer: int = 0          # 0 APIC, 1 PIC
 
     @property
     def inv_dx(self):
@@ -82,7 +83,8 @@ def params_from_config(cfg) -> Params:
                   tau_Y=cfg.yield_stress, mass=cfg.rho * V0, V0=V0,
                   gravity=tuple(cfg.gravity), bc=tuple(cfg.bc), bc_width=cfg.bc_width,
                   plate_enabled=cfg.plate_enabled, plate_y0=cfg.plate_y0,
-                  plate_velocity=tuple(cfg.plate_velocity), force_mode=cfg.force_mode)
+                  plate_velocity=tuple(cfg.plate_velocity), force_mode=cfg.force_mode,
+                  transfer=getattr(cfg, "transfer", 0))
 
 
 # ---------------------------------------------------------------------------
@@ -132,8 +134,11 @@ def p2g(x, v, C, tau, P: Params):
     tau = np.asarray(tau, np.float64)
     node, W, d, gW = _stencil(x, P)
     m = P.mass
-    # APIC momentum: w m (v_p + C_p d)
-    mom = W[..., None] * m * (v[:, None, :] + np.einsum("pij,pnj->pni", C, d))
+    # APIC momentum: w m (v_p + C_p d); PIC: w m v_p
+    if P.transfer == 1:
+        mom = W[..., None] * m * np.broadcast_to(v[:, None, :], d.shape)
+    else:
+        mom = W[..., None] * m * (v[:, None, :] + np.einsum("pij,pnj->pni", C, d))
     if P.force_mode == 0:   # MLS force (reading #1): -dt V0 (4/dx^2) w tau d
         mom -= P.dt * P.V0 * (4.0 / P.dx ** 2) * W[..., None] * np.einsum("pij,pnj->pni", tau, d)
     else:                   # Eq. (6): -dt tau grad(w) V0

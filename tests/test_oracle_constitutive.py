@@ -238,3 +238,33 @@ def test_elastoplastic_update_models():
             return_map_drucker_prager(s, mu, lam, dp_alpha(30))
         same = np.all(Z == s, axis=1)
         assert np.allclose(FE[same], F[same], atol=1e-14)
+
+
+def test_stvk_as_printed_is_elastic_hencky():
+    """Model 4, the appendix's "StVK elasticity": no return map
+    (F^E = F_trial even far beyond any yield surface), tau = dpsi/dF F^T with the Hencky
+    energy psi = mu |log Sigma|^2 + lam/2 (sum log Sigma)^2 (U^T per reading #3), zero at
+    F = I, and isotropic: tau(Q F) = Q tau(F) Q^T for a rotation Q."""
+    from oracle.constitutive import elastoplastic_update
+    rng = np.random.default_rng(11)
+    mu, lam = 1.3, 0.9
+
+    def psi(F):
+        s = np.linalg.svd(F, compute_uv=False)
+        e = np.log(s)
+        return mu * np.sum(e ** 2) + 0.5 * lam * np.sum(e) ** 2
+
+    FE, tau0 = elastoplastic_update(np.eye(3)[None], 4, mu, lam)
+    assert np.allclose(tau0, 0.0, atol=1e-14)
+    for _ in range(12):
+        F = np.eye(3) + 0.4 * rng.normal(size=(3, 3))
+        if np.linalg.det(F) < 0.2:
+            continue
+        FE, tau = elastoplastic_update(F[None], 4, mu, lam)
+        assert np.array_equal(FE[0], F)
+        assert np.allclose(tau[0], _fd_tau(psi, F), atol=2e-7)
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        if np.linalg.det(q) < 0:
+            q[:, 0] *= -1
+        _, tq = elastoplastic_update((q @ F)[None], 4, mu, lam)
+        assert np.allclose(tq[0], q @ tau[0] @ q.T, atol=1e-12)

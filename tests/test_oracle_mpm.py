@@ -305,3 +305,26 @@ def test_brute_force_consistency_tiny():
         for r in range(len(uid)):
             m, mv = grid[tuple(gnode[r])]
             assert np.isclose(gm[r], m, rtol=1e-13) and np.allclose(gp[r], mv, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("fm", [0, 1])
+def test_pic_transfer(fm):
+    """PIC: m_i v_i = sum_p w m_p v_p.  Linear momentum is
+    conserved; the grid's angular momentum is exactly sum_p x_p x m v_p (the
+    B-spline's first moment), i.e. the particles' affine spin is dropped, unlike
+    APIC (test_p2g_angular_momentum); mass is unchanged; and the PIC and APIC
+    momenta differ by exactly the affine term."""
+    import dataclasses
+    rng = np.random.default_rng(7)
+    P = P_free(fm)
+    Ppic = dataclasses.replace(P, transfer=1)
+    x, v, C, F, tau = rand_state(rng, 150)
+    zero = np.zeros_like(tau)
+    _, gnode, gm, gp = p2g(x, v, C, zero, Ppic)
+    assert np.allclose(gp.sum(0), (P.mass * v).sum(0), rtol=1e-12, atol=1e-14)
+    L_grid = np.cross(gnode * P.dx, gp).sum(0)
+    assert np.allclose(L_grid, np.cross(x, P.mass * v).sum(0), rtol=1e-11, atol=1e-13)
+    _, gnode_a, gm_a, gp_a = p2g(x, v, C, zero, P)
+    assert np.array_equal(gnode, gnode_a) and np.allclose(gm, gm_a, rtol=1e-14)
+    _, _, _, gp_c = p2g(x, np.zeros_like(v), C, zero, P)   # APIC with v = 0: the affine term alone
+    assert np.allclose(gp_a - gp, gp_c, rtol=1e-10, atol=1e-14)
