@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define NSF_MPM_ABI_VERSION 1
+#define NSF_MPM_ABI_VERSION 2
 
 typedef struct nsf_mpm nsf_mpm; /* opaque; owns all device state */
 
@@ -78,8 +78,15 @@ typedef enum {
   NSF_FIXED_COROTATED = 0, /* tau = 2 mu (F - R) F^T + lambda (J-1) J I   (#2) */
   NSF_DRUCKER_PRAGER = 1,  /* sand return map */
   NSF_VON_MISES = 2,       /* perfect plasticity, radial return          (#4) */
-  NSF_NEURAL_STRESS = 3    /* tau = sigma_tau h(X, z) */
+  NSF_NEURAL_STRESS = 3,   /* tau = sigma_tau h(X, z) */
+  NSF_HENCKY = 4           /* the appendix's "StVK elasticity": Hencky, no return map (#3) */
 } nsf_model;
+
+/* Particle-grid transfer of P2G's momentum. */
+typedef enum {
+  NSF_TRANSFER_APIC = 0,   /* m_i v_i = sum w m_p (v_p + C_p (x_i - x_p)) */
+  NSF_TRANSFER_PIC = 1     /* m_i v_i = sum w m_p v_p (C_p still updated and used for F)  */
+} nsf_transfer;
 
 /* Wall boundary condition on the nodes within bc_width of a face (#11, #12). */
 typedef enum {
@@ -113,6 +120,7 @@ typedef struct {
   int32_t n_scenes;             /* >= 1; each scene owns a grid_res^3 grid          */
   double particle_volume;       /* V_p^0 (m^3); <= 0 -> dx^3/8 (8 ppc, #16); m = rho V0 */
   double stress_scale;          /* sigma_tau (Pa) multiplying the NSF output (#20)   */
+  int32_t transfer;             /* nsf_transfer (ABI 2)                              */
 } nsf_material;
 
 /* read_state field mask; dst[k] is the k-th requested field in bit order. */

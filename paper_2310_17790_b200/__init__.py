@@ -23,7 +23,8 @@ NSF_OK, NSF_ERR_INVALID_ARGUMENT, NSF_ERR_OUT_OF_DOMAIN, NSF_ERR_NONFINITE, NSF_
     NSF_ERR_OUT_OF_MEMORY, NSF_ERR_BAD_STATE = range(7)
 STATUS_NAMES = ["NSF_OK", "NSF_ERR_INVALID_ARGUMENT", "NSF_ERR_OUT_OF_DOMAIN", "NSF_ERR_NONFINITE",
                 "NSF_ERR_CUDA", "NSF_ERR_OUT_OF_MEMORY", "NSF_ERR_BAD_STATE"]
-NSF_FIXED_COROTATED, NSF_DRUCKER_PRAGER, NSF_VON_MISES, NSF_NEURAL_STRESS = range(4)
+NSF_FIXED_COROTATED, NSF_DRUCKER_PRAGER, NSF_VON_MISES, NSF_NEURAL_STRESS, NSF_HENCKY = range(5)
+NSF_TRANSFER_APIC, NSF_TRANSFER_PIC = range(2)
 NSF_BC_NONE, NSF_BC_STICKY, NSF_BC_SLIP = range(3)
 NSF_FORCE_MLS, NSF_FORCE_GRADW = range(2)
 NSF_FIELD_X, NSF_FIELD_V, NSF_FIELD_C, NSF_FIELD_F, NSF_FIELD_TAU = 1, 2, 4, 8, 16
@@ -45,7 +46,7 @@ class nsf_material(C.Structure):
                 ("plate_enabled", C.c_int32), ("plate_y0", C.c_double),
                 ("plate_velocity", C.c_double * 3), ("force_mode", C.c_int32),
                 ("deterministic", C.c_int32), ("n_scenes", C.c_int32),
-                ("particle_volume", C.c_double), ("stress_scale", C.c_double)]
+                ("particle_volume", C.c_double), ("stress_scale", C.c_double), ("transfer", C.c_int32)]
 
 
 class NsfError(RuntimeError):
@@ -157,6 +158,7 @@ def make_material(cfg) -> nsf_material:
     m.n_scenes = cfg.n_scenes
     m.particle_volume = cfg.particle_volume
     m.stress_scale = cfg.stress_scale
+    m.transfer = int(getattr(cfg, "transfer", 0))
     return m
 
 

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(128) k_p2g_direct(int64_t n, const float* __re
   // Q = m C - (MLS) dt V0 4/dx^2 tau
   float Q[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cp[k] - (FORCE == 0 ? P.mls_coef * T[k] : 0.0f);
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cp[k] - (FORCE == 0 ? P.mls_coef * T[k] : 0.0f);
   float4* base_ptr = acc + (int64_t)scene * P.nodes_per_scene;
 #pragma unroll
   for (int a = 0; a < 3; ++a)

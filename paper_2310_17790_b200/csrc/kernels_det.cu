@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(128) k_p2g_fixed(int64_t n, const float* __res
   const float T[9] = {tp[0], tp[5], tp[4], tp[5], tp[1], tp[3], tp[4], tp[3], tp[2]};
   float Q[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cp[k] - (FORCE == 0 ? P.mls_coef * T[k] : 0.0f);
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cp[k] - (FORCE == 0 ? P.mls_coef * T[k] : 0.0f);
   const float sm = kFx / m;   // momentum -> fixed point
   const int64_t so = (int64_t)scene * P.nodes_per_scene;
 #pragma unroll

@@ -121,7 +121,7 @@ __device__ __forceinline__ void p2g_stage_particle(const float* __restrict__ S, 
   const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
   float Q[9];   // Q = m C - dt V0 (4/dx^2) tau  (MLS, reading #1)
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cm[k] - P.mls_coef * Tm[k];
   // contribution to node base + o:  W_o [ m ; m v + Q (o - f) dx ] = W_o [ m ; u0 + dx Q o ]
   const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
   const float u0x = m * v0 - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2);
@@ -144,7 +144,7 @@ __device__ __forceinline__ void p2g_stage_values(const float x[3], const float v
   const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
   float Q[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cm[k] - P.mls_coef * Tm[k];
   const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
   const float u0x = m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2);
   const float u0y = m * v[1] - P.dx * (Q[3] * f0 + Q[4] * f1 + Q[5] * f2);
@@ -180,7 +180,7 @@ __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float
   const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
   float Q[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cm[k] - P.mls_coef * Tm[k];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -240,7 +240,7 @@ __device__ __forceinline__ void p2g_scatter_warp(bool direct, const float x[3], 
     const float Tm[9] = {pT[0], pT[5], pT[4], pT[5], pT[1], pT[3], pT[4], pT[3], pT[2]};
     float Q[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Q[k] = m * pC[k] - P.mls_coef * Tm[k];
+    for (int k = 0; k < 9; ++k) Q[k] = P.mC * pC[k] - P.mls_coef * Tm[k];
     for (int node = r; node < 27; node += nact) {
       const int a = node / 9, b = (node / 3) % 3, c = node % 3;
       const float wa = a == 0 ? ax[0].w[0] : (a == 1 ? ax[0].w[1] : ax[0].w[2]);
@@ -881,7 +881,7 @@ __device__ __forceinline__ void p2g_stage_values_f(const float x[3], const float
   const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
   float Q[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cm[k] - P.mls_coef * Tm[k];
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cm[k] - P.mls_coef * Tm[k];
   const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
   const float vals[kSlotFields] = {a0.w[0], a0.w[1], a0.w[2], a1.w[0], a1.w[1], a1.w[2], a2.w[0], a2.w[1], a2.w[2],
                                    m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2),

@@ -64,6 +64,7 @@ struct DevParams {
   float gradw_coef;  // dt V0
   float stress_scale;
   int deterministic;  // 1: fixed-point P2G (kernels_det.cu), bitwise reproducible
+  float mC;           // affine mass of P2G: m_p (APIC) or 0 (PIC)
 };
 
 __host__ __device__ inline long long block_id(int b0, int b1, int b2, const DevParams& P) {

@@ -125,7 +125,7 @@ __device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int scene, const 
   const float T[9] = {tp[0], tp[5], tp[4], tp[5], tp[1], tp[3], tp[4], tp[3], tp[2]};
   float Q[9];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) Q[k] = m * Cp[k] - P.mls_coef * T[k];
+  for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cp[k] - P.mls_coef * T[k];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll

@@ -238,7 +238,8 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   if (!grid_res || !m) return NSF_ERR_INVALID_ARGUMENT;
   if (!(dx > 0) || !(dt > 0) || !std::isfinite(dx) || !std::isfinite(dt)) return NSF_ERR_INVALID_ARGUMENT;
   if (!(m->E > 0) || !(m->nu >= 0 && m->nu < 0.5) || !(m->rho > 0)) return NSF_ERR_INVALID_ARGUMENT;
-  if (m->model < 0 || m->model > 3) return NSF_ERR_INVALID_ARGUMENT;
+  if (m->model < 0 || m->model > 4) return NSF_ERR_INVALID_ARGUMENT;
+  if (m->transfer != NSF_TRANSFER_APIC && m->transfer != NSF_TRANSFER_PIC) return NSF_ERR_INVALID_ARGUMENT;
   if (m->model == NSF_DRUCKER_PRAGER && !(m->friction_angle_deg > 0 && m->friction_angle_deg < 90))
     return NSF_ERR_INVALID_ARGUMENT;
   if (!(m->yield_stress >= 0)) return NSF_ERR_INVALID_ARGUMENT;
@@ -296,6 +297,11 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   P.plate_enabled = m->plate_enabled;
   P.plate_y0 = (float)m->plate_y0;
   P.model = m->model;
+  if (m->model == NSF_HENCKY) {   // Hencky without a return map = the von Mises code path that never yields
+    P.model = NSF_VON_MISES;
+    P.tau_Y = INFINITY;
+  }
+  P.mC = m->transfer == NSF_TRANSFER_PIC ? 0.0f : P.mass;
   P.force_mode = m->force_mode;
   P.mls_coef = (float)(dt * V0 * 4.0 / (dx * dx));
   P.gradw_coef = (float)(dt * V0);

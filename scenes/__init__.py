@@ -31,7 +31,8 @@ import numpy as np
 
 # ---------------------------------------------------------------------------
 # model / bc / force-mode codes (mirror include/nsf_mpm.h enums; plain ints)
-FIXED_COROTATED, DRUCKER_PRAGER, VON_MISES, NEURAL_STRESS = 0, 1, 2, 3
+FIXED_COROTATED, DRUCKER_PRAGER, VON_MISES, NEURAL_STRESS, HENCKY = 0, 1, 2, 3, 4
+TRANSFER_APIC, TRANSFER_PIC = 0, 1
 BC_NONE, BC_STICKY, BC_SLIP = 0, 1, 2
 FORCE_MLS, FORCE_GRADW = 0, 1
 
@@ -59,6 +60,7 @@ class Config:
     plate_velocity: tuple = (0.0, 0.0, 0.0)
     force_mode: int = FORCE_MLS
     deterministic: int = 0         # 1: fixed-point (bitwise reproducible) P2G on the GPU
+    transfer: int = TRANSFER_APIC  # P2G momentum transfer
     particle_volume: float = 0.0   # <=0 -> dx^3/8
     n_scenes: int = 1
     stress_scale: float = 100.0    # sigma_tau for the NSF output (reading #20)
@@ -276,8 +278,8 @@ def block_scene(name: str, grid_res: int, lo, hi, model: int, seed: int,
     """Stratified block of cells [lo,hi) on a grid_res^3 grid with optional
     seeded perturbations of v, C and F (used to exercise every branch)."""
     base = {FIXED_COROTATED: config("C1"), DRUCKER_PRAGER: config("C2"),
-            VON_MISES: config("C3")}[model]
-    cfg = Config(**{**base.as_dict(), "name": name, "grid_res": grid_res})
+            VON_MISES: config("C3"), HENCKY: config("C3")}[model]
+    cfg = Config(**{**base.as_dict(), "name": name, "grid_res": grid_res, "model": model})
     if model == VON_MISES:
         cfg.plate_y0 = hi[1] / grid_res
     for k, val in cfg_over.items():

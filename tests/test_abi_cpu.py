@@ -50,7 +50,9 @@ def test_binding_covers_header(built_lib):
 
 def test_abi_version(built_lib):
     import paper_2310_17790_b200 as nsf
-    assert nsf.nsf_mpm_abi_version() == 1
+    hdr = open(os.path.join(ROOT, "include", "nsf_mpm.h")).read()
+    ver = int(hdr.split("#define NSF_MPM_ABI_VERSION")[1].split()[0])
+    assert nsf.nsf_mpm_abi_version() == ver == 2
 
 
 def test_material_struct_layout_matches_header(built_lib, tmp_path):

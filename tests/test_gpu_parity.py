@@ -53,6 +53,14 @@ def small_scenes():
                                 keep=6000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0),
         "DP_mix": S.block_scene("DPm", 32, (8, 3, 9), (20, 16, 21), S.DRUCKER_PRAGER, 17,
                                 keep=6000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0),
+        # the appendix's StVK (elastic Hencky, model 4) and the PIC transfer
+        "HENCKY": S.block_scene("HE", 32, (9, 3, 8), (21, 13, 22), S.HENCKY, 18,
+                                keep=5000, vnoise=0.2, Fnoise=0.1, Cnoise=2.0),
+        "FC_pic": S.block_scene("FCp", 32, (9, 6, 10), (22, 17, 19), S.FIXED_COROTATED, 19,
+                                keep=5000, vnoise=0.3, Fnoise=0.02, Cnoise=3.0, transfer=S.TRANSFER_PIC),
+        "VM_pic_gradw": S.block_scene("VMpg", 32, (9, 3, 8), (21, 13, 22), S.VON_MISES, 20,
+                                      keep=4000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0, transfer=S.TRANSFER_PIC,
+                                      force_mode=S.FORCE_GRADW),
         "FC_gradw": S.block_scene("FCg", 32, (9, 6, 10), (20, 15, 19), S.FIXED_COROTATED, 14,
                                   keep=3333, vnoise=0.3, Fnoise=0.02, Cnoise=3.0,
                                   force_mode=S.FORCE_GRADW),
