@@ -179,6 +179,30 @@ nsf_status nsf_mpm_load_stress_field(nsf_mpm* h, int32_t in_dim, int32_t width,
 nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const float* dz,
                                int32_t on_device);
 
+/* Neural deformation field g(X, z) -> x (architecture P:498-500), the
+ * network that invert_latents inverts.  Same parameter layout and numerics as
+ * load_stress_field; in_dim = 3 + r, out_dim = 3, width = 128, 1 <= n_hidden
+ * <= 4.  INVALID_ARGUMENT otherwise; BAD_STATE before load_particles. */
+nsf_status nsf_mpm_load_deformation_field(nsf_mpm* h, int32_t in_dim, int32_t width,
+                                          int32_t n_hidden, int32_t out_dim,
+                                          const uint16_t* W_bf16, const float* b,
+                                          int32_t on_device);
+
+/* Network inversion (Eq. (10)): per scene s, starting from the latent
+ * the last substep used, z_s(n) = z_s + n dz_s, run n_iters Gauss-Newton
+ * iterations (1 = the first-order Taylor variant) of
+ *     min_z sum_{p in S_s} || g(X_p, z) - x_p ||^2
+ * where S_s = the scene's first n_sample points in load order and x_p their
+ * current positions.  Jacobians by forward mode on the GPU; normal equations
+ * in fp64.  The handle's latents become z_s := z_hat_s, dz_s := 0 (the next
+ * substeps use the inverted latent).  z_out (n_scenes x r, host or device per
+ * on_device, or NULL) receives z_hat.  Requires the NSF model with
+ * load_stress_field (X_ref), set_latents and load_deformation_field;
+ * 1 <= n_sample, 1 <= n_iters <= 16.  A scene whose normal matrix is not
+ * positive definite keeps its latent. */
+nsf_status nsf_mpm_invert_latents(nsf_mpm* h, int32_t n_sample, int32_t n_iters, float* z_out,
+                                  int32_t on_device);
+
 /* Enqueue n >= 0 substeps on the handle's stream (a cached CUDA graph of the
  * substep is replayed).  Asynchronous.  NSF_ERR_BAD_STATE before
  * load_particles, or for NSF without load_stress_field / set_latents. */

@@ -33,6 +33,7 @@ FIELD_SHAPES = {NSF_FIELD_X: (3,), NSF_FIELD_V: (3,), NSF_FIELD_C: (3, 3), NSF_F
 
 EXPORTS = ["nsf_mpm_abi_version", "nsf_mpm_create", "nsf_mpm_set_stream", "nsf_mpm_set_allocator",
            "nsf_mpm_load_particles", "nsf_mpm_load_stress_field", "nsf_mpm_set_latents",
+           "nsf_mpm_load_deformation_field", "nsf_mpm_invert_latents",
            "nsf_mpm_substep", "nsf_mpm_eval_stress_field", "nsf_mpm_read_state", "nsf_mpm_sync",
            "nsf_mpm_step_count", "nsf_mpm_inverted_count", "nsf_mpm_last_error", "nsf_mpm_destroy",
            "nsf_mpm_debug_bins", "nsf_mpm_debug_grid", "nsf_mpm_set_profiling",
@@ -78,6 +79,8 @@ def lib():
         "nsf_mpm_load_particles": (i32, [vp, i64, vp, vp, vp, vp, vp, i32]),
         "nsf_mpm_load_stress_field": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, i32]),
         "nsf_mpm_set_latents": (i32, [vp, i32, vp, vp, i32]),
+        "nsf_mpm_load_deformation_field": (i32, [vp, i32, i32, i32, i32, vp, vp, i32]),
+        "nsf_mpm_invert_latents": (i32, [vp, i32, i32, vp, i32]),
         "nsf_mpm_substep": (i32, [vp, i32]),
         "nsf_mpm_eval_stress_field": (i32, [vp, vp, i64, vp, vp, i32]),
         "nsf_mpm_read_state": (i32, [vp, u32, dp(vp), i32]),
@@ -217,6 +220,21 @@ def nsf_mpm_set_latents(h, r, z, dz=None):
     _check(h, lib().nsf_mpm_set_latents(h, r, pz, pd, on))
 
 
+def nsf_mpm_load_deformation_field(h, in_dim, width, n_hidden, out_dim, W_bf16, b):
+    pw, dw, kw = _ptr(W_bf16, np.uint16)
+    pb, db, kb = _ptr(b)
+    on = _same_residency(dw, db)
+    _check(h, lib().nsf_mpm_load_deformation_field(h, in_dim, width, n_hidden, out_dim, pw, pb, on))
+
+
+def nsf_mpm_invert_latents(h, n_sample: int, n_iters: int, z_out=None):
+    """Gauss-Newton network inversion (header).  z_out: None, a float32 numpy array
+    (n_scenes x r) or a CUDA tensor, filled with z_hat."""
+    po, don, ko = _ptr(z_out)
+    _check(h, lib().nsf_mpm_invert_latents(h, int(n_sample), int(n_iters), po, don or 0))
+    return z_out
+
+
 def nsf_mpm_substep(h, n: int):
     _check(h, lib().nsf_mpm_substep(h, int(n)))
 
@@ -351,6 +369,19 @@ class Simulator:
 
     def substep(self, n=1):
         nsf_mpm_substep(self.h, n)
+
+    def load_deformation_field(self, mlp):
+        dims = mlp["dims"]
+        W = np.concatenate([w.reshape(-1) for w in mlp["W_bits"]])
+        b = np.concatenate(mlp["b"])
+        nsf_mpm_load_deformation_field(self.h, dims[0], dims[1], len(dims) - 2, dims[-1], W, b)
+        self._r = dims[0] - 3
+
+    def invert_latents(self, n_sample, n_iters=3):
+        """Network inversion; returns z_hat (n_scenes x r)."""
+        out = np.empty((self.cfg.n_scenes, self._r), dtype=np.float32)
+        nsf_mpm_invert_latents(self.h, n_sample, n_iters, out)
+        return out
 
     def sync(self):
         nsf_mpm_sync(self.h)

@@ -49,4 +49,10 @@ void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X /*3 planes, pitch
                     int64_t tau_pitch, int aos_out, const NsfP2G* q = nullptr);
 // ... with q: the same kernel then runs the P2G of each point with its tau
 
+// kernels_inv.cu -- network inversion (Gauss-Newton over the deformation field)
+size_t gn_smem_bytes(const MlpDev& g);
+void launch_gn_invert(cudaStream_t st, int64_t n, const int32_t* ids, const int64_t* scene_off, int n_scenes,
+                      int n_sample, int r, const float* S, const float* z, const float* dz, const int64_t* d_step,
+                      const MlpDev& g, int n_iters, int32_t* slots, float* zw, double* accum);
+
 }  // namespace nsf

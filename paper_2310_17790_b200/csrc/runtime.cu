@@ -55,6 +55,13 @@ struct nsf_mpm {
   uint16_t* W = nullptr;
   float* b = nullptr;
   unsigned int* mlp_ctr = nullptr;   // MLP tile ticket + completion counter (kernels_nsf_tc.cu)
+  MlpDev gdef{};                      // deformation field g (network inversion)
+  uint16_t* gW = nullptr;
+  float* gb = nullptr;
+  bool gdef_loaded = false;
+  int32_t* inv_slots = nullptr;       // inversion scratch: sample slots, working latents, fp64 sums
+  float* inv_z = nullptr;
+  double* inv_acc = nullptr;
   MlpDev mlp{};
   bool mlp_loaded = false;
   float* X = nullptr;            // 3 planes, pitch
@@ -474,6 +481,68 @@ nsf_status nsf_mpm_load_stress_field(nsf_mpm* h, int32_t in_dim, int32_t width, 
   h->mlp_loaded = true;
   pipeline_on_mlp(h, &h->pb);
   invalidate_graph(h);
+  return NSF_OK;
+}
+
+nsf_status nsf_mpm_load_deformation_field(nsf_mpm* h, int32_t in_dim, int32_t width, int32_t n_hidden,
+                                          int32_t out_dim, const uint16_t* W_bf16, const float* b,
+                                          int32_t on_device) {
+  if (!h) return NSF_ERR_INVALID_ARGUMENT;
+  if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
+  if (!(in_dim >= 4 && in_dim <= 16) || width != 128 || !(n_hidden >= 1 && n_hidden <= 4) || out_dim != 3)
+    return fail(h, NSF_ERR_INVALID_ARGUMENT, "unsupported deformation field (in<=16, width=128, 1<=hidden<=4, out=3)");
+  if (!W_bf16 || !b) return fail(h, NSF_ERR_INVALID_ARGUMENT, "W and b are required");
+  if (!h->loaded) return fail(h, NSF_ERR_BAD_STATE, "load_particles first");
+  MlpDev& M = h->gdef;
+  M.in_dim = in_dim; M.width = width; M.n_hidden = n_hidden; M.out_dim = out_dim;
+  const int L = n_hidden + 1;
+  int64_t wo = 0, bo = 0;
+  for (int l = 0; l < L; ++l) {
+    const int in = l == 0 ? in_dim : width;
+    const int out = l == L - 1 ? out_dim : width;
+    M.w_off[l] = wo; M.b_off[l] = bo;
+    wo += (int64_t)in * out;
+    bo += out;
+  }
+  M.w_off[L] = wo; M.b_off[L] = bo;
+  M.ctr = nullptr;
+  if (gn_smem_bytes(M) > 227 * 1024) return fail(h, NSF_ERR_INVALID_ARGUMENT, "deformation field too large");
+  nsf_status s;
+  CK(cudaStreamSynchronize(h->stream));
+  if ((s = alloc_into(h, &h->gW, sizeof(uint16_t) * wo)) != NSF_OK) return s;
+  if ((s = alloc_into(h, &h->gb, sizeof(float) * bo)) != NSF_OK) return s;
+  if ((s = to_device(h, W_bf16, sizeof(uint16_t) * wo, on_device, h->gW)) != NSF_OK) return s;
+  if ((s = to_device(h, b, sizeof(float) * bo, on_device, h->gb)) != NSF_OK) return s;
+  CK(cudaStreamSynchronize(h->stream));
+  M.W = h->gW;
+  M.b = h->gb;
+  h->gdef_loaded = true;
+  return NSF_OK;
+}
+
+nsf_status nsf_mpm_invert_latents(nsf_mpm* h, int32_t n_sample, int32_t n_iters, float* z_out, int32_t on_device) {
+  if (!h) return NSF_ERR_INVALID_ARGUMENT;
+  if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
+  if (n_sample < 1 || n_iters < 1 || n_iters > 16) return fail(h, NSF_ERR_INVALID_ARGUMENT, "1 <= n_sample, 1 <= n_iters <= 16");
+  if (h->mat.model != NSF_NEURAL_STRESS || !h->loaded || !h->mlp_loaded || !h->latents_loaded || !h->X ||
+      !h->gdef_loaded)
+    return fail(h, NSF_ERR_BAD_STATE, "needs the NSF model with load_stress_field, set_latents, load_deformation_field");
+  if (h->gdef.in_dim != 3 + h->r) return fail(h, NSF_ERR_INVALID_ARGUMENT, "deformation field input must be 3 + r");
+  const int ns = h->mat.n_scenes, r = h->r;
+  const int nterm = r * (r + 1) / 2 + r;
+  nsf_status s;
+  if ((s = alloc_into(h, &h->inv_slots, sizeof(int32_t) * (size_t)ns * n_sample)) != NSF_OK) return s;
+  if ((s = alloc_into(h, &h->inv_z, sizeof(float) * (size_t)ns * r)) != NSF_OK) return s;
+  if ((s = alloc_into(h, &h->inv_acc, sizeof(double) * (size_t)ns * nterm)) != NSF_OK) return s;
+  launch_gn_invert(h->stream, h->n, h->ids[h->cur], h->scene_off, ns, n_sample, r, h->S[h->cur], h->z, h->dz,
+                   h->d_step, h->gdef, n_iters, h->inv_slots, h->inv_z, h->inv_acc);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h->z, h->inv_z, sizeof(float) * (size_t)ns * r, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemsetAsync(h->dz, 0, sizeof(float) * (size_t)ns * r, h->stream));
+  if (z_out)
+    CK(cudaMemcpyAsync(z_out, h->inv_z, sizeof(float) * (size_t)ns * r,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
   return NSF_OK;
 }
 
