@@ -129,9 +129,19 @@ __global__ void __launch_bounds__(inv::kRows) k_gn_accumulate(int n_scenes, int 
       } else {
         for (int q = 0; q < width; ++q) {
           const float hk = bf(hin[q * kRows + t]);
+          const uint4* wrow = reinterpret_cast<const uint4*>(W + q * width);   // 8 bf16 per load (broadcast)
 #pragma unroll
-          for (int j = 0; j < kMaxWidth; ++j)
-            if (j < width) acc[j] = fmaf(bf(W[q * width + j]), hk, acc[j]);
+          for (int j8 = 0; j8 < kMaxWidth / 8; ++j8) {
+            if (j8 * 8 < width) {
+              const uint4 wv = wrow[j8];
+              const uint32_t wa[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                acc[j8 * 8 + 2 * c] = fmaf(__uint_as_float(wa[c] << 16), hk, acc[j8 * 8 + 2 * c]);
+                acc[j8 * 8 + 2 * c + 1] = fmaf(__uint_as_float(wa[c] & 0xffff0000u), hk, acc[j8 * 8 + 2 * c + 1]);
+              }
+            }
+          }
         }
       }
       // primal: ELU and ELU'(a) for the point's tangent rows

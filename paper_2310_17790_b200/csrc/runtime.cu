@@ -62,6 +62,7 @@ struct nsf_mpm {
   int32_t* inv_slots = nullptr;       // inversion scratch: sample slots, working latents, fp64 sums
   float* inv_z = nullptr;
   double* inv_acc = nullptr;
+  size_t inv_cap[3] = {0, 0, 0};      // their capacities (bytes); grown, never shrunk
   MlpDev mlp{};
   bool mlp_loaded = false;
   float* X = nullptr;            // 3 planes, pitch
@@ -531,9 +532,11 @@ nsf_status nsf_mpm_invert_latents(nsf_mpm* h, int32_t n_sample, int32_t n_iters,
   const int ns = h->mat.n_scenes, r = h->r;
   const int nterm = r * (r + 1) / 2 + r;
   nsf_status s;
-  if ((s = alloc_into(h, &h->inv_slots, sizeof(int32_t) * (size_t)ns * n_sample)) != NSF_OK) return s;
-  if ((s = alloc_into(h, &h->inv_z, sizeof(float) * (size_t)ns * r)) != NSF_OK) return s;
-  if ((s = alloc_into(h, &h->inv_acc, sizeof(double) * (size_t)ns * nterm)) != NSF_OK) return s;
+  const size_t need[3] = {sizeof(int32_t) * (size_t)ns * n_sample, sizeof(float) * (size_t)ns * r,
+                          sizeof(double) * (size_t)ns * nterm};
+  if (need[0] > h->inv_cap[0]) { if ((s = alloc_into(h, &h->inv_slots, need[0])) != NSF_OK) return s; h->inv_cap[0] = need[0]; }
+  if (need[1] > h->inv_cap[1]) { if ((s = alloc_into(h, &h->inv_z, need[1])) != NSF_OK) return s; h->inv_cap[1] = need[1]; }
+  if (need[2] > h->inv_cap[2]) { if ((s = alloc_into(h, &h->inv_acc, need[2])) != NSF_OK) return s; h->inv_cap[2] = need[2]; }
   launch_gn_invert(h->stream, h->n, h->ids[h->cur], h->scene_off, ns, n_sample, r, h->S[h->cur], h->z, h->dz,
                    h->d_step, h->gdef, n_iters, h->inv_slots, h->inv_z, h->inv_acc);
   CK(cudaGetLastError());

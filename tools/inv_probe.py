@@ -63,3 +63,25 @@ def after_substeps():
         z_start = sc.z0.astype(np.float64) + k * sc.dz.astype(np.float64)
         zo = invert_scenes(sc.X_ref, x, sc.scene_offsets, 64, z_start, gnet, 1, "emulate")
         print(k, np.linalg.norm(zg - zo) / np.linalg.norm(zo - z_start), np.linalg.norm(zo - z_start))
+
+
+def timing():
+    import torch
+    import paper_2310_17790_b200 as nsf
+    sc = __import__("scenes").c5()
+    gnet = deformation_net(77)
+    sim = nsf.Simulator(sc.cfg)
+    sim.load_scene(sc)
+    sim.load_deformation_field(gnet)
+    sim.substep(3)
+    sim.sync()
+    for iters in (1, 3):
+        sim.invert_latents(64, iters)
+        torch.cuda.synchronize()
+        import time
+        t0 = time.perf_counter()
+        for _ in range(10):
+            sim.invert_latents(64, iters)
+        torch.cuda.synchronize()
+        print(f"C5 inversion 256 scenes x 64 samples, {iters} GN iters: {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms (host-timed, incl. sync)")
+    sim.close()
