@@ -51,6 +51,9 @@ void launch_nsf_mlp(cudaStream_t st, int64_t n, const float* X /*3 planes, pitch
 
 // kernels_inv.cu -- network inversion (Gauss-Newton over the deformation field)
 size_t gn_smem_bytes(const MlpDev& g);
+bool gn_tc_supported(const MlpDev& g, int r);
+void launch_gn_tc(cudaStream_t st, int n_scenes, int n_sample, int r, const int32_t* slots, const float* S,
+                  const float* zw, const MlpDev& g, double* accum);
 void launch_gn_invert(cudaStream_t st, int64_t n, const int32_t* ids, const int64_t* scene_off, int n_scenes,
                       int n_sample, int r, const float* S, const float* z, const float* dz, const int64_t* d_step,
                       const MlpDev& g, int n_iters, int32_t* slots, float* zw, double* accum);

@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "kernels.h"
 #include "params.cuh"
 
@@ -268,8 +269,15 @@ void launch_gn_invert(cudaStream_t st, int64_t n, const int32_t* ids, const int6
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = ((int64_t)n_scenes * n_sample + (inv::kRows / rp) - 1) / (inv::kRows / rp);
   const int grid = (int)(tiles < sms ? tiles : sms);
+  static int force_simt = -1;
+  if (force_simt < 0) {
+    const char* e = getenv("NSF_GN_SIMT");
+    force_simt = (e && e[0] != '0') ? 1 : 0;
+  }
+  const bool tc = !force_simt && gn_tc_supported(g, r);
   for (int it = 0; it < n_iters; ++it) {
-    k_gn_accumulate<<<grid > 0 ? grid : 1, inv::kRows, smem, st>>>(n_scenes, n_sample, r, rp, slots, S, zw, g, accum);
+    if (tc) launch_gn_tc(st, n_scenes, n_sample, r, slots, S, zw, g, accum);
+    else k_gn_accumulate<<<grid > 0 ? grid : 1, inv::kRows, smem, st>>>(n_scenes, n_sample, r, rp, slots, S, zw, g, accum);
     k_gn_solve<<<(n_scenes + 127) / 128, 128, 0, st>>>(n_scenes, r, accum, zw);
   }
 }

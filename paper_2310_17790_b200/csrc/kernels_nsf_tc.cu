@@ -445,6 +445,272 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   }
 }
 
+// ---------------------------------------------------------------------------
+// Network inversion pass on the tensor cores (kernels_inv.cu has the CUDA-core
+// version and the Gauss-Newton solve): per tile of 128 rows = 16 points x 8
+// rows (primal, r <= 7 tangents of z, padding), the deformation field g and its
+// forward-mode tangents go through the same MMAs as the stress field: layer 1
+// tf32 on [hi | lo] inputs (primal: (X, z, 1, 1) -> bias by the MMA; tangent k:
+// e_{3+k}, no bias), hidden layers bf16, output N = 16 (3 used).  Hidden
+// epilogues in two phases: primal rows apply bias + ELU and publish ELU'(a)
+// (fp32, shared memory); after a stream barrier the tangent rows scale their
+// pre-activations by it (no bias).  Tangents are rounded to bf16 like
+// activations.  Per point, J^T J and J^T (g - x) go into fp64 per-scene sums.
+namespace gn {
+constexpr int kS = 2;              // streams (128 rows each)
+constexpr int kRP = 8;             // rows per point
+constexpr int kPts = kM / kRP;     // 16 points per tile
+struct __align__(1024) GnSmem {
+  uint8_t wB[kMaxHiddenMMA][kTileBytes];
+  uint8_t wOut[kOutBBytes];
+  uint8_t a[kS][kTileBytes];
+  uint8_t w1t[kW * 128];
+  float bias[kMaxHiddenMMA + 1][kW];
+  float bout[kOutN];
+  float dbuf[kS][kPts][kW];        // ELU'(a) of each point's primal row
+  float outb[kS][kM][4];
+  unsigned long long bar[kS];
+  uint32_t tmem_base;
+};
+}  // namespace gn
+
+__global__ void __launch_bounds__(gn::kS * 128, 1)
+k_gn_tc(int n_scenes, int n_sample, int r, const int32_t* __restrict__ slots, const float* __restrict__ S,
+        const float* __restrict__ zw, MlpDev g, double* __restrict__ accum) {
+  using namespace gn;
+  extern __shared__ uint8_t smem_raw[];
+  GnSmem& sm = *reinterpret_cast<GnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x;
+  const int s = tid >> 7;
+  const int t = tid & 127;
+  const int warp = tid >> 5;
+  const int L = g.n_hidden + 1;
+  const int n_mma_hidden = g.n_hidden - 1;
+  const int in_dim = g.in_dim;
+  // ---- weights (same layout as the stress-field kernel) ----
+  for (int l = 0; l < n_mma_hidden; ++l) {
+    const uint16_t* W = g.W + g.w_off[l + 1];
+    for (int c = tid; c < kW * (kW / 8); c += kS * 128) {
+      const int nrow = c >> 4, kc = c & 15;
+      cp_async16(smem_u32(sm.wB[l] + sw128_offset(nrow, kc * 8, kW)), W + nrow * kW + kc * 8, 16);
+    }
+  }
+  {
+    const uint16_t* W = g.W + g.w_off[L - 1];
+    for (int c = tid; c < kOutN * (kW / 8); c += kS * 128) {
+      const int nrow = c >> 4, kc = c & 15;
+      const bool in = nrow < g.out_dim;
+      cp_async16(smem_u32(sm.wOut + sw128_offset(nrow, kc * 8, kOutN)), in ? W + nrow * kW + kc * 8 : W, in ? 16 : 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int e = tid; e < kW * 32; e += kS * 128) {
+    const int j = e >> 5, k = e & 31, i = k & 15;
+    const float bj = g.b[g.b_off[0] + j];
+    const float b_hi = __uint_as_float(to_tf32(bj));
+    float w = 0.0f;
+    if (i < in_dim) w = __uint_as_float(((uint32_t)g.W[g.w_off[0] + j * in_dim + i]) << 16);
+    else if (i == in_dim) w = b_hi;
+    else if (i == in_dim + 1) w = __uint_as_float(to_tf32(bj - b_hi));
+    *reinterpret_cast<float*>(sm.w1t + j * 128 + ((((k >> 2) ^ (j & 7))) << 4) + (k & 3) * 4) = w;
+  }
+  for (int e = tid; e < (kMaxHiddenMMA + 1) * kW; e += kS * 128) {
+    const int l = e / kW, j = e % kW;
+    sm.bias[l][j] = l < g.n_hidden ? g.b[g.b_off[l] + j] : 0.0f;
+  }
+  if (tid < kOutN) sm.bout[tid] = tid < g.out_dim ? g.b[g.b_off[L - 1] + tid] : 0.0f;
+  if (tid == 0) {
+    for (int k = 0; k < kS; ++k) mbar_init(&sm.bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t d_col = tmem + (uint32_t)(kTmemStride * s);
+  const uint32_t o_col = d_col + 128u;
+  const uint32_t lane_sel = ((uint32_t)(32 * (warp & 3))) << 16;
+  const uint32_t a_saddr = smem_u32(sm.a[s]);
+  const uint32_t w1_saddr = smem_u32(sm.w1t);
+  const uint32_t bias_saddr = smem_u32(&sm.bias[0][0]);
+  constexpr uint32_t kIdesc1 = make_idesc(kM, kW, 2u);
+  constexpr uint32_t kIdescH = make_idesc(kM, kW);
+  constexpr uint32_t kIdescO = make_idesc(kM, kOutN);
+  uint32_t phase = 0;
+  const int point = t / kRP, kk = t % kRP;
+  const bool primal = kk == 0, tangent = kk >= 1 && kk <= r;
+  const int64_t n_pts = (int64_t)n_scenes * n_sample;
+  const int64_t n_tiles = (n_pts + kPts - 1) / kPts;
+  const int nterm = r * (r + 1) / 2 + r;
+  for (int64_t tile = (int64_t)blockIdx.x * kS + s; tile < n_tiles; tile += (int64_t)gridDim.x * kS) {
+    const int64_t e = tile * kPts + point;
+    const int scene = e < n_pts ? (int)(e / n_sample) : 0;
+    const int slot = e < n_pts ? slots[e] : -1;
+    const bool live = slot >= 0;
+    // ---- layer-1 A row: [hi(u) | lo(u)] ----
+    float u[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) u[i] = 0.0f;
+    float xt[3] = {0.f, 0.f, 0.f};
+    if (live && primal) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        u[a] = S[pbase(slot) + (PXR + a) * 32];
+        xt[a] = S[pbase(slot) + (PX + a) * 32];
+      }
+      for (int q = 0; q < r; ++q) u[3 + q] = zw[scene * r + q];
+      u[in_dim] = 1.0f;        // bias columns of the layer-1 B operand
+      u[in_dim + 1] = 1.0f;
+    } else if (live && tangent) {
+      u[3 + (kk - 1)] = 1.0f;
+    }
+    {
+      const uint32_t row = a_saddr + (uint32_t)t * 128u;
+      const uint32_t sw = (uint32_t)(t & 7);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 hi, lo;
+        uint32_t* ph = &hi.x;
+        uint32_t* pl = &lo.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float x = u[4 * c + q];
+          const uint32_t xh = to_tf32(x);
+          ph[q] = xh;
+          pl[q] = to_tf32(x - __uint_as_float(xh));
+        }
+        sts_u4(row + (((uint32_t)c ^ sw) << 4), hi);
+        sts_u4(row + (((uint32_t)(c + 4) ^ sw) << 4), lo);
+      }
+    }
+    fence_async_smem();
+    stream_barrier(s);
+    for (int layer = 0; layer <= n_mma_hidden; ++layer) {   // layer 0: tf32 layer 1; then the hidden MMAs
+      if (t == 0) {
+        fence_after();
+        if (layer == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            mma_tf32(d_col, make_desc(a_saddr + q * 32), make_desc(w1_saddr + q * 32), kIdesc1, q > 0 ? 1u : 0u);
+        } else {
+          const uint32_t b_saddr = smem_u32(sm.wB[layer - 1]);
+#pragma unroll
+          for (int q = 0; q < kW / 16; ++q) {
+            const uint32_t koff = (uint32_t)((q >> 2) * (kM * 128) + (q & 3) * 32);
+            const uint32_t kofb = (uint32_t)((q >> 2) * (kW * 128) + (q & 3) * 32);
+            mma_bf16(d_col, make_desc(a_saddr + koff), make_desc(b_saddr + kofb), kIdescH, q > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit(&sm.bar[s]);
+      }
+      mbar_wait(&sm.bar[s], phase);
+      phase ^= 1;
+      fence_after();
+      // per 32-column chunk (tcgen05.ld is warp-collective: every row loads its
+      // chunk): primal rows add the bias (layers >= 2; layer 1's came from the
+      // MMA), publish ELU'(a) and store ELU(a); then tangent rows store
+      // ELU'(a) * (W t_prev); padding rows store zeros
+#pragma unroll 1
+      for (int c0 = 0; c0 < kW; c0 += 32) {
+        float h[32];
+        tmem_ld32(d_col + lane_sel + c0, h);
+        if (primal) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float a = h[q] + (layer > 0 ? sm.bias[layer][c0 + q] : 0.0f);
+            sm.dbuf[s][point][c0 + q] = a > 0.0f ? 1.0f : __expf(a);
+            h[q] = elu(a);
+          }
+          store_act32(a_saddr, t, c0, h);
+        }
+        stream_barrier(s);
+        if (!primal) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) h[q] = tangent ? sm.dbuf[s][point][c0 + q] * h[q] : 0.0f;
+          store_act32(a_saddr, t, c0, h);
+        }
+      }
+      fence_before();
+      fence_async_smem();
+      stream_barrier(s);
+    }
+    // ---- output layer (N = 16, 3 used): primal -> g, tangent k -> dg/dz_k ----
+    if (t == 0) {
+      fence_after();
+      const uint32_t b_saddr = smem_u32(sm.wOut);
+#pragma unroll
+      for (int q = 0; q < kW / 16; ++q) {
+        const uint32_t koff = (uint32_t)((q >> 2) * (kM * 128) + (q & 3) * 32);
+        const uint32_t kofb = (uint32_t)((q >> 2) * (kOutN * 128) + (q & 3) * 32);
+        mma_bf16(o_col, make_desc(a_saddr + koff), make_desc(b_saddr + kofb), kIdescO, q > 0 ? 1u : 0u);
+      }
+      mma_commit(&sm.bar[s]);
+    }
+    mbar_wait(&sm.bar[s], phase);
+    phase ^= 1;
+    fence_after();
+    {
+      float y[8];
+      tmem_ld8(o_col + lane_sel, y);
+#pragma unroll
+      for (int o = 0; o < 3; ++o) sm.outb[s][t][o] = y[o] + (primal ? sm.bout[o] : 0.0f);
+    }
+    fence_before();
+    stream_barrier(s);
+    if (primal && live) {
+      double res[3], J[3][8];
+#pragma unroll
+      for (int o = 0; o < 3; ++o) res[o] = (double)sm.outb[s][t][o] - (double)xt[o];
+      for (int q = 0; q < r; ++q)
+#pragma unroll
+        for (int o = 0; o < 3; ++o) J[o][q] = (double)sm.outb[s][t + 1 + q][o];
+      double* A = accum + (int64_t)scene * nterm;
+      int idx = 0;
+      for (int a = 0; a < r; ++a)
+        for (int c = a; c < r; ++c, ++idx)
+          atomicAdd(A + idx, J[0][a] * J[0][c] + J[1][a] * J[1][c] + J[2][a] * J[2][c]);
+      for (int a = 0; a < r; ++a) atomicAdd(A + idx + a, J[0][a] * res[0] + J[1][a] * res[1] + J[2][a] * res[2]);
+    }
+    stream_barrier(s);   // outb, the A tile and the accumulators are free for the next tile
+  }
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+bool gn_tc_supported(const MlpDev& g, int r) {
+  return g.width == kW && g.n_hidden >= 2 && g.n_hidden - 1 <= kMaxHiddenMMA && g.in_dim <= 14 && g.out_dim == 3 &&
+         r >= 1 && r + 1 <= gn::kRP;
+}
+
+void launch_gn_tc(cudaStream_t st, int n_scenes, int n_sample, int r, const int32_t* slots, const float* S,
+                  const float* zw, const MlpDev& g, double* accum) {
+  static int n_sms = 0;
+  static bool attr = false;
+  const size_t smem = sizeof(gn::GnSmem) + 1024;
+  if (!attr) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_gn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int64_t tiles = ((int64_t)n_scenes * n_sample + gn::kPts - 1) / gn::kPts;
+  int64_t grid = (tiles + gn::kS - 1) / gn::kS;
+  if (grid > n_sms) grid = n_sms;
+  if (grid < 1) grid = 1;
+  k_gn_tc<<<(unsigned)grid, gn::kS * 128, smem, st>>>(n_scenes, n_sample, r, slots, S, zw, g, accum);
+}
+
 bool nsf_mlp_tc_supported(const MlpDev& mlp) {
   return mlp.width == kW && mlp.n_hidden >= 2 && mlp.n_hidden - 1 <= kMaxHiddenMMA && mlp.in_dim <= 14 &&
          mlp.out_dim <= 8;

@@ -85,3 +85,16 @@ def timing():
         torch.cuda.synchronize()
         print(f"C5 inversion 256 scenes x 64 samples, {iters} GN iters: {(time.perf_counter() - t0) / 10 * 1e3:.3f} ms (host-timed, incl. sync)")
     sim.close()
+
+
+def conditioning(n_sample=256):
+    import paper_2310_17790_b200 as nsf
+    from oracle.inversion import invert_scenes
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+    from tests.test_gpu_inversion import _scene, _invert
+    sc, gnet, _ = _scene()
+    zg, x = _invert(nsf, sc, gnet, n_sample, 1)
+    zo = invert_scenes(sc.X_ref, x, sc.scene_offsets, n_sample, sc.z0.astype(np.float64), gnet, 1, "emulate")
+    ze = invert_scenes(sc.X_ref, x, sc.scene_offsets, n_sample, sc.z0.astype(np.float64), gnet, 1, "exact")
+    print(n_sample, "gpu-oracle", np.linalg.norm(zg - zo) / np.linalg.norm(zo - sc.z0),
+          "emulate-exact", np.linalg.norm(ze - zo) / np.linalg.norm(zo - sc.z0))
