@@ -339,6 +339,35 @@ def run_ours(args):
                     "peak_source": peak_src}
     step_gbs = B_ALG_PER_PARTICLE_SUBSTEP * n / (ms / args.steps * 1e-3) / 1e9
 
+    # ---- C5: network inversion (Eq. (10)), 3 Gauss-Newton iterations over 64 samples per scene ----
+    inversion = None
+    if args.config == "C5":
+        import scenes as _sc
+        g = _sc.deformation_field()
+        sim.load_deformation_field(g)
+        sim.invert_latents(64, 3)
+        sim.sync()
+        ia = torch.cuda.Event(enable_timing=True)
+        ib = torch.cuda.Event(enable_timing=True)
+        reps = 5
+        ia.record(stream)
+        for _ in range(reps):
+            sim.invert_latents(64, 3)
+        ib.record(stream)
+        ib.synchronize()
+        inv_ms = ia.elapsed_time(ib) / reps
+        dims = g["dims"]
+        row_flop = 2.0 * sum(a_ * b_ for a_, b_ in zip(dims[:-1], dims[1:]))
+        flop_iter = row_flop * (1 + (dims[0] - 3)) * sc.cfg.n_scenes * 64
+        pk_t = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops_sustained", 1351.3)) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1351.3
+        inversion = {"n_sample_per_scene": 64, "gauss_newton_iters": 3, "ms": inv_ms,
+                     "flop_per_iter": flop_iter, "achieved_tflops": flop_iter * 3 / (inv_ms * 1e-3) / 1e12,
+                     "frac_of_bf16_sustained": flop_iter * 3 / (inv_ms * 1e-3) / 1e12 / pk_t,
+                     "note": "per call: sample collection, 3 x (tensor-core forward + 6 tangents, fp64 normal "
+                             "equations, per-scene Cholesky), latent update; host-synchronous API call"}
+        nsf.nsf_mpm_set_latents(sim.h, dims[0] - 3, sc.z0, sc.dz)   # back to the scene's latents
+
     # ---- end to end through the public API with host buffers ----
     pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(sc, k))).pin_memory() for k in ("x", "v", "C", "F")}
     out_x = torch.empty((n, 3), dtype=torch.float32).pin_memory()
@@ -396,6 +425,8 @@ def run_ours(args):
             "launches_per_substep": launches / max(args.steps, 1),
             "cpu_baseline": cpu,
         }
+        if inversion is not None:
+            line["inversion"] = inversion
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

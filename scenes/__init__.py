@@ -269,6 +269,19 @@ def c5(seed: int = SEEDS["C5"], n_scenes: int = 256, per_scene: int = 2048,
     return sc
 
 
+def deformation_field(seed: int = SEEDS["C5"] + 1000, r: int = 6, width: int = 128, n_hidden: int = 4) -> dict:
+    """Random-init neural deformation field g(X, z) -> x,
+    reading #20's initialisation, with the output layer scaled by 1/16 (exact in bf16)
+    and its bias set to 0.5 so that g stays inside the unit domain: a stand-in for the
+    trained network the network inversion (Eq. (10)) runs on."""
+    g = xavier_bf16_mlp(np.random.default_rng(seed), [3 + r] + [width] * n_hidden + [3])
+    w = (g["W"][-1] / np.float32(16.0)).astype(np.float32)
+    g["W"][-1] = w
+    g["W_bits"][-1] = (w.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+    g["b"][-1] = np.full(3, 0.5, np.float32)
+    return g
+
+
 # ---------------------------------------------------------------------------
 # small parity variants (several tiles + ragged tails, oracle-friendly sizes)
 

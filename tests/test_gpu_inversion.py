@@ -15,8 +15,10 @@ import pytest
 import scenes
 from oracle.inversion import g_with_tangents, invert_scenes
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tools"))
-from inv_probe import deformation_net  # noqa: E402
+
+
+def deformation_net(seed):
+    return scenes.deformation_field(seed)
 
 pytestmark = pytest.mark.gpu
 

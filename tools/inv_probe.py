@@ -7,15 +7,8 @@ import numpy as np  # noqa: E402
 
 
 def deformation_net(seed):
-    """Random-init g with a small output layer (x 1/16, exact in bf16) and bias 0.5, so
-    g(X, z) stays inside the unit domain."""
     import scenes
-    g = scenes.xavier_bf16_mlp(np.random.default_rng(seed), [9, 128, 128, 128, 128, 3])
-    w = g["W"][-1] / np.float32(16.0)
-    g["W"][-1] = w.astype(np.float32)
-    g["W_bits"][-1] = (w.astype(np.float32).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
-    g["b"][-1] = np.full(3, 0.5, np.float32)
-    return g
+    return scenes.deformation_field(seed)
 
 
 def main():
