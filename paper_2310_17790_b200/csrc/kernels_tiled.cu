@@ -279,15 +279,16 @@ __device__ __forceinline__ void p2g_accumulate(const float* sl, int my_cell, int
 #pragma unroll
     for (int oy = 0; oy < 3; ++oy) {
       const float wxy = wx * wyv[oy];
-      const float uyx = fmaf((float)oy, q1x, ux), uyy = fmaf((float)oy, q1y, uy), uyz = fmaf((float)oy, q1z, uz);
+      const float uyx = oy ? fmaf((float)oy, q1x, ux) : ux, uyy = oy ? fmaf((float)oy, q1y, uy) : uy,
+                  uyz = oy ? fmaf((float)oy, q1z, uz) : uz;   // fmaf(0, q, u) is not folded
 #pragma unroll
       for (int oz = 0; oz < 3; ++oz) {
         const float W = wxy * wzv[oz];
         const int k = oy * 3 + oz;
         accm[k] += W;
-        accp[k][0] = fmaf(W, fmaf((float)oz, q2x, uyx), accp[k][0]);
-        accp[k][1] = fmaf(W, fmaf((float)oz, q2y, uyy), accp[k][1]);
-        accp[k][2] = fmaf(W, fmaf((float)oz, q2z, uyz), accp[k][2]);
+        accp[k][0] = fmaf(W, oz ? fmaf((float)oz, q2x, uyx) : uyx, accp[k][0]);
+        accp[k][1] = fmaf(W, oz ? fmaf((float)oz, q2y, uyy) : uyy, accp[k][1]);
+        accp[k][2] = fmaf(W, oz ? fmaf((float)oz, q2z, uyz) : uyz, accp[k][2]);
       }
     }
   }
@@ -378,15 +379,16 @@ k_p2g_tiled(const float* __restrict__ S, int64_t pitch, const int32_t* __restric
 #pragma unroll
           for (int oy = 0; oy < 3; ++oy) {
             const float wxy = wx * wyv[oy];
-            const float uyx = fmaf((float)oy, q1x, ux), uyy = fmaf((float)oy, q1y, uy), uyz = fmaf((float)oy, q1z, uz);
+            const float uyx = oy ? fmaf((float)oy, q1x, ux) : ux, uyy = oy ? fmaf((float)oy, q1y, uy) : uy,
+                  uyz = oy ? fmaf((float)oy, q1z, uz) : uz;   // fmaf(0, q, u) is not folded
 #pragma unroll
             for (int oz = 0; oz < 3; ++oz) {
               const float W = wxy * wzv[oz];
               const int k = oy * 3 + oz;
               accm[k] += W;
-              accp[k][0] = fmaf(W, fmaf((float)oz, q2x, uyx), accp[k][0]);
-              accp[k][1] = fmaf(W, fmaf((float)oz, q2y, uyy), accp[k][1]);
-              accp[k][2] = fmaf(W, fmaf((float)oz, q2z, uyz), accp[k][2]);
+              accp[k][0] = fmaf(W, oz ? fmaf((float)oz, q2x, uyx) : uyx, accp[k][0]);
+              accp[k][1] = fmaf(W, oz ? fmaf((float)oz, q2y, uyy) : uyy, accp[k][1]);
+              accp[k][2] = fmaf(W, oz ? fmaf((float)oz, q2z, uyz) : uyz, accp[k][2]);
             }
           }
         }
@@ -911,15 +913,16 @@ __device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, i
 #pragma unroll
     for (int oy = 0; oy < 3; ++oy) {
       const float wxy = wx * wyv[oy];
-      const float uyx = fmaf((float)oy, q1x, ux), uyy = fmaf((float)oy, q1y, uy), uyz = fmaf((float)oy, q1z, uz);
+      const float uyx = oy ? fmaf((float)oy, q1x, ux) : ux, uyy = oy ? fmaf((float)oy, q1y, uy) : uy,
+                  uyz = oy ? fmaf((float)oy, q1z, uz) : uz;   // fmaf(0, q, u) is not folded
 #pragma unroll
       for (int oz = 0; oz < 3; ++oz) {
         const float W = wxy * wzv[oz];
         const int k = oy * 3 + oz;
         accm[k] += W;
-        accp[k][0] = fmaf(W, fmaf((float)oz, q2x, uyx), accp[k][0]);
-        accp[k][1] = fmaf(W, fmaf((float)oz, q2y, uyy), accp[k][1]);
-        accp[k][2] = fmaf(W, fmaf((float)oz, q2z, uyz), accp[k][2]);
+        accp[k][0] = fmaf(W, oz ? fmaf((float)oz, q2x, uyx) : uyx, accp[k][0]);
+        accp[k][1] = fmaf(W, oz ? fmaf((float)oz, q2y, uyy) : uyy, accp[k][1]);
+        accp[k][2] = fmaf(W, oz ? fmaf((float)oz, q2z, uyz) : uyz, accp[k][2]);
       }
     }
   }
