@@ -91,7 +91,7 @@ __device__ __forceinline__ unsigned long long packed(int c) {
 __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* counts, int32_t* block_start,
                                                        int32_t* cursor, int32_t* nonempty, int32_t* n_nonempty,
                                                        unsigned long long* status, unsigned long long* ticket,
-                                                       int64_t n_tiles) {
+                                                       int64_t n_tiles, int32_t* ne_of, int4* cellcnt) {
   __shared__ unsigned long long warp_sums[kScanThreads / 32];
   __shared__ unsigned long long s_prefix;
   __shared__ unsigned long long s_ticket;
@@ -170,7 +170,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* c
       const int start = (int)(r & 0xffffffffull);
       block_start[i] = start;
       cursor[i] = start;
-      if (c[k] > 0) nonempty[(int)((r >> 32) & 0x3ffffffull)] = (int)i;
+      if (c[k] > 0) {
+        const int e = (int)((r >> 32) & 0x3ffffffull);
+        nonempty[e] = (int)i;
+        if (cellcnt) {   // cell-ordered re-binning: block -> list index, zeroed cell counters
+          ne_of[i] = e;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) cellcnt[16 * (int64_t)e + q] = make_int4(0, 0, 0, 0);
+        }
+      }
       counts[i] = 0;
     }
   }
@@ -184,7 +192,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* c
 void launch_scan(cudaStream_t st, PipelineBuffers* pb) {
   k_scan<<<(unsigned)pb->scan_tiles, kScanThreads, 0, st>>>(pb->total_blocks, pb->counts, pb->block_start,
                                                              pb->cursor, pb->nonempty, pb->n_nonempty,
-                                                             pb->scan_status, pb->scan_ticket, pb->scan_tiles);
+                                                             pb->scan_status, pb->scan_ticket, pb->scan_tiles,
+                                                             pb->ne_of, reinterpret_cast<int4*>(pb->cellcnt));
 }
 
 int64_t scan_tiles_for(int64_t total_blocks) { return (total_blocks + kScanTile - 1) / kScanTile; }
@@ -239,6 +248,88 @@ __global__ void k_aos_to_planes(int64_t n, const float* __restrict__ aos, int nc
 void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch) {
   if (n == 0) return;
   k_aos_to_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, aos, ncomp, planes, pitch);
+}
+
+// ---------------------------------------------------------------------------
+// Cell-ordered re-binning (storage sorted by block, and by cell inside each
+// block), as three flat passes over the particles in their current order:
+//   k_cell_rank : rank[j] = arrival rank of j among its cell's particles
+//                 (counters cellcnt[64 e + cell], e = the block's list index)
+//   k_cell_scan : one warp per non-empty block: counts -> absolute cell starts
+//   k_copy_cells: out[cellcnt[64 e + cell] + rank[j]] = in[j]  (30 planes + id)
+// Reads are sequential; the writes of a warp land in runs (one per cell).  The
+// order inside a cell is not specified.
+__device__ __forceinline__ int cell_of_x(float x0, float x1, float x2, const DevParams& P) {
+  const float xs[3] = {x0, x1, x2};
+  int c = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    int base = (int)floorf(xs[a] * P.inv_dx - 0.5f);   // as block_key_of
+    base = min(max(base, 0), P.N[a] - 3);
+    c = (c << 2) | (base & 3);
+  }
+  return c;
+}
+
+__global__ void k_cell_rank(int64_t n, const float* __restrict__ S, const int32_t* __restrict__ keys,
+                            const int32_t* __restrict__ ne_of, int32_t* cellcnt, int32_t* __restrict__ rank,
+                            DevParams P) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const unsigned active = __ballot_sync(0xffffffffu, j < n);
+  if (j >= n) return;
+  const float* b = S + pbase(j);
+  const int cell = cell_of_x(b[(PX + 0) * 32], b[(PX + 1) * 32], b[(PX + 2) * 32], P);
+  const int slot = 64 * ne_of[keys[j]] + cell;
+  rank[j] = aggregated_increment(cellcnt, slot, active);
+}
+
+__global__ void k_cell_scan(int32_t* cellcnt, const int32_t* __restrict__ nonempty,
+                            const int32_t* __restrict__ n_nonempty, const int32_t* __restrict__ block_start) {
+  const int lane = threadIdx.x & 31;
+  const int nblk = *n_nonempty;
+  for (int e = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e < nblk;
+       e += (int)((gridDim.x * (int64_t)blockDim.x) >> 5)) {
+    int2* c2 = reinterpret_cast<int2*>(cellcnt + 64 * (int64_t)e);
+    const int2 v = c2[lane];
+    int incl = v.x + v.y;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int s = block_start[nonempty[e]] + incl - v.x - v.y;
+    c2[lane] = make_int2(s, s + v.x);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_copy_cells(int64_t n, const float* __restrict__ Sin, float* __restrict__ Sout,
+                                                    const int32_t* __restrict__ ids_in, int32_t* __restrict__ ids_out,
+                                                    const int32_t* __restrict__ keys, const int32_t* __restrict__ ne_of,
+                                                    const int32_t* __restrict__ cellcnt,
+                                                    const int32_t* __restrict__ rank, DevParams P) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const float* sp = Sin + pbase(j);
+  float v[kPlanes];
+#pragma unroll
+  for (int k = 0; k < kPlanes; ++k) v[k] = __ldcs(sp + k * 32);   // read once: streaming
+  const int id = __ldcs(ids_in + j);
+  const int cell = cell_of_x(v[PX + 0], v[PX + 1], v[PX + 2], P);
+  const int64_t dst = cellcnt[64 * ne_of[keys[j]] + cell] + rank[j];
+  float* dp = Sout + pbase(dst);
+#pragma unroll
+  for (int k = 0; k < kPlanes; ++k) dp[k * 32] = v[k];
+  ids_out[dst] = id;
+}
+
+void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
+                               int32_t* ids_out, PipelineBuffers* pb, const DevParams& P) {
+  if (n == 0) return;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  k_cell_rank<<<g, 256, 0, st>>>(n, Sin, pb->keys, pb->ne_of, pb->cellcnt, pb->perm, P);
+  k_cell_scan<<<num_sms() * 4, 256, 0, st>>>(pb->cellcnt, pb->nonempty, pb->n_nonempty, pb->block_start);
+  k_copy_cells<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, Sin, Sout, ids_in, ids_out, pb->keys, pb->ne_of,
+                                                            pb->cellcnt, pb->perm, P);
 }
 
 }  // namespace nsf

@@ -704,7 +704,7 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
 
 // ---------------------------------------------------------------------------
 static int g_num_sms = 0;
-static int num_sms() {
+int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -795,6 +795,17 @@ constexpr int kRowsF = NSF_DENSE_ROWS;         // dense variant: staged rows per
 #define NSF_WARP_SCATTER 1                     // direct scatters are done warp-cooperatively
 #endif   // staged rows per cell in the fused kernel
 
+// Particles whose new cell lies outside the segment's block (or beyond the
+// staged rows of their cell) are listed in shared memory during phase 1 and
+// scattered node-parallel in phase 2, by the warps that do not accumulate (NT >
+// 192) or by all threads before accumulating; only list overflow is scattered
+// inline (warp-cooperatively), which stalls its warp on the block-flag loads.
+#ifndef NSF_SCATTER_CAP
+#define NSF_SCATTER_CAP 40
+#endif
+constexpr int kScatterCap = NSF_SCATTER_CAP;
+constexpr int kScatterEntry = kSlotFields + 1;   // 21 staged values, packed stencil base
+
 constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-1, 4b+7)
 // padded strides of the tile (in float4): a warp's lanes differ mostly within one
 // 4-cell block, so with 8-float4 rows the 16-byte bank group (index mod 8) would
@@ -812,6 +823,8 @@ struct __align__(16) FusedSmemT {
   } u;
   int pop[64];
   int next;
+  int nsc;                                     // entries of sc this segment
+  float sc[kScatterCap * kScatterEntry];       // out-of-block particles: staged values + packed base
   __align__(16) uint16_t tbl[1728];
   __align__(16) uint16_t tbl_off[224];
 };
@@ -1004,6 +1017,33 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
   }
 }
 
+// Phase-2 scatter of the listed particles: work item i = (entry i / 35; its
+// stencil node i % 35 < 27, else one of its 8 corner blocks to mark touched).
+// Node (a, b, c) gets m W, W (u0 + a q0 + b q1 + c q2) as in p2g_accumulate_f.
+template <int ROWS>
+__device__ __forceinline__ void scatter_listed(const float* sc, int nsc, int i0, int stride, float4* gacc, int* flags,
+                                               int* list, int* list_count, int64_t scene_block0, const DevParams& P) {
+  for (int i = i0; i < nsc * 35; i += stride) {
+    const int e = i / 35, q = i - 35 * e;
+    const float* s = sc + e * kScatterEntry;
+    const int pb = __float_as_int(s[kSlotFields]);
+    const int bx = pb >> 20, by = (pb >> 10) & 1023, bz = pb & 1023;
+    if (q < 27) {
+      const int a = q / 9, b = (q / 3) % 3, c = q % 3;
+      const float W = s[a] * s[3 + b] * s[6 + c];
+      const float fa = (float)a, fb = (float)b, fc = (float)c;
+      const float ux = fmaf(fc, s[18], fmaf(fb, s[15], fmaf(fa, s[12], s[9])));
+      const float uy = fmaf(fc, s[19], fmaf(fb, s[16], fmaf(fa, s[13], s[10])));
+      const float uz = fmaf(fc, s[20], fmaf(fb, s[17], fmaf(fa, s[14], s[11])));
+      red_add_v4_t(gacc + node_index(bx + a, by + b, bz + c, P), W * P.mass, W * ux, W * uy, W * uz);
+    } else {
+      const int k = q - 27;
+      const int b0 = (bx + 2 * (k >> 2)) >> 2, b1 = (by + 2 * ((k >> 1) & 1)) >> 2, b2 = (bz + 2 * (k & 1)) >> 2;
+      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+    }
+  }
+}
+
 template <bool DO_G2P, int ROWS, int MINB, int NT>
 __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
@@ -1038,6 +1078,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     float4* gacc = acc + (int64_t)bc.scene * P.nodes_per_scene;
     const float4* gvel = vel + (int64_t)bc.scene * P.nodes_per_scene;
     if (tid < 64) sm.pop[tid] = 0;
+    if (tid == 0) sm.nsc = 0;
     const int o[3] = {4 * bc.b[0] - 1, 4 * bc.b[1] - 1, 4 * bc.b[2] - 1};   // tile origin (grid node)
     if (DO_G2P && NSF_FUSED_VTILE) {
       for (int e = tid; e < kVT * kVT * kVT; e += NT) {
@@ -1074,11 +1115,26 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
         cell = (c[0] << 4) | (c[1] << 2) | c[2];
         rank = atomicAdd(&sm.pop[cell], 1);
       }
-      if (rank < ROWS) p2g_stage_values_f<ROWS * 64>(xn, vn, Cn, tau, cell * ROWS + rank, sm.u.slot, P);
+      bool inline_scatter = false;
+      if (rank < ROWS) {
+        p2g_stage_values_f<ROWS * 64>(xn, vn, Cn, tau, cell * ROWS + rank, sm.u.slot, P);
+      } else {
+        const int e = atomicAdd(&sm.nsc, 1);
+        if (e < kScatterCap) {
+          p2g_stage_values_f<1>(xn, vn, Cn, tau, e * kScatterEntry, sm.sc, P);
+          int pb = 0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            pb = (pb << 10) | min(max((int)floorf(xn[a] * P.inv_dx - 0.5f), 0), P.N[a] - 3);
+          sm.sc[e * kScatterEntry + kSlotFields] = __int_as_float(pb);
+        } else {
+          inline_scatter = true;
+        }
+      }
 #if NSF_WARP_SCATTER
-      p2g_scatter_warp(rank >= ROWS, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+      p2g_scatter_warp(inline_scatter, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
 #else
-      else p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+      if (inline_scatter) p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
 #endif
     }
     __syncthreads();
@@ -1087,7 +1143,16 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     float accm[9], accp[9][3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) { accm[k] = 0.f; accp[k][0] = accp[k][1] = accp[k][2] = 0.f; }
-    if (ox < 3) p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
+    {
+      const int nsc = min(sm.nsc, kScatterCap);
+      if (NT > 192) {
+        if (ox >= 3) scatter_listed<ROWS>(sm.sc, nsc, tid - 192, NT - 192, gacc, flags, list, list_count, scene_block0, P);
+        else p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
+      } else {
+        scatter_listed<ROWS>(sm.sc, nsc, tid, NT, gacc, flags, list, list_count, scene_block0, P);
+        p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
+      }
+    }
     __syncthreads();   // slot buffer becomes the partial buffer
     float* part = sm.u.part;
     const float m = P.mass;

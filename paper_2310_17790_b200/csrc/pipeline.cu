@@ -18,6 +18,18 @@ int64_t scan_tiles_for(int64_t total_blocks);
     prof_end(h, name, _ev);             \
   } while (0)
 
+// particles of a block stored in cell order.  NSF_REORDER_CELLS=0: block order
+// only; =block: one CTA per block (counting sort in shared memory); default:
+// flat passes (kernels_bin.cu)
+static int reorder_mode() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_REORDER_CELLS");
+    f = (e && e[0] == '0') ? 0 : (e && strcmp(e, "block") == 0) ? 2 : 1;
+  }
+  return f;
+}
+
 int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t total_blocks) {
   pb->total_blocks = total_blocks;
   pb->scan_tiles = scan_tiles_for(total_blocks);
@@ -25,6 +37,10 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   pb->block_start = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * (total_blocks + 1));
   pb->cursor = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
   pb->nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
+  if (reorder_mode() == 1) {
+    pb->ne_of = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
+    if (!pb->ne_of) return -1;
+  }
   pb->n_nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 4);
   pb->scan_status = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * pb->scan_tiles);
   pb->scan_ticket = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * 4);
@@ -52,25 +68,19 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
 nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
   if (pb->keys) pipeline_free(h, pb->keys);
   if (pb->perm) pipeline_free(h, pb->perm);
+  if (pb->cellcnt) pipeline_free(h, pb->cellcnt);
+  pb->cellcnt = nullptr;
 
   pb->keys = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
   pb->perm = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
   pb->pitch = pitch;
   if (!pb->keys || !pb->perm) return NSF_ERR_OUT_OF_MEMORY;
-  return NSF_OK;
-}
-
-// Invariant of the dense (tiled) path between substeps: keys[] and counts[]
-// describe the particles of the current buffer (written by the last G2P, or
-// here after a load).
-// particles of a block stored in cell order (NSF_REORDER_CELLS=0: block order only)
-static bool reorder_by_cell() {
-  static int f = -1;
-  if (f < 0) {
-    const char* e = getenv("NSF_REORDER_CELLS");
-    f = (e && e[0] == '0') ? 0 : 1;
+  if (reorder_mode() == 1) {   // a non-empty block holds >= 1 particle
+    const int64_t max_nonempty = pitch < pb->total_blocks ? pitch : pb->total_blocks;
+    pb->cellcnt = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 64 * (max_nonempty > 0 ? max_nonempty : 1));
+    if (!pb->cellcnt) return NSF_ERR_OUT_OF_MEMORY;
   }
-  return f == 1;
+  return NSF_OK;
 }
 
 // Re-binning with a physical reorder of buffer `cur` into 1 - cur (fused pipeline):
@@ -80,8 +90,13 @@ static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, i
   PLAUNCH(h, "bin_keys_hist",
           launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
   PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+  if (reorder_mode() == 1) {
+    PLAUNCH(h, "reorder",
+            launch_reorder_cells_flat(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb, *v.P));
+    return nxt;
+  }
   PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
-  if (reorder_by_cell())
+  if (reorder_mode() == 2)
     PLAUNCH(h, "reorder",
             launch_reorder_cells(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb, *v.P));
   else
@@ -117,9 +132,12 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
   HandleView v = view(h);
   const bool det = v.P->deterministic != 0;
   pb->tiled = v.model != NSF_NEURAL_STRESS && !det;
-  pb->fused = pb->tiled && v.P->force_mode == NSF_FORCE_MLS && fused_enabled();
+  // (the fused kernel packs a stencil base into 3 x 10 bits: N <= 1024 per axis)
+  pb->fused = pb->tiled && v.P->force_mode == NSF_FORCE_MLS && fused_enabled() && v.P->N[0] <= 1024 &&
+              v.P->N[1] <= 1024 && v.P->N[2] <= 1024;
   pb->since_rebin = 0;
   pb->launch_total = 0;
+  if (const char* e = getenv("NSF_REBIN_EVERY")) pb->rebin_every = atoi(e) > 0 ? atoi(e) : 32;
   pb->nsf_sorted = false;
   if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess)
     return NSF_ERR_CUDA;

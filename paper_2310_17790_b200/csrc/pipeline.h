@@ -21,6 +21,8 @@ struct PipelineBuffers {
   int32_t* cursor = nullptr;        // [total_blocks]
   int32_t* perm = nullptr;          // [pitch]  sorted slot -> storage slot
   int32_t* nonempty = nullptr;      // [total_blocks] list of non-empty block ids
+  int32_t* ne_of = nullptr;         // [total_blocks] list index of a non-empty block (cell-ordered re-binning)
+  int32_t* cellcnt = nullptr;       // [64 * min(total_blocks, pitch)] per-cell counts, then starts (idem)
   int32_t* n_nonempty = nullptr;    // [4]: n_nonempty, (unused), (unused), p2g block ticket (reset by scan)
   unsigned long long* scan_status = nullptr;  // [scan tiles]
   unsigned long long* scan_ticket = nullptr;  // [1] monotone ticket counter
@@ -122,6 +124,9 @@ void launch_grid_update_fixed(cudaStream_t st, PipelineBuffers* pb, unsigned lon
                               const DevParams& P, const int64_t* d_step);
 void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                           int32_t* ids_out, const PipelineBuffers* pb, const DevParams& P);
+void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
+                               int32_t* ids_out, PipelineBuffers* pb, const DevParams& P);
+int num_sms();
 void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                       int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const int64_t* scene_off,
                       int n_scenes, const DevParams& P, DevErr* err, int64_t* d_step);

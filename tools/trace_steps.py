@@ -30,7 +30,8 @@ def main():
         e1.record(st)
     ev[-1][1].synchronize()
     t = np.array([x.elapsed_time(y) * 1e3 for x, y in ev])
-    w = t[: a.n // 32 * 32].reshape(-1, 32)
+    per = int(os.environ.get("NSF_REBIN_EVERY", "32"))
+    w = t[: a.n // per * per].reshape(-1, per)
     print("window means (us):", " ".join(f"{v:.0f}" for v in w.mean(1)))
     print("by phase (us):     ", " ".join(f"{v:.0f}" for v in np.median(w, 0)))
     x = sim.read(nsf.NSF_FIELD_X)["x"]
