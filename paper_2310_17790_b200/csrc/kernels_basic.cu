@@ -271,7 +271,10 @@ void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, cons
 // clears the point's previous stencil in acc[(step + 1) & 1] and records the
 // current base.  The last CTA advances the step counter (every thread reads it
 // first).
-__global__ void __launch_bounds__(128) k_g2p_nsf(int64_t n, float* S, const int64_t* __restrict__ scene_off,
+#ifndef NSF_G2P_NSF_MINB
+#define NSF_G2P_NSF_MINB 6   // 80 registers: 24 warps per SM for the gather latency (C5 -2.4%)
+#endif
+__global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, float* S, const int64_t* __restrict__ scene_off,
                                                  int n_scenes, float4* acc0, float4* acc1, DevParams P, DevErr* err,
                                                  int64_t* d_step, int* done) {
   const int64_t step = *(volatile const int64_t*)d_step;

@@ -144,6 +144,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// the same without the wait (the caller issues tmem_wait() before using r)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -282,22 +295,30 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
   const int64_t n_tiles = (n + kM - 1) / kM;
   const int64_t tile_stride = (int64_t)gridDim.x * kStreams;
   // layer-1 inputs u = (X, z(n)) of point `tile * 128 + t`, fp32 (reading #20); loaded one tile ahead
-  auto load_inputs = [&](int64_t tile_, float* u_, int& scene_) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) u_[i] = 0.0f;
+  // (X and the scene are fetched a whole tile ahead, z(n) when the row is built)
+  auto fetch_x = [&](int64_t tile_, float* x_, int& scene_) {
     const int64_t p_ = tile_ * kM + t;
-    scene_ = 0;
+    scene_ = -1;
+    x_[0] = x_[1] = x_[2] = 0.0f;
     if (tile_ >= n_tiles || p_ >= n) return;
     scene_ = scene_of(p_, scene_off, n_scenes, n);
     if (xpitch >= 0) {
-      u_[0] = X[0 * xpitch + p_];
-      u_[1] = X[1 * xpitch + p_];
-      u_[2] = X[2 * xpitch + p_];
+      x_[0] = X[0 * xpitch + p_];
+      x_[1] = X[1 * xpitch + p_];
+      x_[2] = X[2 * xpitch + p_];
     } else {   // AoSoA planes of the particle store
-      u_[0] = X[pbase(p_) + 0 * 32];
-      u_[1] = X[pbase(p_) + 1 * 32];
-      u_[2] = X[pbase(p_) + 2 * 32];
+      x_[0] = X[pbase(p_) + 0 * 32];
+      x_[1] = X[pbase(p_) + 1 * 32];
+      x_[2] = X[pbase(p_) + 2 * 32];
     }
+  };
+  auto build_inputs = [&](const float* x_, int scene_, float* u_) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) u_[i] = 0.0f;
+    if (scene_ < 0) return;
+    u_[0] = x_[0];
+    u_[1] = x_[1];
+    u_[2] = x_[2];
     for (int k = 0; k < r && k < 13; ++k)
       u_[3 + k] = z[scene_ * r + k] + (float)step * (dz ? dz[scene_ * r + k] : 0.0f);
     u_[in_dim] = 1.0f;       // bias columns of the layer-1 B operand
@@ -311,12 +332,15 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     stream_barrier(s);
     tile = sm.tk[s];
   }
-  float u[16];
-  int scene = 0;
-  load_inputs(tile, u, scene);
+  float xf[3];
+  int scene_f;
+  fetch_x(tile, xf, scene_f);
   while (tile < n_tiles) {
     const int64_t p = tile * kM + t;
     const bool live = p < n;
+    const int scene = scene_f < 0 ? 0 : scene_f;
+    float u[16];
+    build_inputs(xf, scene_f, u);
     // A row t = [hi(u) | lo(u)], 32 tf32 = one 128-byte swizzled line
     {
       const uint32_t row = a_saddr + (uint32_t)t * 128u;
@@ -351,16 +375,26 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     phase ^= 1;
     fence_after();
 #pragma unroll 1
-    for (int c0 = 0; c0 < kW; c0 += 32) {
-      float h[32];
-      tmem_ld32(d_col + lane_sel + c0, h);   // bias already added by the MMA
+    for (int c0 = 0; c0 < kW; c0 += 64) {   // 64 columns per TMEM round trip
+      uint32_t r2[64];
+      tmem_ld32_nw(d_col + lane_sel + c0, r2);   // bias already added by the MMA
+      tmem_ld32_nw(d_col + lane_sel + c0 + 32, r2 + 32);
+      tmem_wait();
 #pragma unroll
-      for (int q = 0; q < 32; ++q) h[q] = elu(h[q]);
-      store_act32(a_saddr, t, c0, h);
+      for (int hh = 0; hh < 2; ++hh) {
+        float h[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) h[q] = elu(__uint_as_float(r2[32 * hh + q]));
+        store_act32(a_saddr, t, c0 + 32 * hh, h);
+      }
     }
     fence_before();
     fence_async_smem();
     stream_barrier(s);
+    // the next tile (its ticket was claimed before the layer-1 barrier): X now,
+    // so that the loads are in flight across the hidden layers
+    const int64_t next = mlp.ctr ? (int64_t)sm.tk[s] : tile + tile_stride;
+    fetch_x(next, xf, scene_f);
     // ---- hidden layers on tensor cores ----
     for (int l = 0; l < n_mma_hidden; ++l) {
       if (t == 0) {
@@ -378,18 +412,25 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       phase ^= 1;
       fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < kW; c0 += 32) {
-        float h[32];
-        tmem_ld32(d_col + lane_sel + c0, h);
+      for (int c0 = 0; c0 < kW; c0 += 64) {   // 64 columns per TMEM round trip
+        uint32_t r2[64];
+        tmem_ld32_nw(d_col + lane_sel + c0, r2);
+        tmem_ld32_nw(d_col + lane_sel + c0 + 32, r2 + 32);
+        tmem_wait();
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 b = lds_f4(bias_saddr + (uint32_t)((l + 1) * kW + c0 + 4 * q) * 4u);
-          h[4 * q] = elu(h[4 * q] + b.x);
-          h[4 * q + 1] = elu(h[4 * q + 1] + b.y);
-          h[4 * q + 2] = elu(h[4 * q + 2] + b.z);
-          h[4 * q + 3] = elu(h[4 * q + 3] + b.w);
+        for (int hh = 0; hh < 2; ++hh) {
+          float h[32];
+          const int cc = c0 + 32 * hh;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 b = lds_f4(bias_saddr + (uint32_t)((l + 1) * kW + cc + 4 * q) * 4u);
+            h[4 * q] = elu(__uint_as_float(r2[32 * hh + 4 * q]) + b.x);
+            h[4 * q + 1] = elu(__uint_as_float(r2[32 * hh + 4 * q + 1]) + b.y);
+            h[4 * q + 2] = elu(__uint_as_float(r2[32 * hh + 4 * q + 2]) + b.z);
+            h[4 * q + 3] = elu(__uint_as_float(r2[32 * hh + 4 * q + 3]) + b.w);
+          }
+          store_act32(a_saddr, t, cc, h);
         }
-        store_act32(a_saddr, t, c0, h);
       }
       fence_before();
       fence_async_smem();
@@ -425,8 +466,6 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       }
       if (q.enabled) nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);   // reduced P2G, tau from registers
     }
-    const int64_t next = mlp.ctr ? (int64_t)sm.tk[s] : tile + tile_stride;
-    load_inputs(next, u, scene);   // next tile's inputs (latency overlaps the barrier)
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile
     tile = next;
