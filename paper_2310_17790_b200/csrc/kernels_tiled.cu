@@ -767,8 +767,9 @@ static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shar
 //      gathered through L1) and writes the new state in place;
 //   2. stages the new state's P2G data by cell for the particles still inside
 //      block k (register accumulation per (cell, stencil plane), then one
-//      red.global.add.v4 per touched tile node), and scatters particles that left
-//      the block (or overflow a cell) directly with 27 red.global.add.v4;
+//      red.global.add.v4 per node of the thread's 3x3 plane: the L2 sums the
+//      up to 27 cell partials of a node), and scatters particles that left the
+//      block (or overflow a cell) directly with 27 red.global.add.v4;
 //   3. marks every grid block it touched in `flags`.
 // The grid update then visits exactly the flagged blocks.  Re-binning only
 // restores locality; correctness does not depend on it.
@@ -782,7 +783,7 @@ static_assert(sizeof(P2GSmem) + 1024 <= 228 * 1024 / NSF_FUSED_MIN_BLOCKS, "shar
 #define NSF_DENSE_MIN_BLOCKS NSF_FUSED_MIN_BLOCKS   // dense variant: CTAs per SM
 #endif
 #ifndef NSF_DENSE_ROWS
-#define NSF_DENSE_ROWS (NSF_FUSED_VTILE ? 11 : 12)
+#define NSF_DENSE_ROWS 10
 #endif
 constexpr int kRowsF = NSF_DENSE_ROWS;         // dense variant: staged rows per cell
 #ifndef NSF_SPARSE_ROWS
@@ -804,7 +805,6 @@ constexpr int kRowsF = NSF_DENSE_ROWS;         // dense variant: staged rows per
 #define NSF_SCATTER_CAP 40
 #endif
 constexpr int kScatterCap = NSF_SCATTER_CAP;
-constexpr int kScatterEntry = kSlotFields + 1;   // 21 staged values, packed stencil base
 
 constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-1, 4b+7)
 // padded strides of the tile (in float4): a warp's lanes differ mostly within one
@@ -814,19 +814,24 @@ constexpr int kVT = 8;                         // velocity tile edge: nodes [4b-
 constexpr int kVTy = 9, kVTx = 74;
 constexpr int kVTSize = (kVT - 1) * (kVTx + kVTy + 1) + 1;   // 589
 
+// Staged P2G row of one particle (24 floats = 6 float4): w_x(3) w_y(3) w_z(3),
+// u = m v - dx Q f (3), dx Q e_x (3), dx Q e_y (3), dx Q e_z (3), packed stencil
+// base (scatter list only), 2 pad.  Slots are [cell][row] with an odd cell
+// stride in float4, so a warp of 32 cells reading the same row is conflict-free.
+constexpr int kRowF4 = 6;
+template <int ROWS>
+struct FusedSlots {
+  static constexpr int kCellStride4 = ROWS * kRowF4 + 1;
+};
+
 template <int ROWS>
 struct __align__(16) FusedSmemT {
   float4 vt[NSF_FUSED_VTILE ? kVTSize : 1];   // G2P velocity tile (9.4 KB, padded strides)
-  union {
-    float slot[kSlotFields * ROWS * 64];       // [field][cell][row]
-    float part[27 * 4 * 64];                   // [(node*4 + comp)][cell]
-  } u;
+  float4 slot[64 * FusedSlots<ROWS>::kCellStride4];
+  float4 sc[kScatterCap * kRowF4];             // out-of-block particles: staged rows (+ packed base)
   int pop[64];
   int next;
   int nsc;                                     // entries of sc this segment
-  float sc[kScatterCap * kScatterEntry];       // out-of-block particles: staged values + packed base
-  __align__(16) uint16_t tbl[1728];
-  __align__(16) uint16_t tbl_off[224];
 };
 static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_DENSE_MIN_BLOCKS, "fused kernel: CTAs per SM");
 static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPARSE_MIN_BLOCKS,
@@ -888,9 +893,8 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
     for (int jj = 0; jj < 3; ++jj) Cn[i * 3 + jj] = cC * fmaf(-v[i], f[jj], M[i * 3 + jj]);
 }
 
-template <int kSlotStrideF>
-__device__ __forceinline__ void p2g_stage_values_f(const float x[3], const float v[3], const float Cm[9],
-                                                   const float T[6], int s, float* sl, const DevParams& P) {
+__device__ __forceinline__ void p2g_stage_row(const float x[3], const float v[3], const float Cm[9], const float T[6],
+                                              float4* row, const DevParams& P, float packed_base = 0.0f) {
   const float m = P.mass;
   const Axis a0 = bspline_axis(x[0], P.inv_dx), a1 = bspline_axis(x[1], P.inv_dx), a2 = bspline_axis(x[2], P.inv_dx);
   const float Tm[9] = {T[0], T[5], T[4], T[5], T[1], T[3], T[4], T[3], T[2]};
@@ -898,31 +902,31 @@ __device__ __forceinline__ void p2g_stage_values_f(const float x[3], const float
 #pragma unroll
   for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cm[k] - P.mls_coef * Tm[k];
   const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
-  const float vals[kSlotFields] = {a0.w[0], a0.w[1], a0.w[2], a1.w[0], a1.w[1], a1.w[2], a2.w[0], a2.w[1], a2.w[2],
-                                   m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2),
-                                   m * v[1] - P.dx * (Q[3] * f0 + Q[4] * f1 + Q[5] * f2),
-                                   m * v[2] - P.dx * (Q[6] * f0 + Q[7] * f1 + Q[8] * f2),
-                                   P.dx * Q[0], P.dx * Q[3], P.dx * Q[6],
-                                   P.dx * Q[1], P.dx * Q[4], P.dx * Q[7],
-                                   P.dx * Q[2], P.dx * Q[5], P.dx * Q[8]};
-#pragma unroll
-  for (int k = 0; k < kSlotFields; ++k) sl[k * kSlotStrideF + s] = vals[k];
+  row[0] = make_float4(a0.w[0], a0.w[1], a0.w[2], a1.w[0]);
+  row[1] = make_float4(a1.w[1], a1.w[2], a2.w[0], a2.w[1]);
+  row[2] = make_float4(a2.w[2], m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2),
+                       m * v[1] - P.dx * (Q[3] * f0 + Q[4] * f1 + Q[5] * f2),
+                       m * v[2] - P.dx * (Q[6] * f0 + Q[7] * f1 + Q[8] * f2));
+  row[3] = make_float4(P.dx * Q[0], P.dx * Q[3], P.dx * Q[6], P.dx * Q[1]);
+  row[4] = make_float4(P.dx * Q[4], P.dx * Q[7], P.dx * Q[2], P.dx * Q[5]);
+  row[5] = make_float4(P.dx * Q[8], packed_base, 0.0f, 0.0f);
 }
 
-template <int kSlotStrideF>
-__device__ __forceinline__ void p2g_accumulate_f(const float* sl, int my_cell, int ox, int rows, float accm[9],
-                                                 float accp[9][3]) {
+// Thread (cell, ox): sums, over the cell's staged rows, the P2G contributions to
+// its 9 nodes (ox, oy, oz) -- mass weight and affine momentum W (u + ox q0 + oy q1 + oz q2).
+template <int ROWS>
+__device__ __forceinline__ void p2g_accumulate_rows(const float4* slot, int my_cell, int ox, int rows, float accm[9],
+                                                    float accp[9][3]) {
   const float fox = (float)ox;
-  for (int r = 0; r < rows; ++r) {
-    const int s = my_cell * (kSlotStrideF / 64) + r;   // [field][cell][row]
-    const float wx = sl[ox * kSlotStrideF + s];
-    const float wyv[3] = {sl[3 * kSlotStrideF + s], sl[4 * kSlotStrideF + s], sl[5 * kSlotStrideF + s]};
-    const float wzv[3] = {sl[6 * kSlotStrideF + s], sl[7 * kSlotStrideF + s], sl[8 * kSlotStrideF + s]};
-    const float ux = fmaf(fox, sl[12 * kSlotStrideF + s], sl[9 * kSlotStrideF + s]);
-    const float uy = fmaf(fox, sl[13 * kSlotStrideF + s], sl[10 * kSlotStrideF + s]);
-    const float uz = fmaf(fox, sl[14 * kSlotStrideF + s], sl[11 * kSlotStrideF + s]);
-    const float q1x = sl[15 * kSlotStrideF + s], q1y = sl[16 * kSlotStrideF + s], q1z = sl[17 * kSlotStrideF + s];
-    const float q2x = sl[18 * kSlotStrideF + s], q2y = sl[19 * kSlotStrideF + s], q2z = sl[20 * kSlotStrideF + s];
+  const float4* rp = slot + my_cell * FusedSlots<ROWS>::kCellStride4;
+  for (int r = 0; r < rows; ++r, rp += kRowF4) {
+    const float4 A = rp[0], B = rp[1], Cv = rp[2], D = rp[3], E = rp[4], G = rp[5];
+    const float wx = ox == 0 ? A.x : (ox == 1 ? A.y : A.z);
+    const float wyv[3] = {A.w, B.x, B.y};
+    const float wzv[3] = {B.z, B.w, Cv.x};
+    const float ux = fmaf(fox, D.x, Cv.y), uy = fmaf(fox, D.y, Cv.z), uz = fmaf(fox, D.z, Cv.w);
+    const float q1x = D.w, q1y = E.x, q1z = E.y;
+    const float q2x = E.z, q2y = E.w, q2z = G.x;
 #pragma unroll
     for (int oy = 0; oy < 3; ++oy) {
       const float wxy = wx * wyv[oy];
@@ -1019,14 +1023,13 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 
 // Phase-2 scatter of the listed particles: work item i = (entry i / 35; its
 // stencil node i % 35 < 27, else one of its 8 corner blocks to mark touched).
-// Node (a, b, c) gets m W, W (u0 + a q0 + b q1 + c q2) as in p2g_accumulate_f.
-template <int ROWS>
-__device__ __forceinline__ void scatter_listed(const float* sc, int nsc, int i0, int stride, float4* gacc, int* flags,
+// Node (a, b, c) gets m W, W (u0 + a q0 + b q1 + c q2) as in p2g_accumulate_rows.
+__device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0, int stride, float4* gacc, int* flags,
                                                int* list, int* list_count, int64_t scene_block0, const DevParams& P) {
   for (int i = i0; i < nsc * 35; i += stride) {
     const int e = i / 35, q = i - 35 * e;
-    const float* s = sc + e * kScatterEntry;
-    const int pb = __float_as_int(s[kSlotFields]);
+    const float* s = reinterpret_cast<const float*>(sc + e * kRowF4);
+    const int pb = __float_as_int(s[21]);
     const int bx = pb >> 20, by = (pb >> 10) & 1023, bz = pb & 1023;
     if (q < 27) {
       const int a = q / 9, b = (q / 3) % 3, c = q % 3;
@@ -1057,18 +1060,11 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
   const int ox = tid >> 6;
   const int nblk = *(volatile int32_t*)&counters[0];
   if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
-  for (int q = tid; q < 1728 / 8 + 224 / 8; q += NT) {   // 16-byte chunks of both tables, asynchronously
-    if (q < 1728 / 8) cp_async16_f(&sm.tbl[8 * q], &g_p2g_tbl[8 * q], 16);
-    else cp_async16_f(&sm.tbl_off[8 * (q - 1728 / 8)], &g_p2g_tbl_off[8 * (q - 1728 / 8)], 16);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  const float cC_unused = 0.0f;
-  (void)cC_unused;
   // segment tickets: the first here, each next one claimed after phase 1 of the
   // current segment (its round trip overlaps phase 2)
   if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
   while (true) {
-    __syncthreads();   // also: previous segment's readers of part/slot are done
+    __syncthreads();   // also: previous segment's readers of slot are done
     const int bi = sm.next;
     if (bi >= nblk) break;
     const int key = nonempty[bi];
@@ -1117,16 +1113,15 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
       }
       bool inline_scatter = false;
       if (rank < ROWS) {
-        p2g_stage_values_f<ROWS * 64>(xn, vn, Cn, tau, cell * ROWS + rank, sm.u.slot, P);
+        p2g_stage_row(xn, vn, Cn, tau, sm.slot + cell * FusedSlots<ROWS>::kCellStride4 + rank * kRowF4, P);
       } else {
         const int e = atomicAdd(&sm.nsc, 1);
         if (e < kScatterCap) {
-          p2g_stage_values_f<1>(xn, vn, Cn, tau, e * kScatterEntry, sm.sc, P);
           int pb = 0;
 #pragma unroll
           for (int a = 0; a < 3; ++a)
             pb = (pb << 10) | min(max((int)floorf(xn[a] * P.inv_dx - 0.5f), 0), P.N[a] - 3);
-          sm.sc[e * kScatterEntry + kSlotFields] = __int_as_float(pb);
+          p2g_stage_row(xn, vn, Cn, tau, sm.sc + e * kRowF4, P, __int_as_float(pb));
         } else {
           inline_scatter = true;
         }
@@ -1146,67 +1141,32 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     {
       const int nsc = min(sm.nsc, kScatterCap);
       if (NT > 192) {
-        if (ox >= 3) scatter_listed<ROWS>(sm.sc, nsc, tid - 192, NT - 192, gacc, flags, list, list_count, scene_block0, P);
-        else p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
+        if (ox >= 3) scatter_listed(sm.sc, nsc, tid - 192, NT - 192, gacc, flags, list, list_count, scene_block0, P);
+        else p2g_accumulate_rows<ROWS>(sm.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
       } else {
-        scatter_listed<ROWS>(sm.sc, nsc, tid, NT, gacc, flags, list, list_count, scene_block0, P);
-        p2g_accumulate_f<ROWS * 64>(sm.u.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
+        scatter_listed(sm.sc, nsc, tid, NT, gacc, flags, list, list_count, scene_block0, P);
+        p2g_accumulate_rows<ROWS>(sm.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
       }
     }
-    __syncthreads();   // slot buffer becomes the partial buffer
-    float* part = sm.u.part;
-    const float m = P.mass;
+    // each (cell, plane) thread reduces its 9 node sums straight into the grid
+    // accumulator (one red.global.add.v4 per node); the segment's tile blocks
+    // (4x4x4 nodes at 4b and the +1 neighbours its stencils reach) are flagged
+    if (ox < 3 && sm.pop[my_cell] > 0) {
+      const float m = P.mass;
+      const int gi = 4 * bc.b[0] + (my_cell >> 4) + ox;
+      const int cy = 4 * bc.b[1] + ((my_cell >> 2) & 3), cz = 4 * bc.b[2] + (my_cell & 3);
+      const int x_part = (gi >> 2) * (P.NB[1] * P.NB[2] * kBlockNodes) + ((gi & 3) << 4);
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      if (ox >= 3) break;   // threads beyond 64 cells x 3 planes (NT > 192) only stage and reduce
-      const int node = ox * 9 + k;
-      part[(node * 4 + 0) * 64 + my_cell] = accm[k] * m;
-      part[(node * 4 + 1) * 64 + my_cell] = accp[k][0];
-      part[(node * 4 + 2) * 64 + my_cell] = accp[k][1];
-      part[(node * 4 + 3) * 64 + my_cell] = accp[k][2];
-    }
-    __syncthreads();
-    // node t = tid sums its 4 components; the 216 - NT remaining nodes are summed
-    // per component by threads 0 .. 4 (216 - NT) - 1, so no thread does two nodes
-    if (tid < 216) {
-      const int t = tid;
-      float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f;
-      const int q1 = sm.tbl_off[t + 1];
-      for (int q = sm.tbl_off[t]; q < q1; ++q) {
-        const int pr = sm.tbl[q];
-        const float* pp = part + (pr >> 6) * 256 + (pr & 63);
-        r0 += pp[0];
-        r1 += pp[64];
-        r2 += pp[128];
-        r3 += pp[192];
-      }
-      if (r0 > 0.0f) {
-        const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
-        const int gi = 4 * bc.b[0] + nx, gj = 4 * bc.b[1] + ny, gk = 4 * bc.b[2] + nz;
-        if (gi < P.N[0] && gj < P.N[1] && gk < P.N[2]) {
-          red_add_v4_t(gacc + node_index(gi, gj, gk, P), r0, r1, r2, r3);
-          touch_block(flags, list, list_count, (int)(scene_block0 + block_id(gi >> 2, gj >> 2, gk >> 2, P)));
-        }
+      for (int k = 0; k < 9; ++k) {
+        const int gj = cy + k / 3, gk = cz + k % 3;
+        const int off = x_part + ((gj >> 2) * P.NB[2] + (gk >> 2)) * kBlockNodes + ((gj & 3) << 2) + (gk & 3);
+        red_add_v4_t(gacc + off, accm[k] * m, accp[k][0], accp[k][1], accp[k][2]);
       }
     }
-    if (NT < 216 && tid < 4 * (216 - NT)) {
-      const int t = NT + (tid >> 2), comp = tid & 3;
-      float r = 0.f;
-      const int q1 = sm.tbl_off[t + 1];
-      for (int q = sm.tbl_off[t]; q < q1; ++q) {
-        const int pr = sm.tbl[q];
-        r += part[(pr >> 6) * 256 + (pr & 63) + 64 * comp];
-      }
-      if (r != 0.0f) {
-        const int nx = t / 36, ny = (t / 6) % 6, nz = t % 6;
-        const int gi = 4 * bc.b[0] + nx, gj = 4 * bc.b[1] + ny, gk = 4 * bc.b[2] + nz;
-        if (gi < P.N[0] && gj < P.N[1] && gk < P.N[2]) {
-          float* g = reinterpret_cast<float*>(gacc + node_index(gi, gj, gk, P)) + comp;
-          atomicAdd(g, r);
-          if (comp == 0 && r > 0.0f)
-            touch_block(flags, list, list_count, (int)(scene_block0 + block_id(gi >> 2, gj >> 2, gk >> 2, P)));
-        }
-      }
+    if (tid < 8) {
+      const int b0 = bc.b[0] + (tid >> 2), b1 = bc.b[1] + ((tid >> 1) & 1), b2 = bc.b[2] + (tid & 1);
+      if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])
+        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
     }
   }
 }
