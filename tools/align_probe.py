@@ -22,9 +22,10 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     for sh in a.shifts:
         d = [int(t) for t in sh.split(",")]
-        sc = {"C2": scenes.c2, "C3": scenes.c3, "C4": scenes.c4}[a.config]()
+        sc = {"C1": scenes.c1, "C2": scenes.c2, "C3": scenes.c3, "C4": scenes.c4, "C5": scenes.c5}[a.config]()
         for ax in range(3):
-            sc.x[:, ax] += d[ax] * sc.cfg.dx
+            if d[ax]:
+                sc.x[:, ax] += d[ax] * sc.cfg.dx
         stream = torch.cuda.Stream()
         sim = nsf.Simulator(sc.cfg, stream=stream.cuda_stream)
         sim.load_scene(sc)
