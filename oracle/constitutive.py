@@ -126,6 +126,44 @@ def return_map_von_mises(sigma, mu, tau_Y):
     return Z
 
 
+def return_map_von_mises_hs(sigma, mu, tau_Y, hardening=0.0, softening=0.0):
+    """PAPER.md line 545, von Mises with a per-particle yield stress (readings #30-#32).
+
+    tau_Y: (n,) yield stress of each particle at t_n.  For a live particle
+    (tau_Y > 0) the return map is return_map_von_mises with that tau_Y; then
+      hardening:  tau_Y^{n+1} = tau_Y^n + 2 mu xi delta_gamma
+      softening:  tau_Y^{n+1} = tau_Y^n - theta ||eps - proj(eps)||_F
+    (both applied when both coefficients are set), with eps = log(Sigma) and
+    proj(eps) = log(Z), only where the map projects (delta_gamma > 0).  "When
+    tau_Y reaches zero, the material is considered damaged and its Lame parameters
+    are set to zero": with softening (theta > 0), tau_Y^{n+1} <= 0 -> 0 and the
+    particle is damaged from this update on: it keeps Z = Sigma (no return map;
+    mu = 0 leaves delta_gamma undefined) and zero stress (the caller zeroes tau
+    where the returned `damaged` is set).  Without softening tau_Y only grows
+    (a zero initial yield stress is perfect plasticity, not damage).
+    Returns (Z, tau_Y_new, damaged).
+    """
+    s = np.maximum(np.asarray(sigma, dtype=np.float64), SIGMA_FLOOR)
+    tau_Y = np.broadcast_to(np.asarray(tau_Y, dtype=np.float64), s.shape[:1]).copy()
+    live = ~((softening > 0.0) & ~(tau_Y > 0.0))
+    eps = np.log(s)
+    tr = eps.sum(axis=1)
+    eps_hat = eps - tr[:, None] / 3.0
+    nrm = np.linalg.norm(eps_hat, axis=1)
+    dg = nrm - tau_Y / (2.0 * mu)
+    Z = s.copy()
+    proj = live & (dg > 0.0)
+    if np.any(proj):
+        Z[proj] = np.exp(eps[proj] - (dg[proj] / nrm[proj])[:, None] * eps_hat[proj])
+    tY = tau_Y.copy()
+    if np.any(proj):
+        plastic = np.linalg.norm(eps[proj] - np.log(Z[proj]), axis=1)   # ||eps - proj(eps)||_F
+        tY[proj] = tau_Y[proj] + 2.0 * mu * hardening * dg[proj] - softening * plastic
+    tY = np.where(tY > 0.0, tY, 0.0)
+    damaged = (softening > 0.0) & ~(tY > 0.0)
+    return Z, tY, damaged
+
+
 def elastoplastic_update(F_trial, model, mu, lam, alpha=0.0, tau_Y=0.0):
     """F^E = returnMap(F_trial), tau = tau(F^E).
 
@@ -148,3 +186,16 @@ def elastoplastic_update(F_trial, model, mu, lam, alpha=0.0, tau_Y=0.0):
         raise ValueError("model")
     F_E = _diag_sandwich(U, Z, V)
     return F_E, tau_hencky(U, Z, mu, lam)
+
+
+def elastoplastic_update_vm_hs(F_trial, mu, lam, tau_Y, hardening=0.0, softening=0.0):
+    """von Mises with hardening / softening and damage (readings
+    #30-#32): F^E = U Z V^T, tau = tau(F^E) with zero Lame parameters for damaged
+    particles.  Returns (F_E, tau, tau_Y_new)."""
+    F_trial = np.asarray(F_trial, dtype=np.float64)
+    U, s, V = svd_rotation_safe(F_trial)
+    Z, tY, damaged = return_map_von_mises_hs(s, mu, tau_Y, hardening, softening)
+    F_E = _diag_sandwich(U, Z, V)
+    tau = tau_hencky(U, Z, mu, lam)
+    tau[damaged] = 0.0
+    return F_E, tau, tY

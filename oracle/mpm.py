@@ -31,7 +31,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .constitutive import lame, dp_alpha, elastoplastic_update, tau_fixed_corotated, \
+from .constitutive import lame, dp_alpha, elastoplastic_update, elastoplastic_update_vm_hs, tau_fixed_corotated, \
     svd_rotation_safe, tau_hencky
 
 OFFSETS = np.array([(a, b, c) for a in range(3) for b in range(3) for c in range(3)],
@@ -66,6 +66,8 @@ class Params:
     plate_velocity: tuple = (0.0, 0.0, 0.0)
     force_mode: int = 0        # 0 MLS, 1 GRADW
     transfer: int = 0          # 0 APIC, 1 PIC
+    hardening: float = 0.0     # VM xi   (#30)
+    softening: float = 0.0     # VM theta (#30)
 
     @property
     def inv_dx(self):
@@ -84,7 +86,8 @@ def params_from_config(cfg) -> Params:
                   gravity=tuple(cfg.gravity), bc=tuple(cfg.bc), bc_width=cfg.bc_width,
                   plate_enabled=cfg.plate_enabled, plate_y0=cfg.plate_y0,
                   plate_velocity=tuple(cfg.plate_velocity), force_mode=cfg.force_mode,
-                  transfer=getattr(cfg, "transfer", 0))
+                  transfer=getattr(cfg, "transfer", 0), hardening=getattr(cfg, "hardening", 0.0),
+                  softening=getattr(cfg, "softening", 0.0))
 
 
 # ---------------------------------------------------------------------------
@@ -215,17 +218,25 @@ def substep(state: dict, P: Params, step: int, check=True) -> dict:
     uid, gnode, gm, gp = p2g(x, v, C, tau, P)
     vi = grid_update(gnode, gm, gp, P, step)
     x_new, v_new, C_new, F_tr = g2p(x, F, uid, vi, P)
-    F_E, tau_new = elastoplastic_update(F_tr, P.model, P.mu, P.lam, P.alpha, P.tau_Y)
+    out = {}
+    if P.model == 2 and (P.hardening != 0.0 or P.softening != 0.0):
+        # per-particle yield stress (#30-#32); state["tau_Y"] defaults to the material's
+        tY = np.asarray(state.get("tau_Y", np.full(x.shape[0], P.tau_Y)), np.float64)
+        F_E, tau_new, out["tau_Y"] = elastoplastic_update_vm_hs(F_tr, P.mu, P.lam, tY, P.hardening, P.softening)
+    else:
+        F_E, tau_new = elastoplastic_update(F_tr, P.model, P.mu, P.lam, P.alpha, P.tau_Y)
     if check:
         check_domain(x_new, P)
-    return {"x": x_new, "v": v_new, "C": C_new, "F": F_E, "tau": tau_new,
-            "grid": {"ids": uid, "node": gnode, "m": gm, "mv": gp, "v": vi}}
+    out.update({"x": x_new, "v": v_new, "C": C_new, "F": F_E, "tau": tau_new,
+                "grid": {"ids": uid, "node": gnode, "m": gm, "mv": gp, "v": vi}})
+    return out
 
 
 def run(state: dict, P: Params, n: int, step0: int = 0) -> dict:
-    s = {k: np.asarray(state[k], np.float64) for k in ("x", "v", "C", "F", "tau")}
+    s = {k: np.asarray(state[k], np.float64) for k in ("x", "v", "C", "F", "tau", "tau_Y") if k in state}
     for k in range(n):
         s = substep(s, P, step0 + k)
+        s.pop("grid")
     return s
 
 

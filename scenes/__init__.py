@@ -52,6 +52,8 @@ class Config:
     rho: float
     friction_angle_deg: float = 30.0
     yield_stress: float = 0.0
+    hardening: float = 0.0         # VM hardening coefficient xi
+    softening: float = 0.0         # VM softening coefficient theta
     gravity: tuple = (0.0, -9.8, 0.0)
     bc: tuple = (BC_STICKY,) * 6   # faces -x,+x,-y,+y,-z,+z
     bc_width: int = 3
