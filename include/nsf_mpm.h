@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define NSF_MPM_ABI_VERSION 2
+#define NSF_MPM_ABI_VERSION 3
 
 typedef struct nsf_mpm nsf_mpm; /* opaque; owns all device state */
 
@@ -121,6 +121,15 @@ typedef struct {
   double particle_volume;       /* V_p^0 (m^3); <= 0 -> dx^3/8 (8 ppc, #16); m = rho V0 */
   double stress_scale;          /* sigma_tau (Pa) multiplying the NSF output (#20)   */
   int32_t transfer;             /* nsf_transfer (ABI 2)                              */
+  /* von Mises yield-stress evolution (ABI 3, readings #30-#32): with
+   * either coefficient non-zero every particle carries its own tau_Y (starting at
+   * yield_stress); after a projecting return map (delta_gamma > 0)
+   *   tau_Y <- tau_Y + 2 mu hardening delta_gamma - softening ||eps - proj(eps)||_F
+   * (the norm equals delta_gamma).  With softening > 0 a particle whose tau_Y reaches 0
+   * is damaged: zero Lame parameters (tau = 0) and no return map from then on.
+   * Both >= 0 and finite (else INVALID_ARGUMENT); ignored for other models. */
+  double hardening;             /* xi                                                */
+  double softening;             /* theta (1/Pa * Pa: tau_Y units per unit log strain) */
 } nsf_material;
 
 /* read_state field mask; dst[k] is the k-th requested field in bit order. */
@@ -129,6 +138,7 @@ typedef struct {
 #define NSF_FIELD_C 4u   /* n x 3 x 3                               */
 #define NSF_FIELD_F 8u   /* n x 3 x 3 (elastic F_E; not for NSF)     */
 #define NSF_FIELD_TAU 16u /* n x 6 Voigt (stress used by the NEXT P2G) */
+#define NSF_FIELD_TAU_Y 32u /* n x 1 per-particle von Mises yield stress (ABI 3) */
 
 /* Version of this header's ABI (NSF_MPM_ABI_VERSION). */
 int32_t nsf_mpm_abi_version(void);

@@ -27,9 +27,9 @@ NSF_FIXED_COROTATED, NSF_DRUCKER_PRAGER, NSF_VON_MISES, NSF_NEURAL_STRESS, NSF_H
 NSF_TRANSFER_APIC, NSF_TRANSFER_PIC = range(2)
 NSF_BC_NONE, NSF_BC_STICKY, NSF_BC_SLIP = range(3)
 NSF_FORCE_MLS, NSF_FORCE_GRADW = range(2)
-NSF_FIELD_X, NSF_FIELD_V, NSF_FIELD_C, NSF_FIELD_F, NSF_FIELD_TAU = 1, 2, 4, 8, 16
+NSF_FIELD_X, NSF_FIELD_V, NSF_FIELD_C, NSF_FIELD_F, NSF_FIELD_TAU, NSF_FIELD_TAU_Y = 1, 2, 4, 8, 16, 32
 FIELD_SHAPES = {NSF_FIELD_X: (3,), NSF_FIELD_V: (3,), NSF_FIELD_C: (3, 3), NSF_FIELD_F: (3, 3),
-                NSF_FIELD_TAU: (6,)}
+                NSF_FIELD_TAU: (6,), NSF_FIELD_TAU_Y: ()}
 
 EXPORTS = ["nsf_mpm_abi_version", "nsf_mpm_create", "nsf_mpm_set_stream", "nsf_mpm_set_allocator",
            "nsf_mpm_load_particles", "nsf_mpm_load_stress_field", "nsf_mpm_set_latents",
@@ -47,7 +47,8 @@ class nsf_material(C.Structure):
                 ("plate_enabled", C.c_int32), ("plate_y0", C.c_double),
                 ("plate_velocity", C.c_double * 3), ("force_mode", C.c_int32),
                 ("deterministic", C.c_int32), ("n_scenes", C.c_int32),
-                ("particle_volume", C.c_double), ("stress_scale", C.c_double), ("transfer", C.c_int32)]
+                ("particle_volume", C.c_double), ("stress_scale", C.c_double), ("transfer", C.c_int32),
+                ("hardening", C.c_double), ("softening", C.c_double)]
 
 
 class NsfError(RuntimeError):
@@ -162,6 +163,8 @@ def make_material(cfg) -> nsf_material:
     m.particle_volume = cfg.particle_volume
     m.stress_scale = cfg.stress_scale
     m.transfer = int(getattr(cfg, "transfer", 0))
+    m.hardening = float(getattr(cfg, "hardening", 0.0))
+    m.softening = float(getattr(cfg, "softening", 0.0))
     return m
 
 
@@ -258,7 +261,7 @@ def nsf_mpm_eval_stress_field(h, z, points, out=None):
 def nsf_mpm_read_state(h, mask: int, n: int, device=None):
     """Returns a list of arrays (numpy if device is None, else torch tensors on it)."""
     outs = []
-    for bit in (1, 2, 4, 8, 16):
+    for bit in (1, 2, 4, 8, 16, 32):
         if mask & bit:
             shape = (n,) + FIELD_SHAPES[bit]
             if device is None:
@@ -388,7 +391,7 @@ class Simulator:
 
     def read(self, mask=NSF_FIELD_X | NSF_FIELD_V | NSF_FIELD_C | NSF_FIELD_F | NSF_FIELD_TAU, device=None):
         outs = nsf_mpm_read_state(self.h, mask, self.n, device)
-        names = [nm for bit, nm in ((1, "x"), (2, "v"), (4, "C"), (8, "F"), (16, "tau")) if mask & bit]
+        names = [nm for bit, nm in ((1, "x"), (2, "v"), (4, "C"), (8, "F"), (16, "tau"), (32, "tau_Y")) if mask & bit]
         return dict(zip(names, outs))
 
     def close(self):

@@ -44,6 +44,7 @@ __global__ void k_unpack(int64_t n, const float* __restrict__ x, const float* __
 #pragma unroll
     for (int k = 0; k < 6; ++k) S[pbase(p) + (PT + k) * 32] = 0.0f;
   }
+  S[pbase(p) + PTY * 32] = P.tau_Y;   // per-particle yield stress starts at the material's
 }
 
 void launch_unpack(cudaStream_t st, int64_t n, const float* x, const float* v, const float* C,
@@ -240,7 +241,14 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
         Ft[i * 3 + j] = Fp[i * 3 + j] + P.dt * (G[i * 3 + 0] * Fp[0 * 3 + j] + G[i * 3 + 1] * Fp[1 * 3 + j] +
                                                 G[i * 3 + 2] * Fp[2 * 3 + j]);
     float FE[9], tau[6];
-    float J = elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    float J;
+    if (P.vm_hs) {   // per-particle yield stress
+      float tY = S[pbase(p) + PTY * 32];
+      J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
+      S[pbase(p) + PTY * 32] = tY;
+    } else {
+      J = elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
 #pragma unroll
     for (int k = 0; k < 9; ++k) { S[pbase(p) + (PF + k) * 32] = FE[k]; finite &= isfinite(FE[k]); }

@@ -692,7 +692,14 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
       Ft[i * 3 + jj] = st.F[i * 3 + jj] + P.dt * (G[i * 3 + 0] * st.F[0 * 3 + jj] + G[i * 3 + 1] * st.F[1 * 3 + jj] +
                                                   G[i * 3 + 2] * st.F[2 * 3 + jj]);
   float FE[9], tau[6];
-  const float J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+  float J;
+  float tY = Sin[pbase(p) + PTY * 32];
+  if (P.vm_hs) {   // per-particle yield stress
+    J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
+  } else {
+    J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+  }
+  ob[PTY * 32] = tY;
 #pragma unroll
   for (int k = 0; k < 9; ++k) { ob[(PF + k) * 32] = FE[k]; chk += FE[k]; }
 #pragma unroll
@@ -957,7 +964,7 @@ __device__ __forceinline__ void load_xF(const float* __restrict__ S, int j, floa
   for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
 }
 
-template <bool DO_G2P>
+template <bool DO_G2P, bool HS>
 __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const float xin[3], const float Fin[9],
                                                    const int o[3], const float4* vt, const float4* __restrict__ gvel,
                                                    const DevParams& P, DevErr* err, float xn[3], float vn[3],
@@ -1002,7 +1009,14 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
         Ft[i * 3 + jj] = F[i * 3 + jj] + P.dt * (G[i * 3 + 0] * F[0 * 3 + jj] + G[i * 3 + 1] * F[1 * 3 + jj] +
                                                  G[i * 3 + 2] * F[2 * 3 + jj]);
     float FE[9];
-    const float J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    float J;
+    if (HS) {   // per-particle yield stress (#30-#32)
+      float tY = base[PTY * 32];
+      J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
+      base[PTY * 32] = tY;
+    } else {
+      J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    }
     float chk = xn[0] + xn[1] + xn[2] + vn[0] + vn[1] + vn[2];
 #pragma unroll
     for (int k = 0; k < 9; ++k) { base[(PF + k) * 32] = FE[k]; chk += FE[k]; }
@@ -1047,7 +1061,7 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
   }
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT>
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false>
 __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
@@ -1094,7 +1108,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     for (int j = s0 + tid; j < s1; j += NT) {
       float xn[3], vn[3], Cn[9], tau[6];
       if (DO_G2P && j != s0 + tid) load_xF(S, j, x0, F0);
-      fused_g2p_particle<DO_G2P>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
+      fused_g2p_particle<DO_G2P, HS>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
       // ---- P2G of the new state: by cell if still inside this block, else direct ----
       int c[3];
       bool core = true;
@@ -1295,22 +1309,27 @@ void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_
                                                  pb->n_nonempty, P);
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT>
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false>
 static void launch_g2p2g_t(cudaStream_t st, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
   const size_t smem = sizeof(FusedSmemT<ROWS>);
   if (!attr) {
-    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_g2p2g<DO_G2P, ROWS, MINB, NT><<<num_sms() * MINB, NT, smem, st>>>(
+  k_g2p2g<DO_G2P, ROWS, MINB, NT, HS><<<num_sms() * MINB, NT, smem, st>>>(
       S, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
       pb->n_nonempty, P, err, d_step);
 }
 
 void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
                   const DevParams& P, DevErr* err, int64_t* d_step) {
+  if (do_g2p && P.vm_hs) {   // von Mises with a per-particle yield stress
+    if (pb->sparse) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192, true>(st, S, vel, acc, pb, P, err, d_step);
+    else launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS, true>(st, S, vel, acc, pb, P, err, d_step);
+    return;
+  }
   if (pb->sparse) {
     if (do_g2p) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192>(st, S, vel, acc, pb, P, err, d_step);
     else launch_g2p2g_t<false, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192>(st, S, vel, acc, pb, P, err, d_step);

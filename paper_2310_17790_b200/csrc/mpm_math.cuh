@@ -169,8 +169,11 @@ __device__ __forceinline__ void svd3(const float A[9], float U[3][3], float sig[
 // ---------------------------------------------------------------------------
 // constitutive update: F_trial -> (F_E, tau Voigt).  Returns det(F_E).
 //   model 0: fixed corotated   1: Drucker-Prager + Hencky   2: von Mises + Hencky
+// dg_out (optional): the von Mises delta_gamma where the map projects, else 0
+// (the per-particle yield-stress update of P:545 uses it).
 __device__ __forceinline__ float elastoplastic(const float Ft[9], int model, float mu, float lam,
-                                               float alpha, float tau_Y, float FE[9], float tau[6]) {
+                                               float alpha, float tau_Y, float FE[9], float tau[6],
+                                               float* dg_out = nullptr) {
   float U[3][3], V[3][3], s[3];
   svd3(Ft, U, s, V);
   if (model == 0) {
@@ -218,6 +221,7 @@ __device__ __forceinline__ float elastoplastic(const float Ft[9], int model, flo
   } else {
     dg = nrm - tau_Y / (2.0f * mu);
   }
+  if (dg_out) *dg_out = (model == 2 && dg > 0.0f) ? dg : 0.0f;
   float le[3];   // log Z
   bool elastic = false;
   if (expand) {
@@ -263,6 +267,7 @@ __device__ __forceinline__ float elastoplastic(const float Ft[9], int model, flo
 
 // ---------------------------------------------------------------------------
 // Fast constitutive path (same results as elastoplastic() up to rounding).
+// (vm_hs_update below wraps it for the per-particle yield stress of P:545.)
 //
 // Log-strain models (DP, VM): with F = U Sigma V^T, the left Cauchy-Green tensor
 // b = F F^T = U Sigma^2 U^T, so a symmetric Jacobi eigen-decomposition of b gives
@@ -388,7 +393,7 @@ __device__ __forceinline__ Sym6 sym_exp_small(const Sym6& A, float a2) {
 // Returns false (caller falls back to the eigen path) outside the series' range.
 __device__ __forceinline__ bool elastoplastic_series(const float Ft[9], const Sym6& S, int model, float mu,
                                                      float lam, float alpha, float tau_Y, float FE[9], float tau[6],
-                                                     float& detFE) {
+                                                     float& detFE, float* dg_out = nullptr) {
   if (!(sym_fro2(S) <= 0.09f)) return false;
   // Y = S (2I + S)^-1
   const Sym6 M{2.0f + S.xx, 2.0f + S.yy, 2.0f + S.zz, S.yz, S.xz, S.xy};
@@ -422,6 +427,7 @@ __device__ __forceinline__ bool elastoplastic_series(const float Ft[9], const Sy
   } else {            // von Mises
     dg = nrm - tau_Y / (2.0f * mu);
   }
+  if (dg_out) *dg_out = (model == 2 && dg > 0.0f) ? dg : 0.0f;
   Sym6 Ee = E;   // eps_E
   if (expand || dg > 0.0f) {
     // A = eps_E - eps: -eps (DP tip) or -(dg / |eps_hat|) eps_hat
@@ -459,12 +465,12 @@ __device__ __forceinline__ bool elastoplastic_series(const float Ft[9], const Sy
 }
 
 __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model, float mu, float lam, float alpha,
-                                                    float tau_Y, float FE[9], float tau[6]) {
+                                                    float tau_Y, float FE[9], float tau[6], float* dg_out = nullptr) {
   const float J = det3(Ft);
-  if (!(J > 1e-6f)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+  if (!(J > 1e-6f)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau, dg_out);
   if (model == 0) {
     float R[9];
-    if (!polar_newton(Ft, R)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+    if (!polar_newton(Ft, R)) return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau, dg_out);
     float D[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) D[k] = Ft[k] - R[k];
@@ -505,14 +511,14 @@ __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model
   {
     float detS;
     const Sym6 S6{Bm[0][0], Bm[1][1], Bm[2][2], Bm[1][2], Bm[0][2], Bm[0][1]};
-    if (elastoplastic_series(Ft, S6, model, mu, lam, alpha, tau_Y, FE, tau, detS)) return detS;
+    if (elastoplastic_series(Ft, S6, model, mu, lam, alpha, tau_Y, FE, tau, detS, dg_out)) return detS;
   }
 #endif
   float U[3][3];
   sym_eig3(Bm, U);
   const float kFloor2 = 1e-8f;   // sigma >= 1e-4
   if (!(1.0f + Bm[0][0] > kFloor2 && 1.0f + Bm[1][1] > kFloor2 && 1.0f + Bm[2][2] > kFloor2))
-    return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau);
+    return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau, dg_out);
   // eps = log sigma = log(lambda)/2
   const float e[3] = {0.5f * log1pf(Bm[0][0]), 0.5f * log1pf(Bm[1][1]), 0.5f * log1pf(Bm[2][2])};
   const float tr = e[0] + e[1] + e[2];
@@ -526,6 +532,7 @@ __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model
   } else {
     dg = nrm - tau_Y / (2.0f * mu);
   }
+  if (dg_out) *dg_out = (model == 2 && dg > 0.0f) ? dg : 0.0f;
   float le[3];
   bool elastic = false;
   if (expand) {
@@ -572,6 +579,33 @@ __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model
 }
 
 // Elastic stress of a given (admissible) F, used for tau^0 at load (reading #9).
+// von Mises with a per-particle yield stress (readings #30-#32):
+// the return map with tau_Y^n, then tau_Y^{n+1} = tau_Y^n + 2 mu xi dg - theta dg
+// (||eps - proj(eps)||_F = dg for the radial return); with softening (theta > 0)
+// tau_Y <= 0 is damage: Lame parameters zero (tau = 0) and no return map.
+// tY is read and updated in place; returns det F_E.
+__device__ __forceinline__ float vm_hs_update(const float Ft[9], float mu, float lam, float hard_k, float soft,
+                                              float& tY, float FE[9], float tau[6]) {
+  if (soft > 0.0f && !(tY > 0.0f)) {   // damaged
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) tau[k] = 0.0f;
+    tY = 0.0f;
+    return det3(Ft);
+  }
+  float dg = 0.0f;
+  const float J = elastoplastic_fast(Ft, 2, mu, lam, 0.0f, tY, FE, tau, &dg);
+  float t1 = fmaf(hard_k, dg, tY) - soft * dg;
+  t1 = t1 > 0.0f ? t1 : 0.0f;
+  if (soft > 0.0f && !(t1 > 0.0f)) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) tau[k] = 0.0f;
+  }
+  tY = t1;
+  return J;
+}
+
 __device__ __forceinline__ void elastic_tau(const float F[9], int model, float mu, float lam, float tau[6]) {
   float FE[9];
   // FC: same formula; DP/VM: Hencky of F itself (no return map at load)

@@ -26,7 +26,8 @@ enum Plane : int {
   // reduced (NSF) model, which has no F: plane PF holds the packed stencil base of
   // the last P2G, planes PXR..PXR+2 the reference position X (MLP input)
   PXR = PF + 1,
-  kPlanes = 30
+  PTY = 30,  // per-particle von Mises yield stress (hardening / softening); load value elsewhere
+  kPlanes = 31
 };
 
 constexpr int kTileP = 32;
@@ -65,6 +66,9 @@ struct DevParams {
   float stress_scale;
   int deterministic;  // 1: fixed-point P2G (kernels_det.cu), bitwise reproducible
   float mC;           // affine mass of P2G: m_p (APIC) or 0 (PIC)
+  int vm_hs;          // 1: von Mises with a per-particle yield stress (plane PTY, #30-#32)
+  float vm_hard_k;    //   2 mu xi (hardening)
+  float vm_soft;      //   theta (softening; tau_Y <= 0 is damage)
 };
 
 __host__ __device__ inline long long block_id(int b0, int b1, int b2, const DevParams& P) {

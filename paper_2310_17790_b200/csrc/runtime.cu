@@ -251,6 +251,8 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   if (m->model == NSF_DRUCKER_PRAGER && !(m->friction_angle_deg > 0 && m->friction_angle_deg < 90))
     return NSF_ERR_INVALID_ARGUMENT;
   if (!(m->yield_stress >= 0)) return NSF_ERR_INVALID_ARGUMENT;
+  if (!(m->hardening >= 0 && std::isfinite(m->hardening)) || !(m->softening >= 0 && std::isfinite(m->softening)))
+    return NSF_ERR_INVALID_ARGUMENT;
   if (m->bc_width < 0) return NSF_ERR_INVALID_ARGUMENT;
   for (int f = 0; f < 6; ++f)
     if (m->bc[f] < 0 || m->bc[f] > 2) return NSF_ERR_INVALID_ARGUMENT;
@@ -310,6 +312,9 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
     P.tau_Y = INFINITY;
   }
   P.mC = m->transfer == NSF_TRANSFER_PIC ? 0.0f : P.mass;
+  P.vm_hs = m->model == NSF_VON_MISES && (m->hardening > 0 || m->softening > 0);
+  P.vm_hard_k = (float)(2.0 * mu * m->hardening);
+  P.vm_soft = (float)m->softening;
   P.force_mode = m->force_mode;
   P.mls_coef = (float)(dt * V0 * 4.0 / (dx * dx));
   P.gradw_coef = (float)(dt * V0);
@@ -646,17 +651,17 @@ nsf_status nsf_mpm_read_state(nsf_mpm* h, uint32_t mask, float* const* dst, int3
   if (!h) return NSF_ERR_INVALID_ARGUMENT;
   if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
   if (!h->loaded) return fail(h, NSF_ERR_BAD_STATE, "nothing loaded");
-  if (mask == 0 || (mask & ~31u)) return fail(h, NSF_ERR_INVALID_ARGUMENT, "bad field mask");
+  if (mask == 0 || (mask & ~63u)) return fail(h, NSF_ERR_INVALID_ARGUMENT, "bad field mask");
   if (!dst) return fail(h, NSF_ERR_INVALID_ARGUMENT, "dst required");
   if ((mask & NSF_FIELD_F) && h->mat.model == NSF_NEURAL_STRESS)
     return fail(h, NSF_ERR_INVALID_ARGUMENT, "F is not tracked by the reduced (NSF) variant");
   nsf_status err_status = check_device_errors(h);
   if (h->poisoned) return err_status;
-  const int planes[5] = {PX, PV, PC, PF, PT};
-  const int comps[5] = {3, 3, 9, 9, 6};
+  const int planes[6] = {PX, PV, PC, PF, PT, PTY};
+  const int comps[6] = {3, 3, 9, 9, 6, 1};
   int k = 0;
   int64_t n = h->n;
-  for (int f = 0; f < 5; ++f) {
+  for (int f = 0; f < 6; ++f) {
     if (!(mask & (1u << f))) continue;
     float* out = dst[k++];
     if (!out) return fail(h, NSF_ERR_INVALID_ARGUMENT, "dst[%d] is NULL", k - 1);
