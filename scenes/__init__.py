@@ -284,6 +284,25 @@ def deformation_field(seed: int = SEEDS["C5"] + 1000, r: int = 6, width: int = 1
     return g
 
 
+def affine_field(seed: int = SEEDS["C5"] + 2000, r: int = 6, width: int = 128, n_hidden: int = 4) -> dict:
+    """Random-init neural affine-velocity field l(X, z) -> C (9, row-major; PAPER.md
+    line 253), reading #20's initialisation with the output layer scaled by 1/16 and
+    zero output bias: a stand-in for the trained network of network inference."""
+    l = xavier_bf16_mlp(np.random.default_rng(seed), [3 + r] + [width] * n_hidden + [9])
+    w = (l["W"][-1] / np.float32(16.0)).astype(np.float32)
+    l["W"][-1] = w
+    l["W_bits"][-1] = (w.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+    l["b"][-1] = np.zeros(9, np.float32)
+    return l
+
+
+def reference_body(seed: int = SEEDS["C5"], n_ref: int = 200000) -> np.ndarray:
+    """C5's shared reference body (reading #19): n_ref points U[0.3, 0.7]^3 (the same
+    stream c5() draws its per-scene samples from)."""
+    rref = _streams(seed, 6)[0]
+    return rref.uniform(0.3, 0.7, size=(n_ref, 3))
+
+
 # ---------------------------------------------------------------------------
 # small parity variants (several tiles + ragged tails, oracle-friendly sizes)
 
