@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define NSF_MPM_ABI_VERSION 3
+#define NSF_MPM_ABI_VERSION 4
 
 typedef struct nsf_mpm nsf_mpm; /* opaque; owns all device state */
 
@@ -212,6 +212,44 @@ nsf_status nsf_mpm_load_deformation_field(nsf_mpm* h, int32_t in_dim, int32_t wi
  * positive definite keeps its latent. */
 nsf_status nsf_mpm_invert_latents(nsf_mpm* h, int32_t n_sample, int32_t n_iters, float* z_out,
                                   int32_t on_device);
+
+/* Neural affine-velocity field l(X, z) -> C (9 outputs, row-major 3 x 3; PAPER.md
+ * line 253) for infer_state (ABI 4).  Same parameter layout and numerics as
+ * load_stress_field; in_dim = 3 + r, width = 128, 1 <= n_hidden <= 8, out_dim = 9.
+ * INVALID_ARGUMENT otherwise.  Synchronous. */
+nsf_status nsf_mpm_load_affine_field(nsf_mpm* h, int32_t in_dim, int32_t width, int32_t n_hidden,
+                                     int32_t out_dim, const uint16_t* W_bf16, const float* b,
+                                     int32_t on_device);
+
+/* Network inference (ABI 4) for every current point p with
+ * reference position X_p (load_stress_field's X_ref):
+ *     x_p = g(X_p, z_n),  v_p = (g(X_p, z_n) - g(X_p, z_prev)) / dt,  C_p = l(X_p, z_n)
+ * with z_n = z + n dz the latent of the next substep (n = the step counter) and
+ * z_prev (n_scenes x r floats, host or device per on_device) the previous latent,
+ * or NULL for z + (n-1) dz (n >= 1) resp. z_n (n = 0: particles at rest).
+ * Overwrites x, v and C (tau comes from the stress field in the next substep).
+ * Asynchronous.  BAD_STATE without the NSF model, load_stress_field with X_ref,
+ * set_latents, load_deformation_field and load_affine_field; INVALID_ARGUMENT if g
+ * or l does not take 3 + r inputs. */
+nsf_status nsf_mpm_infer_state(nsf_mpm* h, const float* z_prev, int32_t on_device);
+
+/* Sample and integration particles (ABI 4).  X_all: the
+ * reference body (n_ref x 3, shared by all scenes); per scene s the sample particles
+ * S_s = X_all[sample_idx[s * n_sample + q]], q < n_sample (distinct within a scene).
+ * With x_p = g(X_p, z_n(s)) (z_n as in infer_state):
+ *     I_s = nodes of the 27-node stencils (base = floor(x/dx - 1/2)) of the x_p, p in S_s
+ *     N_s = { p : the stencil of x_p meets I_s }          (S_s is a subset of N_s)
+ * The handle's points become, per scene, S_s in the given order followed by N_s \ S_s
+ * in increasing index order (so invert_latents' "first n_sample points" are S_s),
+ * with reference positions X_all[p] and infer_state(z_prev) applied; the step
+ * counter and latents are kept.  counts_out (host, n_scenes) receives |N_s|; may be
+ * NULL.  Synchronous; X_all, sample_idx and z_prev are host or device per on_device.
+ * INVALID_ARGUMENT for bad sizes or indices, BAD_STATE as for infer_state,
+ * OUT_OF_DOMAIN if a sample's stencil leaves the grid. */
+nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float* X_all,
+                                         int32_t n_sample, const int32_t* sample_idx,
+                                         const float* z_prev, int64_t* counts_out,
+                                         int32_t on_device);
 
 /* Enqueue n >= 0 substeps on the handle's stream (a cached CUDA graph of the
  * substep is replayed).  Asynchronous.  NSF_ERR_BAD_STATE before

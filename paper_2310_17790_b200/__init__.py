@@ -34,6 +34,7 @@ FIELD_SHAPES = {NSF_FIELD_X: (3,), NSF_FIELD_V: (3,), NSF_FIELD_C: (3, 3), NSF_F
 EXPORTS = ["nsf_mpm_abi_version", "nsf_mpm_create", "nsf_mpm_set_stream", "nsf_mpm_set_allocator",
            "nsf_mpm_load_particles", "nsf_mpm_load_stress_field", "nsf_mpm_set_latents",
            "nsf_mpm_load_deformation_field", "nsf_mpm_invert_latents",
+           "nsf_mpm_load_affine_field", "nsf_mpm_infer_state", "nsf_mpm_build_integration_set",
            "nsf_mpm_substep", "nsf_mpm_eval_stress_field", "nsf_mpm_read_state", "nsf_mpm_sync",
            "nsf_mpm_step_count", "nsf_mpm_inverted_count", "nsf_mpm_last_error", "nsf_mpm_destroy",
            "nsf_mpm_debug_bins", "nsf_mpm_debug_grid", "nsf_mpm_set_profiling",
@@ -82,6 +83,9 @@ def lib():
         "nsf_mpm_set_latents": (i32, [vp, i32, vp, vp, i32]),
         "nsf_mpm_load_deformation_field": (i32, [vp, i32, i32, i32, i32, vp, vp, i32]),
         "nsf_mpm_invert_latents": (i32, [vp, i32, i32, vp, i32]),
+        "nsf_mpm_load_affine_field": (i32, [vp, i32, i32, i32, i32, vp, vp, i32]),
+        "nsf_mpm_infer_state": (i32, [vp, vp, i32]),
+        "nsf_mpm_build_integration_set": (i32, [vp, i64, vp, i32, vp, vp, dp(i64), i32]),
         "nsf_mpm_substep": (i32, [vp, i32]),
         "nsf_mpm_eval_stress_field": (i32, [vp, vp, i64, vp, vp, i32]),
         "nsf_mpm_read_state": (i32, [vp, u32, dp(vp), i32]),
@@ -228,6 +232,33 @@ def nsf_mpm_load_deformation_field(h, in_dim, width, n_hidden, out_dim, W_bf16, 
     pb, db, kb = _ptr(b)
     on = _same_residency(dw, db)
     _check(h, lib().nsf_mpm_load_deformation_field(h, in_dim, width, n_hidden, out_dim, pw, pb, on))
+
+
+def nsf_mpm_load_affine_field(h, in_dim, width, n_hidden, out_dim, W_bf16, b):
+    pw, dw, kw = _ptr(W_bf16, np.uint16)
+    pb, db, kb = _ptr(b)
+    on = _same_residency(dw, db)
+    _check(h, lib().nsf_mpm_load_affine_field(h, in_dim, width, n_hidden, out_dim, pw, pb, on))
+
+
+def nsf_mpm_infer_state(h, z_prev=None):
+    """Network inference x, v, C (header); z_prev: None or n_scenes x r (numpy / CUDA tensor)."""
+    pz, dz_, kz = _ptr(z_prev)
+    _check(h, lib().nsf_mpm_infer_state(h, pz, dz_ or 0))
+
+
+def nsf_mpm_build_integration_set(h, X_all, sample_idx, z_prev=None, n_scenes=1):
+    """Sample / integration particles (header).  X_all: n_ref x 3; sample_idx: n_scenes x
+    n_sample int32 (numpy, or both CUDA tensors).  Returns |N_s| per scene (numpy int64)."""
+    px, dx_, kx = _ptr(X_all)
+    ps, ds, ks = _ptr(sample_idx, np.int32)
+    pz, dzz, kz = _ptr(z_prev)
+    on = _same_residency(dx_, ds, dzz) if z_prev is not None else _same_residency(dx_, ds)
+    n_ref = int(X_all.shape[0])
+    n_sample = int(np.prod(sample_idx.shape)) // n_scenes
+    counts = (C.c_int64 * n_scenes)()
+    _check(h, lib().nsf_mpm_build_integration_set(h, n_ref, px, n_sample, ps, pz, counts, on))
+    return np.array(counts[:], dtype=np.int64)
 
 
 def nsf_mpm_invert_latents(h, n_sample: int, n_iters: int, z_out=None):
@@ -379,6 +410,22 @@ class Simulator:
         b = np.concatenate(mlp["b"])
         nsf_mpm_load_deformation_field(self.h, dims[0], dims[1], len(dims) - 2, dims[-1], W, b)
         self._r = dims[0] - 3
+
+    def load_affine_field(self, mlp):
+        dims = mlp["dims"]
+        W = np.concatenate([w.reshape(-1) for w in mlp["W_bits"]])
+        b = np.concatenate(mlp["b"])
+        nsf_mpm_load_affine_field(self.h, dims[0], dims[1], len(dims) - 2, dims[-1], W, b)
+
+    def infer_state(self, z_prev=None):
+        """x = g(X, z_n), v = (x - g(X, z_prev)) / dt, C = l(X, z_n) for every point."""
+        nsf_mpm_infer_state(self.h, z_prev)
+
+    def build_integration_set(self, X_all, sample_idx, z_prev=None):
+        """Replace the points by S then N \\ S per scene (header); returns |N_s|."""
+        counts = nsf_mpm_build_integration_set(self.h, X_all, sample_idx, z_prev, self.cfg.n_scenes)
+        self.n = int(counts.sum())
+        return counts
 
     def invert_latents(self, n_sample, n_iters=3):
         """Network inversion; returns z_hat (n_scenes x r)."""

@@ -58,4 +58,17 @@ void launch_gn_invert(cudaStream_t st, int64_t n, const int32_t* ids, const int6
                       int n_sample, int r, const float* S, const float* z, const float* dz, const int64_t* d_step,
                       const MlpDev& g, int n_iters, int32_t* slots, float* zw, double* accum);
 
+// kernels_infer.cu -- network inference and the integration set
+void launch_latent_at(cudaStream_t st, int64_t m, const float* z, const float* dz, int64_t step, float* out);
+void launch_backdiff(cudaStream_t st, int64_t n, float* S, float dt);
+void launch_mark_stencils(cudaStream_t st, int n_sample, const int32_t* idx, const float* x, uint32_t* mask,
+                          const DevParams& P, DevErr* err);
+void launch_member_flags(cudaStream_t st, int64_t n_ref, const float* x, const uint32_t* mask,
+                         const uint8_t* is_sample, uint8_t* flag, const DevParams& P);
+void launch_set_samples(cudaStream_t st, int n_sample, const int32_t* idx, uint8_t* is_sample, uint8_t v);
+int64_t compact_blocks(int64_t n);
+void launch_count_blocks(cudaStream_t st, int64_t n, const uint8_t* flag, int32_t* cnt);
+void launch_compact(cudaStream_t st, int64_t n, const uint8_t* flag, const int32_t* base, int32_t* out);
+void launch_gather_rows3(cudaStream_t st, int64_t m, const int32_t* list, const float* X_all, float* X_new);
+
 }  // namespace nsf

@@ -14,6 +14,7 @@ namespace nsf {
 
 constexpr int kTile = 128;        // points per CTA tile (one per thread)
 constexpr int kMaxWidth = 128;
+constexpr int kMaxOut = 16;       // output width (stress 6, deformation 3, affine velocity 9)
 
 __device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
 
@@ -116,19 +117,19 @@ __global__ void __launch_bounds__(kTile) k_nsf_mlp_simt(int64_t n, const float* 
     {
       const uint16_t* Wt = sm + mlp.w_off[L - 1];
       const float* b = mlp.b + mlp.b_off[L - 1];
-      float y[8];
+      float y[kMaxOut];
 #pragma unroll
-      for (int o = 0; o < 8; ++o) y[o] = (o < mlp.out_dim) ? b[o] : 0.0f;
+      for (int o = 0; o < kMaxOut; ++o) y[o] = (o < mlp.out_dim) ? b[o] : 0.0f;
       for (int k = 0; k < width; ++k) {
         float hk = bf16_bits_to_f32(hA[k * kTile + t]);
 #pragma unroll
-        for (int o = 0; o < 8; ++o)
+        for (int o = 0; o < kMaxOut; ++o)
           if (o < mlp.out_dim) y[o] = fmaf(bf16_bits_to_f32(Wt[k * mlp.out_dim + o]), hk, y[o]);
       }
       if (live) {
-        float tau[8];
+        float tau[kMaxOut];
 #pragma unroll
-        for (int o = 0; o < 8; ++o) tau[o] = stress_scale * y[o];
+        for (int o = 0; o < kMaxOut; ++o) tau[o] = stress_scale * y[o];
         for (int o = 0; o < mlp.out_dim; ++o) {
           if (aos_out) tau_out[p * mlp.out_dim + o] = tau[o];
           else tau_out[pbase(p) + o * 32] = tau[o];   // AoSoA particle store

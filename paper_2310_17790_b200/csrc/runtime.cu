@@ -55,7 +55,12 @@ struct nsf_mpm {
   uint16_t* W = nullptr;
   float* b = nullptr;
   unsigned int* mlp_ctr = nullptr;   // MLP tile ticket + completion counter (kernels_nsf_tc.cu)
-  MlpDev gdef{};                      // deformation field g (network inversion)
+  MlpDev gdef{};                      // deformation field g (network inversion, inference)
+  MlpDev ldef{};                      // affine-velocity field l (inference)
+  uint16_t* lW = nullptr;
+  float* lb = nullptr;
+  bool ldef_loaded = false;
+  float* zprev = nullptr;             // z_{n-1} of inference (n_scenes x r)
   uint16_t* gW = nullptr;
   float* gb = nullptr;
   bool gdef_loaded = false;
@@ -523,6 +528,205 @@ nsf_status nsf_mpm_load_deformation_field(nsf_mpm* h, int32_t in_dim, int32_t wi
   M.W = h->gW;
   M.b = h->gb;
   h->gdef_loaded = true;
+  return NSF_OK;
+}
+
+nsf_status nsf_mpm_load_affine_field(nsf_mpm* h, int32_t in_dim, int32_t width, int32_t n_hidden,
+                                     int32_t out_dim, const uint16_t* W_bf16, const float* b, int32_t on_device) {
+  if (!h) return NSF_ERR_INVALID_ARGUMENT;
+  if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
+  if (!(in_dim >= 4 && in_dim <= 16) || width != 128 || !(n_hidden >= 1 && n_hidden <= 8) || out_dim != 9)
+    return fail(h, NSF_ERR_INVALID_ARGUMENT, "unsupported affine field (in<=16, width=128, 1<=hidden<=8, out=9)");
+  if (!W_bf16 || !b) return fail(h, NSF_ERR_INVALID_ARGUMENT, "W and b are required");
+  MlpDev& M = h->ldef;
+  M.in_dim = in_dim; M.width = width; M.n_hidden = n_hidden; M.out_dim = out_dim;
+  const int L = n_hidden + 1;
+  int64_t wo = 0, bo = 0;
+  for (int l = 0; l < L; ++l) {
+    const int in = l == 0 ? in_dim : width;
+    const int out = l == L - 1 ? out_dim : width;
+    M.w_off[l] = wo; M.b_off[l] = bo;
+    wo += (int64_t)in * out;
+    bo += out;
+  }
+  M.w_off[L] = wo; M.b_off[L] = bo;
+  M.ctr = nullptr;
+  nsf_status s;
+  CK(cudaStreamSynchronize(h->stream));
+  if ((s = alloc_into(h, &h->lW, sizeof(uint16_t) * wo)) != NSF_OK) return s;
+  if ((s = alloc_into(h, &h->lb, sizeof(float) * bo)) != NSF_OK) return s;
+  if ((s = to_device(h, W_bf16, sizeof(uint16_t) * wo, on_device, h->lW)) != NSF_OK) return s;
+  if ((s = to_device(h, b, sizeof(float) * bo, on_device, h->lb)) != NSF_OK) return s;
+  CK(cudaStreamSynchronize(h->stream));
+  M.W = h->lW;
+  M.b = h->lb;
+  h->ldef_loaded = true;
+  return NSF_OK;
+}
+
+static nsf_status inference_ready(nsf_mpm* h) {
+  if (h->mat.model != NSF_NEURAL_STRESS || !h->loaded || !h->mlp_loaded || !h->latents_loaded || !h->X ||
+      !h->gdef_loaded || !h->ldef_loaded)
+    return fail(h, NSF_ERR_BAD_STATE,
+                "needs the NSF model with load_stress_field(X_ref), set_latents, load_deformation_field, "
+                "load_affine_field");
+  if (h->gdef.in_dim != 3 + h->r || h->ldef.in_dim != 3 + h->r)
+    return fail(h, NSF_ERR_INVALID_ARGUMENT, "g and l inputs must be 3 + r");
+  return NSF_OK;
+}
+
+// x = g(X, z_n), v = (x - g(X, z_prev)) / dt, C = l(X, z_n) on the store
+static nsf_status enqueue_infer(nsf_mpm* h) {
+  if (h->n == 0) return NSF_OK;
+  float* S = h->S[h->cur];
+  const float* Xp = S + PXR * 32;   // the store's reference-position planes (follow the points)
+  const int ns = h->mat.n_scenes, r = h->r;
+  launch_nsf_mlp(h->stream, h->n, Xp, -1, h->scene_off, ns, h->zprev, nullptr, r, nullptr, h->gdef, 1.0f,
+                 S + PV * 32, 0, 0);
+  launch_nsf_mlp(h->stream, h->n, Xp, -1, h->scene_off, ns, h->z, h->dz, r, h->d_step, h->gdef, 1.0f, S + PX * 32,
+                 0, 0);
+  launch_backdiff(h->stream, h->n, S, (float)h->dt);
+  launch_nsf_mlp(h->stream, h->n, Xp, -1, h->scene_off, ns, h->z, h->dz, r, h->d_step, h->ldef, 1.0f, S + PC * 32,
+                 0, 0);
+  CK(cudaGetLastError());
+  return NSF_OK;
+}
+
+static nsf_status set_zprev(nsf_mpm* h, const float* z_prev, int32_t on_device) {
+  const size_t m = (size_t)h->mat.n_scenes * h->r;
+  nsf_status s;
+  if ((s = alloc_into(h, &h->zprev, sizeof(float) * m)) != NSF_OK) return s;
+  if (z_prev) return to_device(h, z_prev, sizeof(float) * m, on_device, h->zprev);
+  launch_latent_at(h->stream, (int64_t)m, h->z, h->dz, h->host_step >= 1 ? h->host_step - 1 : 0, h->zprev);
+  CK(cudaGetLastError());
+  return NSF_OK;
+}
+
+nsf_status nsf_mpm_infer_state(nsf_mpm* h, const float* z_prev, int32_t on_device) {
+  if (!h) return NSF_ERR_INVALID_ARGUMENT;
+  if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
+  nsf_status s;
+  if ((s = inference_ready(h)) != NSF_OK) return s;
+  if ((s = set_zprev(h, z_prev, on_device)) != NSF_OK) return s;
+  return enqueue_infer(h);
+}
+
+nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float* X_all, int32_t n_sample,
+                                         const int32_t* sample_idx, const float* z_prev, int64_t* counts_out,
+                                         int32_t on_device) {
+  if (!h) return NSF_ERR_INVALID_ARGUMENT;
+  if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
+  nsf_status s;
+  if ((s = inference_ready(h)) != NSF_OK) return s;
+  const int ns = h->mat.n_scenes, r = h->r;
+  if (n_ref < 1 || n_ref >= (int64_t(1) << 31) / (ns > 0 ? ns : 1) || !X_all || n_sample < 1 || n_sample > n_ref ||
+      !sample_idx)
+    return fail(h, NSF_ERR_INVALID_ARGUMENT, "1 <= n_sample <= n_ref, n_ref * n_scenes < 2^31, X_all and sample_idx");
+  // sample indices: in range and distinct within a scene (checked on the host)
+  std::vector<int32_t> sidx((size_t)ns * n_sample);
+  if (on_device) CK(cudaMemcpy(sidx.data(), sample_idx, sizeof(int32_t) * sidx.size(), cudaMemcpyDeviceToHost));
+  else memcpy(sidx.data(), sample_idx, sizeof(int32_t) * sidx.size());
+  {
+    std::vector<int32_t> seen((size_t)n_ref, -1);
+    for (int sc = 0; sc < ns; ++sc)
+      for (int q = 0; q < n_sample; ++q) {
+        const int32_t i = sidx[(size_t)sc * n_sample + q];
+        if (i < 0 || i >= n_ref || seen[i] == sc)
+          return fail(h, NSF_ERR_INVALID_ARGUMENT, "sample_idx[%d][%d] out of range or repeated", sc, q);
+        seen[i] = sc;
+      }
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  const int64_t pitch_ref = ((n_ref + 127) / 128) * 128;
+  const int64_t nodes = (int64_t)h->grid_res[0] * h->grid_res[1] * h->grid_res[2];
+  const int64_t nblk = compact_blocks(n_ref);
+  float *Xd = nullptr, *Xpl = nullptr, *xg = nullptr, *zc = nullptr, *Xnew = nullptr, *vzero = nullptr;
+  int32_t *sid = nullptr, *cnt = nullptr, *base = nullptr, *list = nullptr;
+  uint32_t* mask = nullptr;
+  uint8_t *is_s = nullptr, *flag = nullptr;
+  int64_t* offd = nullptr;
+  auto cleanup = [&]() {
+    for (void* p : {(void*)Xd, (void*)Xpl, (void*)xg, (void*)zc, (void*)Xnew, (void*)vzero, (void*)sid, (void*)cnt,
+                    (void*)base, (void*)list, (void*)mask, (void*)is_s, (void*)flag, (void*)offd})
+      dfree(h, p);
+  };
+#define TRY(expr) do { if ((s = (expr)) != NSF_OK) { cleanup(); return s; } } while (0)
+#define TRYCU(expr) do { cudaError_t e_ = (expr); if (e_ != cudaSuccess) { cleanup(); return cuda_fail(h, e_, #expr); } } while (0)
+  TRY(alloc_into(h, &Xd, sizeof(float) * 3 * n_ref));
+  TRY(alloc_into(h, &Xpl, sizeof(float) * 3 * pitch_ref));
+  TRY(alloc_into(h, &xg, sizeof(float) * 3 * n_ref));
+  TRY(alloc_into(h, &zc, sizeof(float) * ns * r));
+  TRY(alloc_into(h, &sid, sizeof(int32_t) * sidx.size()));
+  TRY(alloc_into(h, &cnt, sizeof(int32_t) * nblk));
+  TRY(alloc_into(h, &base, sizeof(int32_t) * nblk));
+  TRY(alloc_into(h, &list, sizeof(int32_t) * (size_t)ns * n_ref));
+  TRY(alloc_into(h, &mask, sizeof(uint32_t) * ((nodes + 31) / 32)));
+  TRY(alloc_into(h, &is_s, (size_t)n_ref));
+  TRY(alloc_into(h, &flag, (size_t)n_ref));
+  TRY(to_device(h, X_all, sizeof(float) * 3 * n_ref, on_device, Xd));
+  TRYCU(cudaMemcpyAsync(sid, sidx.data(), sizeof(int32_t) * sidx.size(), cudaMemcpyHostToDevice, h->stream));
+  pipeline_aos_to_planes(h->stream, n_ref, Xd, 3, Xpl, pitch_ref);
+  launch_latent_at(h->stream, (int64_t)ns * r, h->z, h->dz, h->host_step, zc);   // z_n of the next substep
+  TRYCU(cudaMemsetAsync(is_s, 0, (size_t)n_ref, h->stream));
+  TRY(reset_errors(h));
+  std::vector<int64_t> off(ns + 1, 0), counts(ns);
+  std::vector<int32_t> hc(nblk), hb(nblk);
+  for (int sc = 0; sc < ns; ++sc) {
+    const int32_t* si = sid + (size_t)sc * n_sample;
+    // x = g(X_p, z_n(s)) for the whole reference body
+    launch_nsf_mlp(h->stream, n_ref, Xpl, pitch_ref, nullptr, 1, zc + (size_t)sc * r, nullptr, r, nullptr, h->gdef,
+                   1.0f, xg, 0, 1);
+    TRYCU(cudaMemsetAsync(mask, 0, sizeof(uint32_t) * ((nodes + 31) / 32), h->stream));
+    launch_mark_stencils(h->stream, n_sample, si, xg, mask, h->P, h->err);
+    launch_set_samples(h->stream, n_sample, si, is_s, 1);
+    launch_member_flags(h->stream, n_ref, xg, mask, is_s, flag, h->P);
+    launch_set_samples(h->stream, n_sample, si, is_s, 0);
+    launch_count_blocks(h->stream, n_ref, flag, cnt);
+    TRYCU(cudaGetLastError());
+    TRYCU(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost, h->stream));
+    TRYCU(cudaStreamSynchronize(h->stream));
+    int64_t acc = off[sc] + n_sample;   // S first
+    for (int64_t k = 0; k < nblk; ++k) { hb[k] = (int32_t)acc; acc += hc[k]; }
+    off[sc + 1] = acc;
+    counts[sc] = acc - off[sc];
+    TRYCU(cudaMemcpyAsync(base, hb.data(), sizeof(int32_t) * nblk, cudaMemcpyHostToDevice, h->stream));
+    TRYCU(cudaMemcpyAsync(list + off[sc], si, sizeof(int32_t) * n_sample, cudaMemcpyDeviceToDevice, h->stream));
+    launch_compact(h->stream, n_ref, flag, base, list);
+    TRYCU(cudaGetLastError());
+    TRYCU(cudaStreamSynchronize(h->stream));   // hb is reused by the next scene
+  }
+  TRYCU(cudaMemcpyAsync(h->err_host, h->err, sizeof(DevErr), cudaMemcpyDeviceToHost, h->stream));
+  TRYCU(cudaStreamSynchronize(h->stream));
+  if (h->err_host->bits & ERR_OUT_OF_DOMAIN) {
+    reset_errors(h);
+    cleanup();
+    return fail(h, NSF_ERR_OUT_OF_DOMAIN, "a sample particle's stencil leaves the grid");
+  }
+  const int64_t n_new = off[ns];
+  if (n_new >= (int64_t(1) << 31)) { cleanup(); return fail(h, NSF_ERR_INVALID_ARGUMENT, "integration set too large"); }
+  TRY(alloc_into(h, &Xnew, sizeof(float) * 3 * n_new));
+  TRY(alloc_into(h, &vzero, sizeof(float) * 3 * n_new));
+  TRY(alloc_into(h, &offd, sizeof(int64_t) * (ns + 1)));
+  launch_gather_rows3(h->stream, n_new, list, Xd, Xnew);
+  TRYCU(cudaMemsetAsync(vzero, 0, sizeof(float) * 3 * n_new, h->stream));
+  TRYCU(cudaMemcpyAsync(offd, off.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, h->stream));
+  TRYCU(cudaStreamSynchronize(h->stream));
+  // reload the points (placeholders x = X, v = 0), keeping the step counter (z_n = z + n dz)
+  const int64_t step = h->host_step;
+  TRY(nsf_mpm_load_particles(h, n_new, Xnew, vzero, nullptr, nullptr, offd, 1));
+  h->host_step = step;
+  TRYCU(cudaMemcpyAsync(h->d_step, &h->host_step, sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+  TRY(alloc_into(h, &h->X, sizeof(float) * 3 * h->pitch));
+  pipeline_aos_to_planes(h->stream, n_new, Xnew, 3, h->X, h->pitch);
+  pipeline_on_mlp(h, &h->pb);
+  invalidate_graph(h);
+  TRY(set_zprev(h, z_prev, on_device));
+  TRY(enqueue_infer(h));
+  TRYCU(cudaStreamSynchronize(h->stream));
+  if (counts_out) memcpy(counts_out, counts.data(), sizeof(int64_t) * ns);
+  cleanup();
+#undef TRY
+#undef TRYCU
   return NSF_OK;
 }
 

@@ -284,6 +284,40 @@ def deformation_field(seed: int = SEEDS["C5"] + 1000, r: int = 6, width: int = 1
     return g
 
 
+def deformation_field_near_identity(seed: int = SEEDS["C5"] + 3000, r: int = 6, width: int = 128,
+                                    n_hidden: int = 4, eps: float = 0.03) -> dict:
+    """A random-init deformation field that stays close to the identity, g(X, z) ~ r(X) +
+    eps * (random smooth function of X and z), r() = bf16 rounding: hidden units 0..2
+    carry X_a through every layer (weight 1, bias 0; X > 0 so ELU is the identity) and
+    the output adds eps x reading #20's random output layer (weights rounded to bf16).
+    A stand-in for a trained g whose body is not collapsed, for the integration-set
+    construction."""
+    g = xavier_bf16_mlp(np.random.default_rng(seed), [3 + r] + [width] * n_hidden + [3])
+    L = len(g["W"])
+    for k in range(L):
+        W = g["W"][k].copy()
+        b = g["b"][k].copy()
+        if k == 0:
+            W[:3, :] = 0.0
+            W[:3, :3] = np.eye(3, dtype=np.float32)
+            b[:3] = 0.0
+        elif k < L - 1:
+            W[:3, :] = 0.0
+            W[:, :3] = 0.0
+            W[:3, :3] = np.eye(3, dtype=np.float32)
+            b[:3] = 0.0
+        else:
+            W = W * np.float32(eps)
+            W[:, :3] = np.eye(3, dtype=np.float32)
+            b[:] = 0.0
+        bits = W.astype(np.float32).view(np.uint32)
+        rounded = (bits + np.uint32(0x7FFF) + ((bits >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)
+        g["W_bits"][k] = rounded.astype(np.uint16)
+        g["W"][k] = (g["W_bits"][k].astype(np.uint32) << np.uint32(16)).view(np.float32)
+        g["b"][k] = b.astype(np.float32)
+    return g
+
+
 def affine_field(seed: int = SEEDS["C5"] + 2000, r: int = 6, width: int = 128, n_hidden: int = 4) -> dict:
     """Random-init neural affine-velocity field l(X, z) -> C (9, row-major; PAPER.md
     line 253), reading #20's initialisation with the output layer scaled by 1/16 and
