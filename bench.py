@@ -340,7 +340,7 @@ def run_ours(args):
     step_gbs = B_ALG_PER_PARTICLE_SUBSTEP * n / (ms / args.steps * 1e-3) / 1e9
 
     # ---- C5: network inversion (Eq. (10)), 3 Gauss-Newton iterations over 64 samples per scene ----
-    inversion = None
+    inversion = inference = integration = None
     if args.config == "C5":
         import scenes as _sc
         g = _sc.deformation_field()
@@ -367,6 +367,49 @@ def run_ours(args):
                      "note": "per call: sample collection, 3 x (tensor-core forward + 6 tangents, fp64 normal "
                              "equations, per-scene Cholesky), latent update; host-synchronous API call"}
         nsf.nsf_mpm_set_latents(sim.h, dims[0] - 3, sc.z0, sc.dz)   # back to the scene's latents
+
+        # ---- C5: network inference for every point: x = g(X, z_n), g(X, z_{n-1}),
+        #      v by backward difference, C = l(X, z_n) ----
+        lnet = _sc.affine_field()
+        sim.load_affine_field(lnet)
+        sim.infer_state(None)
+        sim.sync()
+        ia.record(stream)
+        for _ in range(reps):
+            sim.infer_state(None)
+        ib.record(stream)
+        ib.synchronize()
+        inf_ms = ia.elapsed_time(ib) / reps
+        ldims = lnet["dims"]
+        row_flop_l = 2.0 * sum(a_ * b_ for a_, b_ in zip(ldims[:-1], ldims[1:]))
+        inf_flop = (2 * row_flop + row_flop_l) * n
+        inference = {"points": n, "ms": inf_ms, "flop": inf_flop,
+                     "achieved_tflops": inf_flop / (inf_ms * 1e-3) / 1e12,
+                     "note": "3 MLP passes over the store on tensor cores (g twice, l with 9 outputs) "
+                             "+ the backward difference; asynchronous API call, device-timed"}
+        # ---- C5: sample / integration sets on a second handle: the 200k-point
+        #      reference body, 64 samples per scene, near-identity stand-in g ----
+        isc = _sc.c5()
+        h2 = nsf.Simulator(isc.cfg, stream=stream.cuda_stream)
+        h2.load_scene(isc)
+        h2.load_deformation_field(_sc.deformation_field_near_identity())
+        h2.load_affine_field(lnet)
+        X_all = _sc.reference_body().astype(np.float32)
+        rs = np.random.default_rng(17795)
+        sidx = np.stack([rs.choice(X_all.shape[0], 64, replace=False)
+                         for _ in range(isc.cfg.n_scenes)]).astype(np.int32)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        counts = h2.build_integration_set(X_all, sidx)
+        h2.sync()
+        build_s = time.perf_counter() - t0
+        integration = {"n_ref": int(X_all.shape[0]), "n_sample_per_scene": 64, "scenes": int(isc.cfg.n_scenes),
+                       "points_after": int(counts.sum()), "mean_N_per_scene": float(counts.mean()),
+                       "ms": build_s * 1e3,
+                       "g_rows": int(X_all.shape[0]) * int(isc.cfg.n_scenes),
+                       "note": "host-timed synchronous call: g over the reference body per scene (tensor cores), "
+                               "stencil bit masks, index-ordered compaction, reload, inference on N"}
+        h2.close()
 
     # ---- end to end through the public API with host buffers ----
     pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(sc, k))).pin_memory() for k in ("x", "v", "C", "F")}
@@ -427,6 +470,10 @@ def run_ours(args):
         }
         if inversion is not None:
             line["inversion"] = inversion
+        if inference is not None:
+            line["inference"] = inference
+        if integration is not None:
+            line["integration_set"] = integration
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

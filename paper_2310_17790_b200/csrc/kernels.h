@@ -69,6 +69,10 @@ void launch_set_samples(cudaStream_t st, int n_sample, const int32_t* idx, uint8
 int64_t compact_blocks(int64_t n);
 void launch_count_blocks(cudaStream_t st, int64_t n, const uint8_t* flag, int32_t* cnt);
 void launch_compact(cudaStream_t st, int64_t n, const uint8_t* flag, const int32_t* base, int32_t* out);
+void launch_scene_scan(cudaStream_t st, int64_t nblk, const int32_t* cnt, int n_sample, int64_t* cursor,
+                       int32_t* base, int64_t* scene_count, int scene, int64_t* sample_base);
+void launch_put_samples(cudaStream_t st, int n_sample, const int32_t* idx, const int64_t* sample_base,
+                        int32_t* list);
 void launch_gather_rows3(cudaStream_t st, int64_t m, const int32_t* list, const float* X_all, float* X_new);
 
 }  // namespace nsf

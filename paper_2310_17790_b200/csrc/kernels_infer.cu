@@ -7,8 +7,9 @@
 //   sets  : per scene, I = stencil nodes of the samples' g(X_S, z_n) as a bit
 //           mask over the scene's grid (k_mark_stencils); N = reference points whose
 //           stencil at g(X_p, z_n) hits I, minus S (k_member_flags), compacted in
-//           index order (k_compact_block + a host-side block scan: the order is
-//           deterministic); the new points are S then N \ S.
+//           index order (k_count_block, k_scene_scan, k_compact_block: the order
+//           is deterministic, offsets carried on the device across scenes); the
+//           new points are S then N \ S.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "kernels.h"
@@ -121,6 +122,63 @@ __global__ void __launch_bounds__(kCompactBlock) k_compact_block(int64_t n, cons
   int off = 0;
   for (int w = 0; w < warp; ++w) off += wsum[w];
   if (f) out[base[blockIdx.x] + off + __popc(bal & ((1u << lane) - 1))] = (int32_t)p;
+}
+
+// per scene, on the device (no host round trip): the scene's points start at *cursor
+// (samples first), the flagged points of block k at base[k]; *cursor advances by
+// the scene's count, which is also written to scene_count[scene]
+__global__ void __launch_bounds__(kCompactBlock) k_scene_scan(int64_t nblk, const int32_t* __restrict__ cnt,
+                                                              int n_sample, int64_t* __restrict__ cursor,
+                                                              int32_t* __restrict__ base,
+                                                              int64_t* __restrict__ scene_count, int scene,
+                                                              int64_t* __restrict__ sample_base) {
+  __shared__ int64_t carry;
+  __shared__ int64_t wsum[kCompactBlock / 32];
+  const int64_t c0 = *cursor;
+  if (threadIdx.x == 0) carry = c0 + n_sample;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t k0 = 0; k0 < nblk; k0 += kCompactBlock) {
+    const int64_t k = k0 + threadIdx.x;
+    const int64_t c = k < nblk ? cnt[k] : 0;
+    int64_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int64_t woff = 0;
+    for (int w = 0; w < warp; ++w) woff += wsum[w];
+    if (k < nblk) base[k] = (int32_t)(carry + woff + incl - c);
+    __syncthreads();
+    if (threadIdx.x == kCompactBlock - 1) carry += woff + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    scene_count[scene] = carry - c0;
+    *sample_base = c0;
+    *cursor = carry;
+  }
+}
+
+// list[*sample_base + q] = sample_idx[q]
+__global__ void k_put_samples(int n_sample, const int32_t* __restrict__ idx, const int64_t* __restrict__ sample_base,
+                              int32_t* __restrict__ list) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n_sample) list[*sample_base + q] = idx[q];
+}
+
+void launch_scene_scan(cudaStream_t st, int64_t nblk, const int32_t* cnt, int n_sample, int64_t* cursor,
+                       int32_t* base, int64_t* scene_count, int scene, int64_t* sample_base) {
+  k_scene_scan<<<1, kCompactBlock, 0, st>>>(nblk, cnt, n_sample, cursor, base, scene_count, scene, sample_base);
+}
+
+void launch_put_samples(cudaStream_t st, int n_sample, const int32_t* idx, const int64_t* sample_base,
+                        int32_t* list) {
+  if (n_sample <= 0) return;
+  k_put_samples<<<(n_sample + 127) / 128, 128, 0, st>>>(n_sample, idx, sample_base, list);
 }
 
 // X_new[j] = X_all[list[j]] (AoS 3)

@@ -213,6 +213,7 @@ __device__ __forceinline__ void store_act32(uint32_t tile, int row, int c0, cons
 
 using namespace tc;
 
+template <bool WIDE>   // WIDE: out_dim in (8, 16] (the affine-velocity field), a second TMEM load
 __global__ void __launch_bounds__(kThreads, 1)
 k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64_t* __restrict__ scene_off,
              int n_scenes, const float* __restrict__ z, const float* __restrict__ dz, int r,
@@ -465,6 +466,16 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
         else tau_out[pbase(p) + o * 32] = tau[o];   // AoSoA particle store (tau fields)
       }
       if (q.enabled) nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);   // reduced P2G, tau from registers
+    }
+    if (WIDE) {   // outputs 8..15 (the affine-velocity field l has 9; tcgen05.ld is warp-collective)
+      float y2[8];
+      tmem_ld8(o_col + lane_sel + 8, y2);
+      if (live)
+        for (int o = 8; o < mlp.out_dim; ++o) {
+          const float val = stress_scale * (y2[o - 8] + sm.bout[o]);
+          if (aos_out) tau_out[p * mlp.out_dim + o] = val;
+          else tau_out[pbase(p) + o * 32] = val;
+        }
     }
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile
@@ -752,7 +763,7 @@ void launch_gn_tc(cudaStream_t st, int n_scenes, int n_sample, int r, const int3
 
 bool nsf_mlp_tc_supported(const MlpDev& mlp) {
   return mlp.width == kW && mlp.n_hidden >= 2 && mlp.n_hidden - 1 <= kMaxHiddenMMA && mlp.in_dim <= 14 &&
-         mlp.out_dim <= 8;
+         mlp.out_dim <= kOutN;
 }
 
 void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
@@ -768,14 +779,19 @@ void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitc
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_nsf_mlp_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_nsf_mlp_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_nsf_mlp_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const int64_t tiles = (n + kM - 1) / kM;
   int64_t grid = (tiles + kStreams - 1) / kStreams;
   if (grid > n_sms) grid = n_sms;
-  k_nsf_mlp_tc<<<(unsigned)grid, kThreads, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step, mlp,
-                                                       stress_scale, tau_out, aos_out, q);
+  if (mlp.out_dim > 8)
+    k_nsf_mlp_tc<true><<<(unsigned)grid, kThreads, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step,
+                                                               mlp, stress_scale, tau_out, aos_out, q);
+  else
+    k_nsf_mlp_tc<false><<<(unsigned)grid, kThreads, smem, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r, d_step,
+                                                                mlp, stress_scale, tau_out, aos_out, q);
 }
 
 }  // namespace nsf

@@ -645,9 +645,10 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
   uint32_t* mask = nullptr;
   uint8_t *is_s = nullptr, *flag = nullptr;
   int64_t* offd = nullptr;
+  int64_t* ctr = nullptr;   // [0] cursor, [1] sample base, [2..] per-scene counts
   auto cleanup = [&]() {
     for (void* p : {(void*)Xd, (void*)Xpl, (void*)xg, (void*)zc, (void*)Xnew, (void*)vzero, (void*)sid, (void*)cnt,
-                    (void*)base, (void*)list, (void*)mask, (void*)is_s, (void*)flag, (void*)offd})
+                    (void*)base, (void*)list, (void*)mask, (void*)is_s, (void*)flag, (void*)offd, (void*)ctr})
       dfree(h, p);
   };
 #define TRY(expr) do { if ((s = (expr)) != NSF_OK) { cleanup(); return s; } } while (0)
@@ -663,6 +664,7 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
   TRY(alloc_into(h, &mask, sizeof(uint32_t) * ((nodes + 31) / 32)));
   TRY(alloc_into(h, &is_s, (size_t)n_ref));
   TRY(alloc_into(h, &flag, (size_t)n_ref));
+  TRY(alloc_into(h, &ctr, sizeof(int64_t) * (2 + ns)));
   TRY(to_device(h, X_all, sizeof(float) * 3 * n_ref, on_device, Xd));
   TRYCU(cudaMemcpyAsync(sid, sidx.data(), sizeof(int32_t) * sidx.size(), cudaMemcpyHostToDevice, h->stream));
   pipeline_aos_to_planes(h->stream, n_ref, Xd, 3, Xpl, pitch_ref);
@@ -670,7 +672,8 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
   TRYCU(cudaMemsetAsync(is_s, 0, (size_t)n_ref, h->stream));
   TRY(reset_errors(h));
   std::vector<int64_t> off(ns + 1, 0), counts(ns);
-  std::vector<int32_t> hc(nblk), hb(nblk);
+  TRYCU(cudaMemsetAsync(ctr, 0, sizeof(int64_t) * (2 + ns), h->stream));
+  // all scenes enqueued back to back; offsets are carried on the device (k_scene_scan)
   for (int sc = 0; sc < ns; ++sc) {
     const int32_t* si = sid + (size_t)sc * n_sample;
     // x = g(X_p, z_n(s)) for the whole reference body
@@ -682,19 +685,14 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
     launch_member_flags(h->stream, n_ref, xg, mask, is_s, flag, h->P);
     launch_set_samples(h->stream, n_sample, si, is_s, 0);
     launch_count_blocks(h->stream, n_ref, flag, cnt);
-    TRYCU(cudaGetLastError());
-    TRYCU(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost, h->stream));
-    TRYCU(cudaStreamSynchronize(h->stream));
-    int64_t acc = off[sc] + n_sample;   // S first
-    for (int64_t k = 0; k < nblk; ++k) { hb[k] = (int32_t)acc; acc += hc[k]; }
-    off[sc + 1] = acc;
-    counts[sc] = acc - off[sc];
-    TRYCU(cudaMemcpyAsync(base, hb.data(), sizeof(int32_t) * nblk, cudaMemcpyHostToDevice, h->stream));
-    TRYCU(cudaMemcpyAsync(list + off[sc], si, sizeof(int32_t) * n_sample, cudaMemcpyDeviceToDevice, h->stream));
+    launch_scene_scan(h->stream, nblk, cnt, n_sample, ctr, base, ctr + 2, sc, ctr + 1);
+    launch_put_samples(h->stream, n_sample, si, ctr + 1, list);
     launch_compact(h->stream, n_ref, flag, base, list);
     TRYCU(cudaGetLastError());
-    TRYCU(cudaStreamSynchronize(h->stream));   // hb is reused by the next scene
   }
+  TRYCU(cudaMemcpyAsync(counts.data(), ctr + 2, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, h->stream));
+  TRYCU(cudaStreamSynchronize(h->stream));
+  for (int sc = 0; sc < ns; ++sc) off[sc + 1] = off[sc] + counts[sc];
   TRYCU(cudaMemcpyAsync(h->err_host, h->err, sizeof(DevErr), cudaMemcpyDeviceToHost, h->stream));
   TRYCU(cudaStreamSynchronize(h->stream));
   if (h->err_host->bits & ERR_OUT_OF_DOMAIN) {
