@@ -956,12 +956,29 @@ __device__ __forceinline__ void p2g_accumulate_rows(const float4* slot, int my_c
 // segment's velocity tile (global gather if the stencil left it), x/v/C/F/tau
 // updated in place, and the new state returned for the next substep's P2G.
 // P2G-only launches (DO_G2P = false) just read the state.
+#ifndef NSF_STREAM_HINTS
+#define NSF_STREAM_HINTS 0   // particle state read / written with evict-first cache hints (.cs)
+#endif
+__device__ __forceinline__ float ld_state(const float* p) {
+#if NSF_STREAM_HINTS
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ void st_state(float* p, float v) {
+#if NSF_STREAM_HINTS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
 __device__ __forceinline__ void load_xF(const float* __restrict__ S, int j, float x[3], float F[9]) {
   const float* base = S + pbase(j);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) x[a] = base[(PX + a) * 32];
+  for (int a = 0; a < 3; ++a) x[a] = ld_state(base + (PX + a) * 32);
 #pragma unroll
-  for (int k = 0; k < 9; ++k) F[k] = base[(PF + k) * 32];
+  for (int k = 0; k < 9; ++k) F[k] = ld_state(base + (PF + k) * 32);
 }
 
 template <bool DO_G2P, bool HS>
@@ -996,11 +1013,11 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       xn[a] = x[a] + P.dt * vn[a];
       const float tt = xn[a] * P.inv_dx;
       ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
-      base[(PX + a) * 32] = xn[a];
-      base[(PV + a) * 32] = vn[a];
+      st_state(base + (PX + a) * 32, xn[a]);
+      st_state(base + (PV + a) * 32, vn[a]);
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) base[(PC + k) * 32] = Cn[k];
+    for (int k = 0; k < 9; ++k) st_state(base + (PC + k) * 32, Cn[k]);
     float Ft[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -1019,9 +1036,9 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
     }
     float chk = xn[0] + xn[1] + xn[2] + vn[0] + vn[1] + vn[2];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) { base[(PF + k) * 32] = FE[k]; chk += FE[k]; }
+    for (int k = 0; k < 9; ++k) { st_state(base + (PF + k) * 32, FE[k]); chk += FE[k]; }
 #pragma unroll
-    for (int k = 0; k < 6; ++k) { base[(PT + k) * 32] = tau[k]; chk += tau[k]; }
+    for (int k = 0; k < 6; ++k) { st_state(base + (PT + k) * 32, tau[k]); chk += tau[k]; }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
     if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, j); }
     if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, j); }
@@ -1339,9 +1356,12 @@ void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, flo
   }
 }
 
+#ifndef NSF_GU_CTAS_PER_SM
+#define NSF_GU_CTAS_PER_SM 8
+#endif
 void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
                               const int64_t* d_step) {
-  const int grid = num_sms() * 8;
+  const int grid = num_sms() * NSF_GU_CTAS_PER_SM;
   k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks,
                                            pb->touched + pb->total_blocks + 1, acc, vel, P, d_step, pb->n_nonempty);
 }
