@@ -83,3 +83,38 @@ def test_full_size_sampled_substep(nsf, name, k):
     got = _state(s1, samples)
     errs = compare(got, ref_s, cfg)
     assert all(e <= BAR_STEP for e in errs.values()), (name, len(samples), errs)
+
+
+def test_full_size_sampled_substep_vm_hardening(nsf):
+    """C3 at full size with a per-particle yield stress (the HS instantiation
+    of the fused kernel): a low yield stress so that particles under the plate
+    yield within 33 substeps; tau_Y is part of the compared state."""
+    sc = scenes.by_name("C3")
+    cfg = sc.cfg
+    cfg.yield_stress, cfg.hardening, cfg.softening = 2e3, 0.5, 1e5
+    k = 33
+    sim = nsf.Simulator(cfg)
+    sim.load_scene(sc)
+    mask = (nsf.NSF_FIELD_X | nsf.NSF_FIELD_V | nsf.NSF_FIELD_C | nsf.NSF_FIELD_F | nsf.NSF_FIELD_TAU
+            | nsf.NSF_FIELD_TAU_Y)
+    sim.substep(k)
+    s0 = sim.read(mask)
+    sim.substep(1)
+    sim.sync()
+    s1 = sim.read(mask)
+    sim.close()
+    rng = np.random.default_rng(20231028)
+    samples, support = _sample_and_support(s0["x"], float(cfg.grid_res), cfg.grid_res, rng)
+    P = mpm.params_from_config(cfg)
+    st = _state(s0, support)
+    st["tau_Y"] = np.asarray(s0["tau_Y"][support], np.float64)
+    ref = mpm.substep(st, P, k)
+    pos = np.searchsorted(support, samples)
+    ref_s = {f: ref[f][pos] for f in FIELDS}
+    got = _state(s1, samples)
+    errs = compare(got, ref_s, cfg)
+    ty_ref, ty_got = ref["tau_Y"][pos], np.asarray(s1["tau_Y"][samples], np.float64)
+    errs["tau_Y"] = float(np.linalg.norm(ty_got - ty_ref) / np.linalg.norm(ty_ref))
+    assert all(e <= BAR_STEP for e in errs.values()), (len(samples), errs)
+    # the law acted somewhere in the body
+    assert np.any(s1["tau_Y"] != np.float32(cfg.yield_stress))
