@@ -808,6 +808,9 @@ constexpr int kRowsF = NSF_DENSE_ROWS;         // dense variant: staged rows per
 // scattered node-parallel in phase 2, by the warps that do not accumulate (NT >
 // 192) or by all threads before accumulating; only list overflow is scattered
 // inline (warp-cooperatively), which stalls its warp on the block-flag loads.
+#ifndef NSF_PF_NEXT
+#define NSF_PF_NEXT 1                          // phase 1 loads the next particle's x, F a pass ahead
+#endif
 #ifndef NSF_SCATTER_CAP
 #define NSF_SCATTER_CAP 40
 #endif
@@ -1124,8 +1127,23 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     // ---- phase 1: per particle ----
     for (int j = s0 + tid; j < s1; j += NT) {
       float xn[3], vn[3], Cn[9], tau[6];
+#if NSF_PF_NEXT
+      // the next particle's x, F load under this one's G2P (needs the registers of
+      // 2 CTAs per SM)
+      float x1[3], F1[9];
+      if (DO_G2P && j + NT < s1) load_xF(S, j + NT, x1, F1);
+#else
       if (DO_G2P && j != s0 + tid) load_xF(S, j, x0, F0);
+#endif
       fused_g2p_particle<DO_G2P, HS>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
+#if NSF_PF_NEXT
+      if (DO_G2P && j + NT < s1) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) x0[a] = x1[a];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) F0[k] = F1[k];
+      }
+#endif
       // ---- P2G of the new state: by cell if still inside this block, else direct ----
       int c[3];
       bool core = true;
@@ -1345,6 +1363,10 @@ void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, flo
   if (do_g2p && P.vm_hs) {   // von Mises with a per-particle yield stress
     if (pb->sparse) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192, true>(st, S, vel, acc, pb, P, err, d_step);
     else launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS, true>(st, S, vel, acc, pb, P, err, d_step);
+    return;
+  }
+  if (do_g2p && pb->dense2) {   // dense, 2 CTAs per SM
+    launch_g2p2g_t<true, kRowsF, 2, NSF_DENSE_THREADS>(st, S, vel, acc, pb, P, err, d_step);
     return;
   }
   if (pb->sparse) {

@@ -161,15 +161,20 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     v = view(h);
     if (cudaMemsetAsync(pb->n_nonempty + 3, 0, sizeof(int32_t), v.stream) != cudaSuccess) return NSF_ERR_CUDA;
     // kernel variant by density: fewer staged rows and more CTAs per SM when the
-    // non-empty blocks hold few particles (NSF_FUSED_VARIANT=dense|sparse overrides)
+    // non-empty blocks hold few particles; among dense scenes, 2 CTAs per SM (more
+    // registers per thread) when there are fewer than 2 segments per CTA of the
+    // 3-per-SM variant (NSF_FUSED_VARIANT=dense|dense2|sparse overrides)
     int32_t nblk = 0;
     if (cudaMemcpyAsync(&nblk, pb->n_nonempty, sizeof(int32_t), cudaMemcpyDeviceToHost, v.stream) != cudaSuccess ||
         cudaStreamSynchronize(v.stream) != cudaSuccess)
       return NSF_ERR_CUDA;
     const char* fv = getenv("NSF_FUSED_VARIANT");
-    if (fv && strcmp(fv, "dense") == 0) pb->sparse = false;
+    if (fv && strncmp(fv, "dense", 5) == 0) pb->sparse = false;
     else if (fv && strcmp(fv, "sparse") == 0) pb->sparse = true;
     else pb->sparse = nblk > 0 && v.n < (int64_t)kSparseParticlesPerBlock * nblk;
+    if (fv && strcmp(fv, "dense2") == 0) pb->dense2 = true;
+    else if (fv) pb->dense2 = false;
+    else pb->dense2 = !pb->sparse && nblk < 2 * 3 * num_sms();
     launch_g2p2g(v.stream, false, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step);   // P2G of state 0
   } else if (pb->tiled) {
     launch_keys_hist(v.stream, v.n, v.S[0], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
