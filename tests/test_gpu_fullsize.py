@@ -61,13 +61,13 @@ def _state(st, idx):
     return out
 
 
-@pytest.mark.parametrize("name,k", [("C2", 33), ("C3", 33), ("C4", 33)])
+@pytest.mark.parametrize("name,k", [("C2", 129), ("C3", 129), ("C4", 33), ("C4", 129)])
 def test_full_size_sampled_substep(nsf, name, k):
     sc = scenes.by_name(name)
     cfg = sc.cfg
     sim = nsf.Simulator(cfg)
     sim.load_scene(sc)
-    sim.substep(k)                     # crosses a re-binning (every 32 substeps)
+    sim.substep(k)                     # crosses a re-binning (every 32, 64 or 128 substeps by speed)
     s0 = sim.read()
     sim.substep(1)
     sim.sync()
@@ -88,11 +88,11 @@ def test_full_size_sampled_substep(nsf, name, k):
 def test_full_size_sampled_substep_vm_hardening(nsf):
     """C3 at full size with a per-particle yield stress (the HS instantiation
     of the fused kernel): a low yield stress so that particles under the plate
-    yield within 33 substeps; tau_Y is part of the compared state."""
+    yield within 129 substeps; tau_Y is part of the compared state."""
     sc = scenes.by_name("C3")
     cfg = sc.cfg
     cfg.yield_stress, cfg.hardening, cfg.softening = 2e3, 0.5, 1e5
-    k = 33
+    k = 129
     sim = nsf.Simulator(cfg)
     sim.load_scene(sc)
     mask = (nsf.NSF_FIELD_X | nsf.NSF_FIELD_V | nsf.NSF_FIELD_C | nsf.NSF_FIELD_F | nsf.NSF_FIELD_TAU
