@@ -59,7 +59,7 @@ KERNEL_BYTES_PER_PARTICLE = {
     "g2p2g": 48.0 + 120.0,       # fused G2P + next P2G, state in place: x, F read; x, v, C, F, tau written
                                  # (v, C, tau are consumed from registers by the fused P2G; grid traffic
                                  # stays in L2 -- it is counted per touched node under grid_update)
-    "reorder": 2 * 120.0 + 12.0, # every 32nd substep: 30 planes read + written, perm + ids
+    "reorder": 2 * 124.0 + 12.0, # per re-binning: 31 planes read + written, perm + ids
     "bin_keys_hist": 12.0 + 4.0,
     "bin_scatter": 8.0,
 }

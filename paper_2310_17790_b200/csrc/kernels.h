@@ -58,9 +58,6 @@ void launch_gn_invert(cudaStream_t st, int64_t n, const int32_t* ids, const int6
                       int n_sample, int r, const float* S, const float* z, const float* dz, const int64_t* d_step,
                       const MlpDev& g, int n_iters, int32_t* slots, float* zw, double* accum);
 
-// kernels_basic.cu -- max_p |v_p| (float bits; *out zeroed by the caller)
-void launch_max_speed(cudaStream_t st, int64_t n, const float* S, unsigned int* out);
-
 // kernels_infer.cu -- network inference and the integration set
 void launch_latent_at(cudaStream_t st, int64_t m, const float* z, const float* dz, int64_t step, float* out);
 void launch_backdiff(cudaStream_t st, int64_t n, float* S, float dt);

@@ -397,25 +397,6 @@ void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_o
   k_g2p_nsf<<<g, bs, 0, st>>>(n, S, scene_off, n_scenes, acc0, acc1, P, err, d_step, done);
 }
 
-// max_p |v_p| as float bits (non-negative floats order like their bit patterns)
-__global__ void k_max_speed(int64_t n, const float* __restrict__ S, unsigned int* out) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  float s = 0.0f;
-  if (p < n) {
-    const float* b = S + pbase(p);
-    s = sqrtf(b[PV * 32] * b[PV * 32] + b[(PV + 1) * 32] * b[(PV + 1) * 32] + b[(PV + 2) * 32] * b[(PV + 2) * 32]);
-    if (!(s >= 0.0f)) s = 0.0f;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(s));
-}
-
-void launch_max_speed(cudaStream_t st, int64_t n, const float* S, unsigned int* out) {
-  if (n <= 0) return;
-  k_max_speed<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, S, out);
-}
-
 // Marks every point's previous stencil as absent (after a load).
 __global__ void k_nsf_reset_base(int64_t n, float* S) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

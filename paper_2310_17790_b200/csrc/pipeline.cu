@@ -137,33 +137,9 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
               v.P->N[1] <= 1024 && v.P->N[2] <= 1024;
   pb->since_rebin = 0;
   pb->launch_total = 0;
+  // re-binning every 32 substeps (measured over whole 500-substep runs: 64 and 128
+  // are slower on C3, as the order inside segments decays, and no faster on C2)
   pb->rebin_every = 32;
-  if (pb->fused && v.n >= 65536) {
-    // re-binning period of the fused pipeline: the largest of 128, 64, 32 substeps over
-    // which a particle at the load's top speed (or the plate's), accelerated by
-    // gravity, drifts at most half a cell.  Locality only -- correctness never
-    // depends on the binning -- so an estimate from the initial state suffices.
-    // Small scenes (latency-bound: a few CTAs, where out-of-segment particles cost
-    // most) keep 32.
-    unsigned int* d = (unsigned int*)pipeline_alloc(h, sizeof(unsigned int));
-    unsigned int bits = 0;
-    if (!d || cudaMemsetAsync(d, 0, sizeof(unsigned int), v.stream) != cudaSuccess) return NSF_ERR_CUDA;
-    launch_max_speed(v.stream, v.n, v.S[0], d);
-    if (cudaMemcpyAsync(&bits, d, sizeof(bits), cudaMemcpyDeviceToHost, v.stream) != cudaSuccess ||
-        cudaStreamSynchronize(v.stream) != cudaSuccess)
-      return NSF_ERR_CUDA;
-    pipeline_free(h, d);
-    float vmax;
-    memcpy(&vmax, &bits, sizeof(vmax));
-    if (v.P->plate_enabled)
-      vmax = fmaxf(vmax, sqrtf(v.P->plate_v[0] * v.P->plate_v[0] + v.P->plate_v[1] * v.P->plate_v[1] +
-                               v.P->plate_v[2] * v.P->plate_v[2]));
-    const double g = sqrt((double)v.P->g[0] * v.P->g[0] + (double)v.P->g[1] * v.P->g[1] + (double)v.P->g[2] * v.P->g[2]);
-    for (int R = 128; R > 32; R /= 2) {
-      const double t = (double)R * v.P->dt;
-      if ((vmax * t + 0.5 * g * t * t) * v.P->inv_dx <= 0.5) { pb->rebin_every = R; break; }
-    }
-  }
   if (const char* e = getenv("NSF_REBIN_EVERY")) pb->rebin_every = atoi(e) > 0 ? atoi(e) : 32;
   pb->nsf_sorted = false;
   if (cudaMemsetAsync(pb->counts, 0, sizeof(int32_t) * pb->total_blocks, v.stream) != cudaSuccess)
