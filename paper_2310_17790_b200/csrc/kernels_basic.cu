@@ -279,6 +279,18 @@ void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, cons
 // clears the point's previous stencil in acc[(step + 1) & 1] and records the
 // current base.  The last CTA advances the step counter (every thread reads it
 // first).
+// 256-bit global accesses (sm_100): a node pair at an even node index is 32-byte
+// aligned (the accumulators come from cudaMalloc / the torch allocator, >= 256 B
+// aligned; scenes start at multiples of 64 nodes)
+__device__ __forceinline__ void ld_nc8(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void st_zero8(float4* p) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "f"(0.0f) : "memory");
+}
+
 #ifndef NSF_G2P_NSF_MINB
 #define NSF_G2P_NSF_MINB 6   // 80 registers: 24 warps per SM for the gather latency (C5 -2.4%)
 #endif
@@ -310,12 +322,17 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
       const int pb_[3] = {packed >> 20, (packed >> 10) & 1023, packed & 1023};
       stencil_offsets(pb_, P, X, Y, Z);
       float4* clr = ((step & 1) ? acc0 : acc1) + so;
+      // each z-run of 3 nodes as a 32-byte pair at an even node index plus one node
+      const int zp = pb_[2] & 1;
+      const int zpair = zp ? Z[1] : Z[0], zone = zp ? Z[0] : Z[2];
 #pragma unroll
       for (int a = 0; a < 3; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) clr[X[a] + Y[b] + Z[c]] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int b = 0; b < 3; ++b) {
+          float4* r = clr + (X[a] + Y[b]);
+          st_zero8(r + zpair);
+          r[zone] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
     stencil_offsets(base, P, X, Y, Z);
     const float4* ab = ((step & 1) ? acc1 : acc0) + so;
@@ -329,29 +346,45 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
     }
     float v[3] = {0.f, 0.f, 0.f};
     float Bm[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    auto accumulate = [&](int a, int b, int c, float4 vi) {
-      const float W = ax[0].w[a] * ax[1].w[b] * ax[2].w[c];
-      const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = ((float)c - ax[2].f) * P.dx;
+    auto accumulate_w = [&](float W, float d0, float d1, float d2, float4 vi) {
       const float wv0 = W * vi.x, wv1 = W * vi.y, wv2 = W * vi.z;
       v[0] += wv0; v[1] += wv1; v[2] += wv2;
       Bm[0] += wv0 * d0; Bm[1] += wv0 * d1; Bm[2] += wv0 * d2;
       Bm[3] += wv1 * d0; Bm[4] += wv1 * d1; Bm[5] += wv1 * d2;
       Bm[6] += wv2 * d0; Bm[7] += wv2 * d1; Bm[8] += wv2 * d2;
     };
+    auto accumulate = [&](int a, int b, int c, float4 vi) {
+      accumulate_w(ax[0].w[a] * ax[1].w[b] * ax[2].w[c], ((float)a - ax[0].f) * P.dx, ((float)b - ax[1].f) * P.dx,
+                   ((float)c - ax[2].f) * P.dx, vi);
+    };
     if (simple) {
       const float gx = P.dt * P.g[0], gy = P.dt * P.g[1], gz = P.dt * P.g[2];
+      // z-runs as a 32-byte pair at an even node index (c = zp, zp + 1) plus one
+      // node (c = zp ? 0 : 2): 6 loads per x-plane; the z weights and offsets
+      // follow that order (slot s holds c = zc[s])
+      const int zp = base[2] & 1;
+      const int zpair = zp ? Z[1] : Z[0], zone = zp ? Z[0] : Z[2];
+      const float zc[3] = {(float)zp, (float)(zp + 1), zp ? 0.0f : 2.0f};
+      const float wz[3] = {zp ? ax[2].w[1] : ax[2].w[0], zp ? ax[2].w[2] : ax[2].w[1], zp ? ax[2].w[0] : ax[2].w[2]};
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         float4 an[9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) an[q] = __ldg(ab + (X[a] + Y[q / 3] + Z[q % 3]));   // 9 loads in flight
+        for (int b = 0; b < 3; ++b) {   // 9 nodes in flight
+          const float4* r = ab + (X[a] + Y[b]);
+          ld_nc8(r + zpair, an[3 * b], an[3 * b + 1]);
+          an[3 * b + 2] = __ldg(r + zone);
+        }
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
           const float rm = an[q].x > 0.0f ? __frcp_rn(an[q].x) : 0.0f;
           const float4 vi = an[q].x > 0.0f ? make_float4(fmaf(an[q].y, rm, gx), fmaf(an[q].z, rm, gy),
                                                          fmaf(an[q].w, rm, gz), an[q].x)
                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-          accumulate(a, q / 3, q % 3, vi);
+          const int b = q / 3, sl = q % 3;
+          const float W = ax[0].w[a] * ax[1].w[b] * wz[sl];
+          const float d0 = ((float)a - ax[0].f) * P.dx, d1 = ((float)b - ax[1].f) * P.dx, d2 = (zc[sl] - ax[2].f) * P.dx;
+          accumulate_w(W, d0, d1, d2, vi);
         }
       }
     } else {
