@@ -413,8 +413,7 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
     if (!finite) flag_error(err, ERR_NONFINITE, (int)p);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
+  if (threadIdx.x == 0) {   // every CTA read d_step at its start (no fence needed)
     if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
       *d_step = step + 1;
       *done = 0;
