@@ -155,7 +155,10 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt,
 nsf_status nsf_mpm_set_stream(nsf_mpm* h, void* cuda_stream);
 
 /* Optional device allocator (e.g. torch's caching allocator), used for every
- * allocation made after this call.  alloc returns NULL on failure. */
+ * allocation made after this call.  alloc returns NULL on failure.  Returned
+ * pointers must be 256-byte aligned (cudaMalloc's and torch's are): the kernels
+ * make 256-bit accesses to grid node pairs; a misaligned pointer fails the
+ * allocating call with NSF_ERR_INVALID_ARGUMENT. */
 nsf_status nsf_mpm_set_allocator(nsf_mpm* h,
                                  void* (*alloc)(size_t bytes, void* stream, void* ctx),
                                  void (*release)(void* ptr, void* stream, void* ctx),

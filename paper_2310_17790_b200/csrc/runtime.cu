@@ -152,6 +152,9 @@ nsf_status alloc_into(nsf_mpm* h, T** dst, size_t bytes) {
   if (*dst) dfree(h, *dst);
   *dst = (T*)dalloc(h, bytes);
   if (!*dst) return fail(h, NSF_ERR_OUT_OF_MEMORY, "device allocation of %zu bytes failed", bytes);
+  // kernels use 256-bit accesses (grid node pairs) and 128-byte particle tiles
+  if (((uintptr_t)*dst & 255u) != 0)
+    return fail(h, NSF_ERR_INVALID_ARGUMENT, "device allocator returned %p, not 256-byte aligned", (void*)*dst);
   return NSF_OK;
 }
 

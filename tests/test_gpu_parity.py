@@ -271,6 +271,28 @@ def test_torch_device_io_and_allocator(nsf):
     sim.close()
 
 
+def test_misaligned_allocator_fails_loudly(nsf):
+    """An allocator hook returning pointers that are not 256-byte aligned (the
+    kernels make 256-bit node-pair accesses) fails the allocating call."""
+    import torch
+    sc = small_scenes()["FC_ragged"]
+    sim = nsf.Simulator(sc.cfg)
+
+    def _alloc(nbytes, stream, ctx):
+        return torch.cuda.caching_allocator_alloc(int(nbytes) + 256, stream=stream or 0) + 16
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(ptr - 16)
+
+    a, f = nsf.ALLOC_FN(_alloc), nsf.FREE_FN(_free)
+    nsf.nsf_mpm_set_allocator(sim.h, a, f)
+    with pytest.raises(nsf.NsfError) as e:
+        sim.load(sc.x, sc.v, sc.C, sc.F)
+    assert e.value.status == nsf.NSF_ERR_INVALID_ARGUMENT
+    assert "256-byte aligned" in nsf.nsf_mpm_last_error(sim.h)
+    sim.close()
+
+
 def test_profiling_counts(nsf):
     sc = small_scenes()["FC_ragged"]
     sim = make(nsf, sc)
