@@ -146,7 +146,10 @@ int32_t nsf_mpm_abi_version(void);
 /* Create a simulator on the current CUDA device.  grid_res: nodes per axis
  * (each a multiple of 4, >= 2*bc_width + 3).  dx, dt > 0 (s, m).  dx should be
  * an exact power of two so B-spline bases are exact in fp32 (#10).  Returns
- * NSF_ERR_INVALID_ARGUMENT on a bad parameter (see nsf_material comments). */
+ * NSF_ERR_INVALID_ARGUMENT on a bad parameter (see nsf_material comments); for
+ * NSF_NEURAL_STRESS also when an axis has more than 1024 nodes or a scene has
+ * 2^31 nodes or more (the reduced G2P packs stencil bases in 10 bits per axis
+ * and addresses a scene's nodes with 32-bit offsets). */
 nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt,
                           const nsf_material* material, nsf_mpm** out);
 
@@ -157,8 +160,15 @@ nsf_status nsf_mpm_set_stream(nsf_mpm* h, void* cuda_stream);
 /* Optional device allocator (e.g. torch's caching allocator), used for every
  * allocation made after this call.  alloc returns NULL on failure.  Returned
  * pointers must be 256-byte aligned (cudaMalloc's and torch's are): the kernels
- * make 256-bit accesses to grid node pairs; a misaligned pointer fails the
- * allocating call with NSF_ERR_INVALID_ARGUMENT. */
+ * make 256-bit accesses to grid node pairs and 128-byte particle tiles; every
+ * allocation is checked, and a misaligned pointer is handed back to `release`
+ * and fails the allocating call (NSF_ERR_INVALID_ARGUMENT from the load / create
+ * calls, NSF_ERR_OUT_OF_MEMORY from internal scratch).  Each block is released
+ * through the release function (and ctx) that was installed when it was
+ * allocated, so the hook may be replaced or removed (alloc = release = NULL:
+ * cudaMalloc again) at any time.  A call that fails part-way leaves the
+ * affected state unloaded (BAD_STATE until it is loaded again), never a
+ * handle that points at released memory. */
 nsf_status nsf_mpm_set_allocator(nsf_mpm* h,
                                  void* (*alloc)(size_t bytes, void* stream, void* ctx),
                                  void (*release)(void* ptr, void* stream, void* ctx),

@@ -280,8 +280,9 @@ void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, cons
 // current base.  The last CTA advances the step counter (every thread reads it
 // first).
 // 256-bit global accesses (sm_100): a node pair at an even node index is 32-byte
-// aligned (the accumulators come from cudaMalloc / the torch allocator, >= 256 B
-// aligned; scenes start at multiples of 64 nodes)
+// aligned.  These accesses go to the two grid arrays h->acc / h->vel, allocated
+// in nsf_mpm_create through dalloc (runtime.cu), which rejects any pointer that is
+// not 256-byte aligned; scenes start at multiples of 64 nodes.
 __device__ __forceinline__ void ld_nc8(const float4* p, float4& a, float4& b) {
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)

@@ -30,7 +30,12 @@ struct nsf_mpm {
   void* (*ualloc)(size_t, void*, void*) = nullptr;
   void (*ufree)(void*, void*, void*) = nullptr;
   void* uctx = nullptr;
-  std::vector<std::pair<void*, bool>> allocs;   // (ptr, from user allocator)
+  struct Alloc {                                // a live device allocation and how to release it
+    void* p;
+    void (*release)(void*, void*, void*);       // NULL: cudaFree; else the hook that was current at allocation
+    void* ctx;
+  };
+  std::vector<Alloc> allocs;
 
   // particles
   int64_t n = 0, pitch = 0;
@@ -121,45 +126,61 @@ nsf_status cuda_fail(nsf_mpm* h, cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(h, _e, #expr);         \
   } while (0)
 
-void* dalloc(nsf_mpm* h, size_t bytes) {
+// Every device allocation goes through here.  Kernels use 256-bit accesses
+// (grid node pairs) and 128-byte particle tiles, so a pointer from an allocator
+// hook that is not 256-byte aligned is released again and the allocation fails.
+void* dalloc(nsf_mpm* h, size_t bytes, bool* misaligned = nullptr) {
+  if (misaligned) *misaligned = false;
   if (bytes == 0) bytes = 256;
   bytes = (bytes + 255) & ~size_t(255);
   void* p = nullptr;
   if (h->ualloc) {
     p = h->ualloc(bytes, (void*)h->stream, h->uctx);
-    if (p) h->allocs.push_back({p, true});
+    if (p && ((uintptr_t)p & 255u) != 0) {
+      h->ufree(p, (void*)h->stream, h->uctx);
+      if (misaligned) *misaligned = true;
+      return nullptr;
+    }
+    if (p) h->allocs.push_back({p, h->ufree, h->uctx});
   } else {
     if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
-    if (p) h->allocs.push_back({p, false});
+    if (p) h->allocs.push_back({p, nullptr, nullptr});
   }
   return p;
 }
 
+// releases through the function recorded with the allocation (the hook may have
+// been changed or removed since)
 void dfree(nsf_mpm* h, void* p) {
   if (!p) return;
   for (size_t i = 0; i < h->allocs.size(); ++i) {
-    if (h->allocs[i].first == p) {
-      if (h->allocs[i].second) h->ufree(p, (void*)h->stream, h->uctx);
-      else cudaFree(p);
+    if (h->allocs[i].p == p) {
+      const nsf_mpm::Alloc a = h->allocs[i];
       h->allocs.erase(h->allocs.begin() + i);
+      if (a.release) a.release(p, (void*)h->stream, a.ctx);
+      else cudaFree(p);
       return;
     }
   }
 }
 
+// (re)allocates *dst; on any failure *dst is NULL (the old buffer is released first)
 template <class T>
 nsf_status alloc_into(nsf_mpm* h, T** dst, size_t bytes) {
   if (*dst) dfree(h, *dst);
-  *dst = (T*)dalloc(h, bytes);
-  if (!*dst) return fail(h, NSF_ERR_OUT_OF_MEMORY, "device allocation of %zu bytes failed", bytes);
-  // kernels use 256-bit accesses (grid node pairs) and 128-byte particle tiles
-  if (((uintptr_t)*dst & 255u) != 0)
-    return fail(h, NSF_ERR_INVALID_ARGUMENT, "device allocator returned %p, not 256-byte aligned", (void*)*dst);
+  *dst = nullptr;
+  bool misaligned = false;
+  T* p = (T*)dalloc(h, bytes, &misaligned);
+  if (misaligned)
+    return fail(h, NSF_ERR_INVALID_ARGUMENT, "device allocator returned a pointer that is not 256-byte aligned");
+  if (!p) return fail(h, NSF_ERR_OUT_OF_MEMORY, "device allocation of %zu bytes failed", bytes);
+  *dst = p;
   return NSF_OK;
 }
 
 nsf_status ensure_staging(nsf_mpm* h, size_t bytes) {
   if (h->staging_bytes >= bytes) return NSF_OK;
+  h->staging_bytes = 0;
   nsf_status s = alloc_into(h, (char**)&h->staging, bytes);
   if (s == NSF_OK) h->staging_bytes = bytes;
   return s;
@@ -271,6 +292,12 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   if (m->deterministic != 0 && m->deterministic != 1) return NSF_ERR_INVALID_ARGUMENT;
   if (m->n_scenes < 1) return NSF_ERR_INVALID_ARGUMENT;
   if (m->model == NSF_NEURAL_STRESS && !std::isfinite(m->stress_scale)) return NSF_ERR_INVALID_ARGUMENT;
+  // the reduced G2P packs the previous stencil base in 10 bits per axis and uses
+  // 32-bit node offsets within a scene (kernels_basic.cu k_g2p_nsf)
+  if (m->model == NSF_NEURAL_STRESS &&
+      (grid_res[0] > 1024 || grid_res[1] > 1024 || grid_res[2] > 1024 ||
+       (int64_t)grid_res[0] * grid_res[1] * grid_res[2] >= (int64_t(1) << 31)))
+    return NSF_ERR_INVALID_ARGUMENT;
   int device = 0;
   if (cudaGetDevice(&device) != cudaSuccess) return NSF_ERR_CUDA;
 
@@ -384,7 +411,8 @@ nsf_status nsf_mpm_load_particles(nsf_mpm* h, int64_t n, const float* x, const f
   std::vector<int64_t> off(ns + 1);
   if (scene_offsets) {
     if (on_device) {
-      CK(cudaMemcpy(off.data(), scene_offsets, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(off.data(), scene_offsets, sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
     } else {
       memcpy(off.data(), scene_offsets, sizeof(int64_t) * (ns + 1));
     }
@@ -398,11 +426,13 @@ nsf_status nsf_mpm_load_particles(nsf_mpm* h, int64_t n, const float* x, const f
   }
   CK(cudaStreamSynchronize(h->stream));
   invalidate_graph(h);
+  h->loaded = false;   // until every buffer below is in place: a failed load leaves no usable state
   bool with_F = h->mat.model != NSF_NEURAL_STRESS;
   int64_t pitch = ((n + 127) / 128) * 128;
   if (pitch == 0) pitch = 128;
-  if (pitch != h->pitch || !h->S[0]) {
+  if (pitch != h->pitch || !h->S[0] || !h->S[1] || !h->ids[0] || !h->ids[1]) {
     nsf_status s;
+    h->pitch = 0;
     for (int k = 0; k < 2; ++k) {
       if ((s = alloc_into(h, &h->S[k], sizeof(float) * kPlanes * pitch)) != NSF_OK) return s;
       if ((s = alloc_into(h, &h->ids[k], sizeof(int32_t) * pitch)) != NSF_OK) return s;
@@ -457,6 +487,9 @@ nsf_status nsf_mpm_load_stress_field(nsf_mpm* h, int32_t in_dim, int32_t width, 
     return fail(h, NSF_ERR_INVALID_ARGUMENT, "unsupported MLP shape (in<=16, width=128, 1<=hidden<=8, out=6)");
   if (!W_bf16 || !b) return fail(h, NSF_ERR_INVALID_ARGUMENT, "W and b are required");
   if (X_ref && !h->loaded) return fail(h, NSF_ERR_BAD_STATE, "load_particles before X_ref");
+  CK(cudaStreamSynchronize(h->stream));
+  invalidate_graph(h);
+  h->mlp_loaded = false;   // until the new weights are in place
   MlpDev& M = h->mlp;
   M.in_dim = in_dim; M.width = width; M.n_hidden = n_hidden; M.out_dim = out_dim;
   int L = n_hidden + 1;
@@ -507,6 +540,7 @@ nsf_status nsf_mpm_load_deformation_field(nsf_mpm* h, int32_t in_dim, int32_t wi
     return fail(h, NSF_ERR_INVALID_ARGUMENT, "unsupported deformation field (in<=16, width=128, 1<=hidden<=4, out=3)");
   if (!W_bf16 || !b) return fail(h, NSF_ERR_INVALID_ARGUMENT, "W and b are required");
   if (!h->loaded) return fail(h, NSF_ERR_BAD_STATE, "load_particles first");
+  h->gdef_loaded = false;   // until the new weights are in place
   MlpDev& M = h->gdef;
   M.in_dim = in_dim; M.width = width; M.n_hidden = n_hidden; M.out_dim = out_dim;
   const int L = n_hidden + 1;
@@ -541,6 +575,7 @@ nsf_status nsf_mpm_load_affine_field(nsf_mpm* h, int32_t in_dim, int32_t width, 
   if (!(in_dim >= 4 && in_dim <= 16) || width != 128 || !(n_hidden >= 1 && n_hidden <= 8) || out_dim != 9)
     return fail(h, NSF_ERR_INVALID_ARGUMENT, "unsupported affine field (in<=16, width=128, 1<=hidden<=8, out=9)");
   if (!W_bf16 || !b) return fail(h, NSF_ERR_INVALID_ARGUMENT, "W and b are required");
+  h->ldef_loaded = false;   // until the new weights are in place
   MlpDev& M = h->ldef;
   M.in_dim = in_dim; M.width = width; M.n_hidden = n_hidden; M.out_dim = out_dim;
   const int L = n_hidden + 1;
@@ -627,7 +662,10 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
     return fail(h, NSF_ERR_INVALID_ARGUMENT, "1 <= n_sample <= n_ref, n_ref * n_scenes < 2^31, X_all and sample_idx");
   // sample indices: in range and distinct within a scene (checked on the host)
   std::vector<int32_t> sidx((size_t)ns * n_sample);
-  if (on_device) CK(cudaMemcpy(sidx.data(), sample_idx, sizeof(int32_t) * sidx.size(), cudaMemcpyDeviceToHost));
+  if (on_device) {
+    CK(cudaMemcpyAsync(sidx.data(), sample_idx, sizeof(int32_t) * sidx.size(), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
   else memcpy(sidx.data(), sample_idx, sizeof(int32_t) * sidx.size());
   {
     std::vector<int32_t> seen((size_t)n_ref, -1);
@@ -768,6 +806,8 @@ nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const floa
   int ns = h->mat.n_scenes;
   nsf_status s;
   CK(cudaStreamSynchronize(h->stream));
+  invalidate_graph(h);
+  h->latents_loaded = false;   // until the new latents are in place
   if ((s = alloc_into(h, &h->z, sizeof(float) * ns * r)) != NSF_OK) return s;
   if ((s = alloc_into(h, &h->dz, sizeof(float) * ns * r)) != NSF_OK) return s;
   if ((s = to_device(h, z, sizeof(float) * ns * r, on_device, h->z)) != NSF_OK) return s;
@@ -898,7 +938,9 @@ int64_t nsf_mpm_step_count(const nsf_mpm* h) { return h ? h->host_step : -1; }
 
 int64_t nsf_mpm_inverted_count(nsf_mpm* h) {
   if (!h || h->poisoned) return -1;
-  if (cudaMemcpy(h->err_host, h->err, sizeof(DevErr), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  if (cudaMemcpyAsync(h->err_host, h->err, sizeof(DevErr), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+      cudaStreamSynchronize(h->stream) != cudaSuccess)
+    return -1;
   return (int64_t)h->err_host->inverted;
 }
 
@@ -911,7 +953,7 @@ void nsf_mpm_destroy(nsf_mpm* h) {
   for (auto& p : h->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : h->free_events) cudaEventDestroy(e);
   pipeline_destroy(h, &h->pb);
-  while (!h->allocs.empty()) dfree(h, h->allocs.back().first);
+  while (!h->allocs.empty()) dfree(h, h->allocs.back().p);
   if (h->err_host) cudaFreeHost(h->err_host);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
