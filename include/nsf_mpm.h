@@ -281,8 +281,9 @@ nsf_status nsf_mpm_read_state(nsf_mpm* h, uint32_t field_mask, float* const* dst
                               int32_t on_device);
 
 /* Block until all enqueued work is done; report deferred device errors
- * (NSF_ERR_OUT_OF_DOMAIN / NSF_ERR_NONFINITE with the particle index and
- * substep in last_error). */
+ * (NSF_ERR_OUT_OF_DOMAIN / NSF_ERR_NONFINITE with the smallest offending
+ * particle index -- its position in the arrays passed to load_particles, not
+ * its internal storage slot -- and the substep count in last_error). */
 nsf_status nsf_mpm_sync(nsf_mpm* h);
 
 /* Substeps enqueued since the last load (host counter). */

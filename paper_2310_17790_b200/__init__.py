@@ -436,6 +436,10 @@ class Simulator:
     def sync(self):
         nsf_mpm_sync(self.h)
 
+    def inverted_count(self) -> int:
+        """Particle updates that produced det F_E <= 0 since the load (#21)."""
+        return nsf_mpm_inverted_count(self.h)
+
     def read(self, mask=NSF_FIELD_X | NSF_FIELD_V | NSF_FIELD_C | NSF_FIELD_F | NSF_FIELD_TAU, device=None):
         outs = nsf_mpm_read_state(self.h, mask, self.n, device)
         names = [nm for bit, nm in ((1, "x"), (2, "v"), (4, "C"), (8, "F"), (16, "tau"), (32, "tau_Y")) if mask & bit]

@@ -16,14 +16,15 @@ void launch_p2g_direct(cudaStream_t st, int64_t n, const float* S, int64_t pitch
                        const int64_t* scene_off, int n_scenes, float4* acc, const DevParams& P);
 void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, const int64_t* scene_off,
                        int n_scenes, const float4* vel, const DevParams& P, DevErr* err, int64_t* d_step,
-                       int with_F);
+                       int with_F, const int32_t* ids);   // ids: load index of each slot (error reports)
 void launch_grid_debug(cudaStream_t st, int stage, int64_t total_nodes, const float4* acc, float4* vel,
                        float* out, const DevParams& P, const int64_t* d_step);
 
 // reduced (NSF) substep pieces (point_ops.cuh, kernels_basic.cu)
 struct NsfP2G;
 void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_off, int n_scenes,
-                    float4* acc0, float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step, int* done);
+                    float4* acc0, float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step, int* done,
+                    const int32_t* ids);
 void launch_nsf_reset_base(cudaStream_t st, int64_t n, float* S);
 
 // kernels_nsf.cu -- neural stress field MLP

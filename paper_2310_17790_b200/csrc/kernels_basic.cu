@@ -18,33 +18,42 @@ __global__ void k_unpack(int64_t n, const float* __restrict__ x, const float* __
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   float xp[3], Fp[9];
+  bool finite = true;   // every input value and tau^0 (else NSF_ERR_NONFINITE at load)
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     xp[a] = x[p * 3 + a];
+    const float vp = v[p * 3 + a];
     S[pbase(p) + (PX + a) * 32] = xp[a];
-    S[pbase(p) + (PV + a) * 32] = v[p * 3 + a];
+    S[pbase(p) + (PV + a) * 32] = vp;
+    finite &= isfinite(xp[a]) && isfinite(vp);
   }
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
-    S[pbase(p) + (PC + k) * 32] = C ? C[p * 9 + k] : 0.0f;
+    const float c = C ? C[p * 9 + k] : 0.0f;
+    S[pbase(p) + (PC + k) * 32] = c;
     Fp[k] = F ? F[p * 9 + k] : ((k % 4 == 0) ? 1.0f : 0.0f);
     if (with_F) S[pbase(p) + (PF + k) * 32] = Fp[k];
+    finite &= isfinite(c) && isfinite(Fp[k]);
   }
   ids[p] = (int32_t)p;
   bool ok = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) ok &= in_safe_region(xp[a] * P.inv_dx, P.N[a]);
-  if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
+  if (!ok && finite) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
   if (with_F) {
     float tau[6];
     elastic_tau(Fp, P.model, P.mu, P.lam, tau);
 #pragma unroll
-    for (int k = 0; k < 6; ++k) S[pbase(p) + (PT + k) * 32] = tau[k];
+    for (int k = 0; k < 6; ++k) {
+      S[pbase(p) + (PT + k) * 32] = tau[k];
+      finite &= isfinite(tau[k]);
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < 6; ++k) S[pbase(p) + (PT + k) * 32] = 0.0f;
   }
   S[pbase(p) + PTY * 32] = P.tau_Y;   // per-particle yield stress starts at the material's
+  if (!finite) flag_error(err, ERR_NONFINITE, (int)p);
 }
 
 void launch_unpack(cudaStream_t st, int64_t n, const float* x, const float* v, const float* C,
@@ -154,7 +163,7 @@ template <int FORCE, int WITH_F>
 __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t pitch,
                                                     const int64_t* __restrict__ scene_off, int n_scenes,
                                                     const float4* __restrict__ vel, DevParams P,
-                                                    DevErr* err, int64_t* d_step) {
+                                                    DevErr* err, int64_t* d_step, const int32_t* __restrict__ ids) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p == 0 && d_step) atomicAdd((unsigned long long*)d_step, 1ull);
   if (p >= n) return;
@@ -255,21 +264,21 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
 #pragma unroll
     for (int k = 0; k < 6; ++k) { S[pbase(p) + (PT + k) * 32] = tau[k]; finite &= isfinite(tau[k]); }
   }
-  if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
-  if (!finite) flag_error(err, ERR_NONFINITE, (int)p);
+  if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, ids[p]);
+  if (!finite) flag_error(err, ERR_NONFINITE, ids[p]);
 }
 
 void launch_g2p_direct(cudaStream_t st, int64_t n, float* S, int64_t pitch, const int64_t* scene_off,
                        int n_scenes, const float4* vel, const DevParams& P, DevErr* err, int64_t* d_step,
-                       int with_F) {
+                       int with_F, const int32_t* ids) {
   int bs = 128;
   unsigned g = (unsigned)((n + bs - 1) / bs);
   if (g == 0) g = 1;   // still bump the step counter
   if (with_F) {
-    if (P.force_mode == 0) k_g2p_direct<0, 1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
-    else k_g2p_direct<1, 1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
+    if (P.force_mode == 0) k_g2p_direct<0, 1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step, ids);
+    else k_g2p_direct<1, 1><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step, ids);
   } else {
-    k_g2p_direct<0, 0><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step);
+    k_g2p_direct<0, 0><<<g, bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, vel, P, err, d_step, ids);
   }
 }
 
@@ -297,7 +306,7 @@ __device__ __forceinline__ void st_zero8(float4* p) {
 #endif
 __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, float* S, const int64_t* __restrict__ scene_off,
                                                  int n_scenes, float4* acc0, float4* acc1, DevParams P, DevErr* err,
-                                                 int64_t* d_step, int* done) {
+                                                 int64_t* d_step, int* done, const int32_t* __restrict__ ids) {
   const int64_t step = *(volatile const int64_t*)d_step;
   // reverse sweep: the MLP/P2G kernel just reduced into the accumulator in
   // forward point order, so its most recent (L2-resident) lines come first
@@ -410,8 +419,8 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
     }
 #pragma unroll
     for (int k = 0; k < 9; ++k) S[pbase(p) + (PC + k) * 32] = cC * Bm[k];
-    if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
-    if (!finite) flag_error(err, ERR_NONFINITE, (int)p);
+    if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, ids[p]);
+    if (!finite) flag_error(err, ERR_NONFINITE, ids[p]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {   // every CTA read d_step at its start (no fence needed)
@@ -423,11 +432,12 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
 }
 
 void launch_g2p_nsf(cudaStream_t st, int64_t n, float* S, const int64_t* scene_off, int n_scenes,
-                    float4* acc0, float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step, int* done) {
+                    float4* acc0, float4* acc1, const DevParams& P, DevErr* err, int64_t* d_step, int* done,
+                    const int32_t* ids) {
   const int bs = 128;
   unsigned g = (unsigned)((n + bs - 1) / bs);
   if (g == 0) g = 1;   // still advances the step counter
-  k_g2p_nsf<<<g, bs, 0, st>>>(n, S, scene_off, n_scenes, acc0, acc1, P, err, d_step, done);
+  k_g2p_nsf<<<g, bs, 0, st>>>(n, S, scene_off, n_scenes, acc0, acc1, P, err, d_step, done, ids);
 }
 
 // Marks every point's previous stencil as absent (after a load).

@@ -461,6 +461,38 @@ __device__ __forceinline__ float4 grid_node_update_t(float4 a, int i, int j, int
   return make_float4(v[0], v[1], v[2], m);
 }
 
+// The same update (readings #11-#14) for nodes updated inside the fused
+// kernel: one correctly rounded reciprocal of m_i and three products instead of
+// three IEEE divisions (<= 1.5 ulp apart); `in_walls` is false when the caller
+// knows the node lies outside every wall region (then only the plate applies).
+__device__ __forceinline__ float4 grid_node_update_rcp(float4 a, int i, int j, int k, const DevParams& P, float y_plate,
+                                                       bool in_walls = true) {
+  const float m = a.x;
+  if (!(m > 0.0f)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const float r = __frcp_rn(m);
+  float v[3] = {fmaf(a.y, r, P.dt * P.g[0]) , fmaf(a.z, r, P.dt * P.g[1]), fmaf(a.w, r, P.dt * P.g[2])};
+  if (in_walls) {
+    const int idx[3] = {i, j, k};
+#pragma unroll
+    for (int face = 0; face < 6; ++face) {
+      const int kind = P.bc[face];
+      if (kind == 0) continue;
+      const int axis = face >> 1;
+      const bool high = face & 1;
+      const bool in = high ? (idx[axis] >= P.N[axis] - P.bc_width) : (idx[axis] < P.bc_width);
+      if (!in) continue;
+      if (kind == 1) { v[0] = v[1] = v[2] = 0.0f; }
+      else v[axis] = high ? fminf(v[axis], 0.0f) : fmaxf(v[axis], 0.0f);
+    }
+  }
+  if (P.plate_enabled && (float)j * P.dx >= y_plate) { v[0] = P.plate_v[0]; v[1] = P.plate_v[1]; v[2] = P.plate_v[2]; }
+  return make_float4(v[0], v[1], v[2], m);
+}
+
+__device__ __forceinline__ float plate_y_at(const DevParams& P, int64_t step) {
+  return (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)step * (double)P.dt));
+}
+
 __global__ void __launch_bounds__(128)
 k_grid_update_blocks(const int32_t* __restrict__ block_start, const int32_t* __restrict__ nonempty,
                      int32_t* __restrict__ n_nonempty, float4* acc, float4* vel,
@@ -541,9 +573,9 @@ __device__ __forceinline__ void load_pstate(PState& s, const float* __restrict__
 // form), from the blocked grid velocities vb (read through L1).  Separable sums:
 // per stencil plane a, T = sum w_y w_z v, Ty = sum o_y w_y w_z v, Tz = sum o_z w_y w_z v;
 // then v = sum w_x T and B = dx (M - v f^T) with M_ij = sum W v_i o_j.
-template <int FORCE>
+template <int FORCE, bool RAW = false>
 __device__ __forceinline__ void g2p_gather(const float x[3], const float4* __restrict__ vb, const DevParams& P,
-                                           float v[3], float Cn[9], float G[9]) {
+                                           float v[3], float Cn[9], float G[9], float y_plate = 0.0f) {
 #pragma unroll
   for (int k = 0; k < 3; ++k) v[k] = 0.f;
 #pragma unroll
@@ -580,7 +612,10 @@ __device__ __forceinline__ void g2p_gather(const float x[3], const float4* __res
     for (int b = 0; b < 3; ++b)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const float4 vi = __ldg(vb + (X[a] + Y[b] + Z[c]));
+        // RAW: vb holds the P2G sums (m, m v); the node is updated here
+        const float4 vi = RAW ? grid_node_update_rcp(__ldcg(vb + (X[a] + Y[b] + Z[c])), ax[0].base + a,
+                                                     ax[1].base + b, ax[2].base + c, P, y_plate)
+                              : __ldg(vb + (X[a] + Y[b] + Z[c]));
         const float wgt = wyz[b * 3 + c];
         Tt[0] = fmaf(wgt, vi.x, Tt[0]); Tt[1] = fmaf(wgt, vi.y, Tt[1]); Tt[2] = fmaf(wgt, vi.z, Tt[2]);
         if (b) {
@@ -662,7 +697,7 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
   for (int a = 0; a < 3; ++a) {
     xn[a] = st.x[a] + P.dt * v[a];
     const float tt = xn[a] * P.inv_dx;
-    ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
+    ok &= !(tt < 0.5f || tt >= (float)P.N[a] - 1.5f);   // NaN: non-finite, not out of domain
     ob[(PX + a) * 32] = xn[a];
     ob[(PV + a) * 32] = v[a];
     chk += xn[a] + v[a];
@@ -984,11 +1019,12 @@ __device__ __forceinline__ void load_xF(const float* __restrict__ S, int j, floa
   for (int k = 0; k < 9; ++k) F[k] = ld_state(base + (PF + k) * 32);
 }
 
-template <bool DO_G2P, bool HS>
+template <bool DO_G2P, bool HS, bool ROT>
 __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const float xin[3], const float Fin[9],
                                                    const int o[3], const float4* vt, const float4* __restrict__ gvel,
                                                    const DevParams& P, DevErr* err, float xn[3], float vn[3],
-                                                   float Cn[9], float tau[6]) {
+                                                   float Cn[9], float tau[6], float y_plate,
+                                                   const int32_t* __restrict__ ids) {
   float* base = S + pbase(j);
       if (DO_G2P) {
     float x[3], F[9], G[9];
@@ -1008,14 +1044,14 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 #pragma unroll
       for (int k = 0; k < 9; ++k) G[k] = Cn[k];
     } else {
-      g2p_gather<0>(x, gvel, P, vn, Cn, G);
+      g2p_gather<0, ROT>(x, gvel, P, vn, Cn, G, y_plate);   // ROT: gvel holds raw P2G sums
     }
     bool ok = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       xn[a] = x[a] + P.dt * vn[a];
       const float tt = xn[a] * P.inv_dx;
-      ok &= (tt >= 0.5f) && (tt < (float)P.N[a] - 1.5f);
+      ok &= !(tt < 0.5f || tt >= (float)P.N[a] - 1.5f);   // NaN: non-finite, not out of domain
       st_state(base + (PX + a) * 32, xn[a]);
       st_state(base + (PV + a) * 32, vn[a]);
     }
@@ -1043,8 +1079,8 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 #pragma unroll
     for (int k = 0; k < 6; ++k) { st_state(base + (PT + k) * 32, tau[k]); chk += tau[k]; }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
-    if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, j); }
-    if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, j); }
+    if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, ids[j]); }
+    if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, ids[j]); }
   } else {
 #pragma unroll
     for (int a = 0; a < 3; ++a) { xn[a] = base[(PX + a) * 32]; vn[a] = base[(PV + a) * 32]; }
@@ -1081,19 +1117,59 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
   }
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false>
+// ROT: the grid update runs inside this kernel (RotGrid, pipeline.h): `vel`,
+// `acc`, `flags`, `list` and `list_count` are ignored and taken from the
+// rotation instead; the segment's velocity tile is staged from the raw P2G sums
+// with every node updated on the way, the blocks of the cleared buffer
+// are zeroed, and the last CTA to finish advances the step counter.
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, bool ROT = false>
 __global__ void __launch_bounds__(NT, MINB)
-k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
+k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
-        int64_t* d_step) {
+        int64_t* d_step, RotGrid rg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FusedSmemT<ROWS>& sm = *reinterpret_cast<FusedSmemT<ROWS>*>(smem_raw);
   const int tid = threadIdx.x;
   const int my_cell = tid & 63;
   const int ox = tid >> 6;
   const int nblk = *(volatile int32_t*)&counters[0];
-  if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
+  int64_t kstep = 0;
+  float y_plate = 0.0f;
+  if (ROT) {
+    // kernel index kw: the P2G written here is that of state kw + 1 (kw = -1 for
+    // the P2G of the loaded state); it reads buffer kw % 3, writes (kw + 1) % 3,
+    // clears (kw + 2) % 3
+    kstep = *(volatile const int64_t*)d_step;
+    const int64_t kw = DO_G2P ? kstep : kstep - 1;
+    const int rb = (int)(((kw % 3) + 3) % 3), wb = (rb + 1) % 3, zb = (rb + 2) % 3;
+    const int64_t TB = rg.total_blocks;
+    vel = rg.buf[rb];
+    acc = rg.buf[wb];
+    flags = rg.flags + wb * TB;
+    list = rg.list + wb * TB;
+    list_count = rg.cnt + (int)(kw & 3);
+    y_plate = plate_y_at(P, kstep);
+    if (DO_G2P) {
+      // clear the blocks of buffer zb (the P2G of kernel kw - 2) and their flags;
+      // CTA c takes list entries c, c + grid, ...
+      const int nz = *(volatile const int*)&rg.cnt[(int)((kw + 2) & 3)];
+      const int* zl = rg.list + zb * TB;
+      int* zf = rg.flags + zb * TB;
+      float4* zbuf = rg.buf[zb];
+      for (int i = tid;; i += NT) {
+        const int e = (int)blockIdx.x + (i >> 6) * (int)gridDim.x;
+        if (e >= nz) break;
+        const int key = zl[e];
+        zbuf[(int64_t)key * kBlockNodes + (i & 63)] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if ((i & 63) == 0) zf[key] = 0;
+      }
+    }
+  } else {
+    // list count slot published by the grid update (or 0 after a load)
+    list_count += *(volatile const int*)(list_count + 2);
+    if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
+  }
   // segment tickets: the first here, each next one claimed after phase 1 of the
   // current segment (its round trip overlaps phase 2)
   if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
@@ -1110,7 +1186,41 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
     if (tid < 64) sm.pop[tid] = 0;
     if (tid == 0) sm.nsc = 0;
     const int o[3] = {4 * bc.b[0] - 1, 4 * bc.b[1] - 1, 4 * bc.b[2] - 1};   // tile origin (grid node)
-    if (DO_G2P && NSF_FUSED_VTILE) {
+    float x0[3], F0[9];   // the first particle's x, F: loaded under the tile copy
+    if (DO_G2P && NSF_FUSED_VTILE && ROT) {
+      // raw P2G sums of the tile's nodes (L2-resident: reduced by the previous
+      // kernel) copied asynchronously; after the wait each thread updates the
+      // nodes it copied in place, so the first particle's loads overlap
+      // the copy and the update, and no extra barrier is needed
+      constexpr int kPer = (kVT * kVT * kVT + NT - 1) / NT;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * NT;
+        if (e < kVT * kVT * kVT) {
+          const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
+          const bool in = i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2];
+          cp_async16_f(&sm.vt[(e >> 6) * kVTx + ((e >> 3) & 7) * kVTy + (e & 7)],
+                       in ? gvel + node_index(i, jn, k, P) : gvel, in ? 16 : 0);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
+      // walls: skip the per-face tests when the tile lies inside [w, N - w) on every axis
+      bool walls = false;
+#pragma unroll
+      for (int ax_ = 0; ax_ < 3; ++ax_)
+        walls |= (o[ax_] < P.bc_width) || (o[ax_] + kVT > P.N[ax_] - P.bc_width);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * NT;
+        if (e < kVT * kVT * kVT) {
+          const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
+          float4* t = &sm.vt[(e >> 6) * kVTx + ((e >> 3) & 7) * kVTy + (e & 7)];
+          *t = grid_node_update_rcp(*t, i, jn, k, P, y_plate, walls);
+        }
+      }
+    } else if (DO_G2P && NSF_FUSED_VTILE) {
       for (int e = tid; e < kVT * kVT * kVT; e += NT) {
         const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
         const bool in = i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2];
@@ -1119,9 +1229,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    // the first particle's x, F load under the tile copy
-    float x0[3], F0[9];
-    if (DO_G2P && s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
+    if (DO_G2P && !ROT && s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // ---- phase 1: per particle ----
@@ -1135,7 +1243,7 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
 #else
       if (DO_G2P && j != s0 + tid) load_xF(S, j, x0, F0);
 #endif
-      fused_g2p_particle<DO_G2P, HS>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau);
+      fused_g2p_particle<DO_G2P, HS, ROT>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau, y_plate, ids);
 #if NSF_PF_NEXT
       if (DO_G2P && j + NT < s1) {
 #pragma unroll
@@ -1218,24 +1326,50 @@ k_g2p2g(float* __restrict__ S, const float4* __restrict__ vel, float4* __restric
         touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
     }
   }
+  if (ROT && tid == 0) {
+    // every CTA has read the step counter and claimed its last ticket: the last
+    // one to finish resets the ticket and the completion counter, and (G2P)
+    // advances the step and empties the count slot the next kernel appends to
+    if (atomicAdd(&rg.cnt[4], 1) == (int)gridDim.x - 1) {
+      rg.cnt[4] = 0;
+      counters[3] = 0;
+      if (DO_G2P) {
+        *d_step = kstep + 1;
+        rg.cnt[(int)((kstep + 1) & 3)] = 0;
+      }
+    }
+  }
 }
 
 // Grid update over the touched blocks: v = mv/m + dt g, walls, plate; the
-// accumulator and the block's flag are cleared.  One warp per listed block; the
-// last CTA to finish empties the list for the next G2P2G.
+// accumulator and the block's flag are cleared.  One warp per listed block.  The
+// list count alternates between two slots by step parity: this kernel reads slot
+// n & 1, empties slot (n + 1) & 1 and publishes it (sel) for the next G2P2G to
+// append to -- no completion counter or fence is needed.
 __global__ void __launch_bounds__(128)
-k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* __restrict__ list_count,
-                   int* __restrict__ done_count, float4* __restrict__ acc, float4* __restrict__ vel, DevParams P,
+k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* __restrict__ cnt2,
+                   float4* __restrict__ acc, float4* __restrict__ vel, DevParams P,
                    const int64_t* __restrict__ d_step, int32_t* __restrict__ counters) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) counters[3] = 0;   // segment ticket of the next k_g2p2g
-  const int nl = *(volatile int*)list_count;
+  // the step, both count slots and this warp's first list entry are loaded
+  // together (the entry speculatively: the list has room for every block)
   const int lane = threadIdx.x & 31;
   const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  const float y_plate = (float)((double)P.plate_y0 + (double)P.plate_v[1] * ((double)(*d_step) * (double)P.dt));
+  const int64_t n = *d_step;
+  const int c0 = cnt2[0], c1 = cnt2[1];
+  int key_next = warp < P.blocks_per_scene * P.n_scenes ? list[warp] : 0;
+  const int s = (int)(n & 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    counters[3] = 0;    // segment ticket of the next k_g2p2g
+    cnt2[s ^ 1] = 0;    // the list the next k_g2p2g appends to
+    cnt2[2] = s ^ 1;
+  }
+  const int nl = s ? c1 : c0;
+  const float y_plate = plate_y_at(P, n);
   const int bps = (int)P.blocks_per_scene;
   for (int e = warp; e < nl; e += nwarps) {
-    const int key = list[e];
+    const int key = key_next;
+    if (e + nwarps < nl) key_next = list[e + nwarps];
     const int scene = key / bps;
     const BlockCoord bc = decode_block(key, P);
     const int64_t gb = (int64_t)scene * P.nodes_per_scene + (int64_t)(key - scene * bps) * kBlockNodes;
@@ -1250,14 +1384,6 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
       acc[gb + l] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (lane == 0) flags[key] = 0;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(done_count, 1) == (int)gridDim.x - 1) {
-      *list_count = 0;
-      *done_count = 0;
-    }
   }
 }
 
@@ -1344,38 +1470,57 @@ void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_
                                                  pb->n_nonempty, P);
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false>
-static void launch_g2p2g_t(cudaStream_t st, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, bool ROT = false>
+static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
   const size_t smem = sizeof(FusedSmemT<ROWS>);
   if (!attr) {
-    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
-  k_g2p2g<DO_G2P, ROWS, MINB, NT, HS><<<num_sms() * MINB, NT, smem, st>>>(
-      S, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
-      pb->n_nonempty, P, err, d_step);
+  k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT><<<num_sms() * MINB, NT, smem, st>>>(
+      S, ids, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
+      pb->n_nonempty, P, err, d_step, pb->rg);
 }
 
-void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
-                  const DevParams& P, DevErr* err, int64_t* d_step) {
+template <bool ROT>
+static void launch_g2p2g_r(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, const float4* vel, float4* acc,
+                           PipelineBuffers* pb, const DevParams& P, DevErr* err, int64_t* d_step) {
   if (do_g2p && P.vm_hs) {   // von Mises with a per-particle yield stress
-    if (pb->sparse) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192, true>(st, S, vel, acc, pb, P, err, d_step);
-    else launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS, true>(st, S, vel, acc, pb, P, err, d_step);
+    if (pb->sparse)
+      launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192, true, ROT>(st, S, ids, vel, acc, pb, P, err, d_step);
+    else
+      launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS, true, ROT>(st, S, ids, vel, acc, pb, P, err,
+                                                                                      d_step);
     return;
   }
   if (do_g2p && pb->dense2) {   // dense, 2 CTAs per SM
-    launch_g2p2g_t<true, kRowsF, 2, NSF_DENSE_THREADS>(st, S, vel, acc, pb, P, err, d_step);
+    launch_g2p2g_t<true, kRowsF, 2, NSF_DENSE_THREADS, false, ROT>(st, S, ids, vel, acc, pb, P, err, d_step);
     return;
   }
   if (pb->sparse) {
-    if (do_g2p) launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192>(st, S, vel, acc, pb, P, err, d_step);
-    else launch_g2p2g_t<false, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192>(st, S, vel, acc, pb, P, err, d_step);
+    if (do_g2p)
+      launch_g2p2g_t<true, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192, false, ROT>(st, S, ids, vel, acc, pb, P, err, d_step);
+    else
+      launch_g2p2g_t<false, NSF_SPARSE_ROWS, NSF_SPARSE_MIN_BLOCKS, 192, false, ROT>(st, S, ids, vel, acc, pb, P, err,
+                                                                                    d_step);
   } else {
-    if (do_g2p) launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS>(st, S, vel, acc, pb, P, err, d_step);
-    else launch_g2p2g_t<false, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS>(st, S, vel, acc, pb, P, err, d_step);
+    if (do_g2p)
+      launch_g2p2g_t<true, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS, false, ROT>(st, S, ids, vel, acc, pb, P, err,
+                                                                                       d_step);
+    else
+      launch_g2p2g_t<false, kRowsF, NSF_DENSE_MIN_BLOCKS, NSF_DENSE_THREADS, false, ROT>(st, S, ids, vel, acc, pb, P, err,
+                                                                                        d_step);
   }
+}
+
+void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, const float4* vel, float4* acc,
+                  PipelineBuffers* pb,
+                  const DevParams& P, DevErr* err, int64_t* d_step) {
+  if (pb->rot) launch_g2p2g_r<true>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
+  else launch_g2p2g_r<false>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
 }
 
 #ifndef NSF_GU_CTAS_PER_SM
@@ -1384,8 +1529,8 @@ void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, flo
 void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
                               const int64_t* d_step) {
   const int grid = num_sms() * NSF_GU_CTAS_PER_SM;
-  k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks,
-                                           pb->touched + pb->total_blocks + 1, acc, vel, P, d_step, pb->n_nonempty);
+  k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks, acc, vel, P,
+                                           d_step, pb->n_nonempty);
 }
 
 void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,

@@ -516,8 +516,11 @@ __device__ __forceinline__ float elastoplastic_fast(const float Ft[9], int model
 #endif
   float U[3][3];
   sym_eig3(Bm, U);
-  const float kFloor2 = 1e-8f;   // sigma >= 1e-4
-  if (!(1.0f + Bm[0][0] > kFloor2 && 1.0f + Bm[1][1] > kFloor2 && 1.0f + Bm[2][2] > kFloor2))
+  // sigma_i^2 = 1 + lambda_i(S) carries an absolute error ~ eps ||S||, so log sigma
+  // loses accuracy as sigma -> 0 (at sigma = 5e-5 the clamp decision of #21 is
+  // lost entirely): below sigma = 1/4 the rotation-safe SVD decides instead
+  const float kEigMin2 = 0.0625f;
+  if (!(1.0f + Bm[0][0] > kEigMin2 && 1.0f + Bm[1][1] > kEigMin2 && 1.0f + Bm[2][2] > kEigMin2))
     return elastoplastic(Ft, model, mu, lam, alpha, tau_Y, FE, tau, dg_out);
   // eps = log sigma = log(lambda)/2
   const float e[3] = {0.5f * log1pf(Bm[0][0]), 0.5f * log1pf(Bm[1][1]), 0.5f * log1pf(Bm[2][2])};

@@ -113,6 +113,39 @@ static bool nsf_sort_enabled() {
   return f == 1;
 }
 
+// grid update inside the fused kernel (three rotating accumulators, RotGrid) or
+// the separate k_grid_update_list pass: NSF_FUSED_GU=rot|kernel forces one
+// (read at every load, so a test can run both in one process)
+static int rot_mode() {
+  const char* e = getenv("NSF_FUSED_GU");
+  return (e && strcmp(e, "kernel") == 0) ? 0 : (e && strcmp(e, "rot") == 0) ? 1 : -1;
+}
+
+static nsf_status rot_setup(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v) {
+  RotGrid& rg = pb->rg;
+  const int64_t TB = pb->total_blocks;
+  if (!pb->grid3) {
+    pb->grid3 = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
+    if (!pb->grid3) return NSF_ERR_OUT_OF_MEMORY;
+  }
+  if (!rg.flags) {
+    rg.flags = (int*)pipeline_alloc(h, sizeof(int) * 3 * TB);
+    rg.list = (int*)pipeline_alloc(h, sizeof(int) * 3 * TB);
+    rg.cnt = (int*)pipeline_alloc(h, sizeof(int) * 8);
+    if (!rg.flags || !rg.list || !rg.cnt) return NSF_ERR_OUT_OF_MEMORY;
+  }
+  rg.buf[0] = v.acc;
+  rg.buf[1] = v.vel;
+  rg.buf[2] = pb->grid3;
+  rg.total_blocks = TB;
+  if (cudaMemsetAsync(v.vel, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess ||
+      cudaMemsetAsync(pb->grid3, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess ||
+      cudaMemsetAsync(rg.flags, 0, sizeof(int) * 3 * TB, v.stream) != cudaSuccess ||
+      cudaMemsetAsync(rg.cnt, 0, sizeof(int) * 8, v.stream) != cudaSuccess)
+    return NSF_ERR_CUDA;
+  return NSF_OK;
+}
+
 static bool fused_enabled() {
   static int f = -1;
   if (f < 0) {
@@ -178,7 +211,15 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     if (fv && strcmp(fv, "dense2") == 0) pb->dense2 = true;
     else if (fv) pb->dense2 = false;
     else pb->dense2 = !pb->sparse && nblk < 2 * 3 * num_sms();
-    launch_g2p2g(v.stream, false, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step);   // P2G of state 0
+    // grid update inside the fused kernel only where it measured faster: the
+    // 2-CTA/SM dense variant (few segments per CTA, e.g. C2); C3 (3 CTAs/SM) and the
+    // sparse variant (512 tile nodes per ~100 particles, C4) keep the separate pass
+    pb->rot = rot_mode() == 1 || (rot_mode() < 0 && pb->dense2);
+    if (pb->rot) {
+      const nsf_status rs = rot_setup(h, pb, v);
+      if (rs != NSF_OK) return rs;
+    }
+    launch_g2p2g(v.stream, false, v.S[cur], v.ids[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step);   // P2G of state 0
   } else if (pb->tiled) {
     launch_keys_hist(v.stream, v.n, v.S[0], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
   } else {
@@ -261,15 +302,15 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
     PLAUNCH(h, "p2g_fixed", launch_p2g_fixed(v.stream, v.n, v.S[cur], v.scene_off, v.n_scenes, pb->fx, pb, *v.P));
     PLAUNCH(h, "grid_update", launch_grid_update_fixed(v.stream, pb, pb->fx, v.vel, *v.P, v.d_step));
     PLAUNCH(h, "g2p_direct", launch_g2p_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, v.vel, *v.P,
-                                               v.err, v.d_step, nsf_model ? 0 : 1));
+                                               v.err, v.d_step, nsf_model ? 0 : 1, v.ids[cur]));
     launches += (v.n > 0) + 2;
     pb->launches = launches;
     return cur;
   }
   if (pb->fused) {
-    PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
-    PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
-    launches = 2;
+    if (!pb->rot) PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
+    PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.ids[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
+    launches = pb->rot ? 1 : 2;
     int next = cur;
     if (variant) {
       next = enqueue_rebin(h, pb, v, cur);
@@ -312,7 +353,7 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
           launch_nsf_mlp(v.stream, v.n, v.S[cur] + PXR * kTileP, -1, v.scene_off, v.n_scenes, v.z, v.dz, v.r,
                          v.d_step, *v.mlp, v.P->stress_scale, v.S[cur] + PT * kTileP, v.pitch, 0, &q));
   PLAUNCH(h, "g2p_nsf", launch_g2p_nsf(v.stream, v.n, v.S[cur], v.scene_off, v.n_scenes, v.acc, v.vel, *v.P, v.err,
-                                       v.d_step, pb->nsf_done));
+                                       v.d_step, pb->nsf_done, v.ids[cur]));
   launches += (v.n > 0 ? 2 : 1);
   if (variant && v.n > 0) {
     pb->launches = launches + 4;
@@ -373,8 +414,18 @@ int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* count
 int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, float* out) {
   HandleView v = view(h);
   if (pb->fused) {
-    // the accumulator already holds P2G of the current state; keep it
-    launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
+    // the accumulator already holds P2G of the current state; keep it (rotation:
+    // buffer step % 3, updated into a scratch grid: the other two are in use)
+    if (pb->rot) {
+      if (!pb->dbg_vel) {
+        pb->dbg_vel = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
+        if (!pb->dbg_vel) return -1;
+      }
+      launch_grid_debug(v.stream, stage, v.total_nodes, pb->rg.buf[v.host_step % 3], pb->dbg_vel, out, *v.P,
+                        v.d_step);
+    } else {
+      launch_grid_debug(v.stream, stage, v.total_nodes, v.acc, v.vel, out, *v.P, v.d_step);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   float4* acc = v.acc;

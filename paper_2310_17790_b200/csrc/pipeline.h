@@ -12,6 +12,23 @@ namespace nsf {
 // fused kernel variant threshold: mean particles per non-empty 4^3-cell block
 constexpr int kSparseParticlesPerBlock = 256;
 
+// Fused full-order pipeline with the grid update inside the G2P2G kernel: three
+// grid accumulators used in rotation.  Kernel k (k = substeps done) reads the
+// raw P2G sums of buffer k % 3 (updating each node as it stages its velocity
+// tile), reduces the next P2G into buffer (k + 1) % 3 and clears the
+// blocks of buffer (k + 2) % 3 (written two kernels ago, read by kernel k - 1;
+// nobody touches it during kernel k).  Each buffer has its own touched-block
+// flags and list; the list of the P2G written by kernel k counts in cnt[k & 3]
+// (kernel k resets cnt[(k + 1) & 3], which kernel k - 1 read last).  cnt[4]
+// counts finished CTAs: the last one advances the step counter.
+struct RotGrid {
+  float4* buf[3] = {nullptr, nullptr, nullptr};
+  int* flags = nullptr;             // [3][total_blocks]
+  int* list = nullptr;              // [3][total_blocks]
+  int* cnt = nullptr;               // [8]
+  int64_t total_blocks = 0;
+};
+
 struct PipelineBuffers {
   // binning: block key per particle slot, per-block counts,
   // start offsets (exclusive scan), scatter cursors, permutation, active list
@@ -37,6 +54,9 @@ struct PipelineBuffers {
   int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
   int* nsf_done = nullptr;          // reduced path: CTA completion counter of the G2P kernel
+  bool rot = false;                 // fused pipeline with the in-kernel grid update (RotGrid)
+  float4* grid3 = nullptr;          // its third grid accumulator
+  RotGrid rg;
   float4* dbg_acc = nullptr;        // reduced path: scratch grids for debug_grid
   unsigned long long* fx = nullptr; // deterministic mode: fixed-point P2G accumulator [total_nodes][4]
   float4* dbg_vel = nullptr;
@@ -61,6 +81,7 @@ struct HandleView {
   DevErr* err;
   int64_t* d_step;
   int cur;                          // current particle buffer
+  int64_t host_step;                // substeps enqueued since load
   const MlpDev* mlp;
   const float* X;
   const float* z;
@@ -112,7 +133,8 @@ void launch_p2g_tiled(cudaStream_t st, const float* S, int64_t pitch, const int3
 void launch_grid_update_blocks(cudaStream_t st, const PipelineBuffers* pb, float4* acc, float4* vel,
                                const DevParams& P, const int64_t* d_step);
 void p2g_tables_init(cudaStream_t st);
-void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const float4* vel, float4* acc, PipelineBuffers* pb,
+void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, const float4* vel, float4* acc,
+                  PipelineBuffers* pb,
                   const DevParams& P, DevErr* err, int64_t* d_step);
 void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
                               const int64_t* d_step);

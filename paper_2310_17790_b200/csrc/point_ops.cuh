@@ -20,8 +20,9 @@ __device__ __forceinline__ void flag_error(DevErr* err, uint32_t bit, int idx) {
   atomicMin(&err->first_index, idx);
 }
 
+// (a NaN coordinate counts as in the region: it is reported as non-finite)
 __device__ __forceinline__ bool in_safe_region(float t, int N) {
-  return t >= 0.5f && t < (float)N - 1.5f;
+  return !(t < 0.5f || t >= (float)N - 1.5f);
 }
 
 // clamp a base index so that base..base+2 stays inside [0, N)

@@ -207,10 +207,10 @@ nsf_status check_device_errors(nsf_mpm* h) {
   CK(cudaStreamSynchronize(h->stream));
   const DevErr& e = *h->err_host;
   if (e.bits & ERR_OUT_OF_DOMAIN)
-    return fail(h, NSF_ERR_OUT_OF_DOMAIN, "particle (slot) %d left the safe region x/dx in [0.5, N-1.5) "
+    return fail(h, NSF_ERR_OUT_OF_DOMAIN, "particle %d (load order) left the safe region x/dx in [0.5, N-1.5) "
                 "by substep %lld", e.first_index, (long long)h->host_step);
   if (e.bits & ERR_NONFINITE)
-    return fail(h, NSF_ERR_NONFINITE, "non-finite state at particle (slot) %d by substep %lld",
+    return fail(h, NSF_ERR_NONFINITE, "non-finite state at particle %d (load order) by substep %lld",
                 e.first_index, (long long)h->host_step);
   return NSF_OK;
 }
@@ -467,11 +467,15 @@ nsf_status nsf_mpm_load_particles(nsf_mpm* h, int64_t n, const float* x, const f
   h->host_step = 0;
   CK(cudaMemcpyAsync(h->err_host, h->err, sizeof(DevErr), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  if (h->err_host->bits & ERR_OUT_OF_DOMAIN) {
-    int idx = h->err_host->first_index;
+  if (h->err_host->bits & (ERR_OUT_OF_DOMAIN | ERR_NONFINITE)) {
+    const int idx = h->err_host->first_index;
+    const bool nonfinite = h->err_host->bits & ERR_NONFINITE;
     reset_errors(h);
     h->loaded = false;
-    return fail(h, NSF_ERR_OUT_OF_DOMAIN, "particle %d is outside the safe region x/dx in [0.5, N-1.5)", idx);
+    if (nonfinite)
+      return fail(h, NSF_ERR_NONFINITE, "particle %d (load order): non-finite x, v, C, F or tau(F)", idx);
+    return fail(h, NSF_ERR_OUT_OF_DOMAIN, "particle %d (load order) is outside the safe region x/dx in [0.5, N-1.5)",
+                idx);
   }
   if ((s = pipeline_on_load(h, &h->pb)) != NSF_OK) return s;
   h->loaded = true;
@@ -1048,6 +1052,7 @@ HandleView view(nsf_mpm* h) {
   v.err = h->err;
   v.d_step = h->d_step;
   v.cur = h->cur;
+  v.host_step = h->host_step;
   v.mlp = &h->mlp;
   v.X = h->X;
   v.z = h->z;

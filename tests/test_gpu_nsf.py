@@ -129,6 +129,8 @@ def test_reduced_full_size_sampled(nsf):
                                      sc.z0[s:s + 1], sc.dz[s:s + 1], step=3, tau_override=s1["tau"][a:b])
         assert rel_err(s1["x"][a:b], ref["x"]) <= BAR_STEP
         assert rel_err(s1["v"][a:b], ref["v"], 9.8 * sc.cfg.dt) <= BAR_STEP
+        vmax = float(np.max(np.linalg.norm(ref["v"], axis=1)))
+        assert rel_err(s1["C"][a:b], ref["C"], vmax * sc.cfg.grid_res) <= BAR_STEP
 
 
 def test_reduced_zero_network_free_fall(nsf):
