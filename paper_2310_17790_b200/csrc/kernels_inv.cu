@@ -269,11 +269,8 @@ void launch_gn_invert(cudaStream_t st, int64_t n, const int32_t* ids, const int6
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = ((int64_t)n_scenes * n_sample + (inv::kRows / rp) - 1) / (inv::kRows / rp);
   const int grid = (int)(tiles < sms ? tiles : sms);
-  static int force_simt = -1;
-  if (force_simt < 0) {
-    const char* e = getenv("NSF_GN_SIMT");
-    force_simt = (e && e[0] != '0') ? 1 : 0;
-  }
+  const char* e = getenv("NSF_GN_SIMT");   // read per call (tests run both passes)
+  const int force_simt = (e && e[0] != '0') ? 1 : 0;
   const bool tc = !force_simt && gn_tc_supported(g, r);
   for (int it = 0; it < n_iters; ++it) {
     if (tc) launch_gn_tc(st, n_scenes, n_sample, r, slots, S, zw, g, accum);

@@ -6,19 +6,11 @@ same state must match the bf16-emulating oracle's step far more closely than bf1
 rounding itself perturbs it (see the bars below).
 Several iterations converge to within the bf16 noise floor of the generating
 latent, as the oracle does."""
-import os
-import sys
-
 import numpy as np
 import pytest
 
-import scenes
 from oracle.inversion import g_with_tangents, invert_scenes
-
-
-
-def deformation_net(seed):
-    return scenes.deformation_field(seed)
+from tests.inv_util import fp32_spread, inversion_scene
 
 pytestmark = pytest.mark.gpu
 
@@ -33,17 +25,7 @@ def nsf():
 
 
 def _scene(n_scenes=3, per_scene=256, seed=3):
-    gnet = deformation_net(77)
-    sc = scenes.c5_small(n_scenes=n_scenes, per_scene=per_scene)
-    rng = np.random.default_rng(seed)
-    z_star = rng.normal(size=(n_scenes, 6)).astype(np.float32)
-    x = sc.x.copy()
-    for s, (a, b) in enumerate(zip(sc.scene_offsets[:-1], sc.scene_offsets[1:])):
-        x[a:b], _ = g_with_tangents(sc.X_ref[a:b], z_star[s], gnet, "emulate")
-    sc.x = x.astype(np.float32)
-    sc.z0 = (z_star + 0.1 * rng.normal(size=z_star.shape)).astype(np.float32)
-    sc.dz = np.zeros_like(sc.z0)
-    return sc, gnet, z_star
+    return inversion_scene(n_scenes, per_scene, seed)
 
 
 def _invert(nsf, sc, gnet, n_sample, iters, substeps=0):
@@ -57,21 +39,40 @@ def _invert(nsf, sc, gnet, n_sample, iters, substeps=0):
     return zg, st["x"]
 
 
-@pytest.mark.parametrize("n_sample", [64, 50])
-def test_one_gauss_newton_step_matches_oracle(nsf, n_sample):
-    """The Gauss-Newton step of a random bf16 network is very sensitive to rounding:
-    the bf16-emulating oracle's step differs from the unrounded one by 15-40% of its
-    length.  The GPU (tensor-core pass, ex2-based ELU) must match the emulating
-    oracle within 10% of the step and within a quarter of that intrinsic gap
-    (observed ~4.5% and ~0.1)."""
+def _objective(sc, gnet, x, z, n_sample):
+    f = 0.0
+    for s_, (a, b) in enumerate(zip(sc.scene_offsets[:-1], sc.scene_offsets[1:])):
+        m = min(n_sample, int(b - a))
+        g, _ = g_with_tangents(sc.X_ref[a:a + m], np.asarray(z[s_], np.float64), gnet, "emulate")
+        f += float(np.sum((g - x[a:a + m]) ** 2))
+    return f
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("n_sample", [64, 50, 256])
+def test_one_gauss_newton_step_matches_oracle(nsf, n_sample, simt, monkeypatch):
+    """One Gauss-Newton step (tensor-core pass, or the CUDA-core pass) vs the
+    bf16-emulating oracle (reading #37).  The step of this random bf16
+    network is ill-conditioned: bf16 rounding alone moves it by 15-50% of its
+    length, and a correct fp32 evaluation of the same emulating network moves it
+    by 0.6-12% depending only on the summation order (tests/inv_util.py).  Bars:
+    (1) the GPU step deviates from the oracle's by no more than the largest of 8
+    such fp32 evaluations (floor 1e-2), and by <= 1/4 of the emulate-vs-exact gap;
+    (2) it reduces the objective of Eq. (10) by the oracle step's reduction to
+    within 1e-2 (the well-conditioned quantity)."""
+    if simt:
+        monkeypatch.setenv("NSF_GN_SIMT", "1")
     sc, gnet, _ = _scene()
     zg, x = _invert(nsf, sc, gnet, n_sample, 1)
     z0 = sc.z0.astype(np.float64)
     zo = invert_scenes(sc.X_ref, x, sc.scene_offsets, n_sample, z0, gnet, 1, "emulate")
-    ze = invert_scenes(sc.X_ref, x, sc.scene_offsets, n_sample, z0, gnet, 1, "exact")
+    spread, gap = fp32_spread(sc, gnet, x, z0, n_sample, orders=8)
     step = np.linalg.norm(zo - z0)
-    assert np.linalg.norm(zg - zo) <= 0.1 * step
-    assert np.linalg.norm(zg - zo) <= 0.25 * np.linalg.norm(ze - zo)
+    dev = np.linalg.norm(zg - zo) / step
+    assert dev <= max(1e-2, spread), (dev, spread)
+    assert dev <= 0.25 * gap, (dev, gap)
+    f0, fo, fg = (_objective(sc, gnet, x, z, n_sample) for z in (z0, zo, zg))
+    assert abs(fg - fo) <= 1e-2 * (f0 - fo), (f0, fo, fg)
 
 
 def test_inversion_after_substeps_uses_the_current_latent(nsf):

@@ -52,9 +52,84 @@ def test_mlp_vs_torch_fp64():
             a = torch.nn.functional.linear(inp, W, b)
             h = torch.nn.functional.elu(a) if k < L - 1 else a
         ours = mlp_forward(u, mlp["W"], mlp["b"], mode)
-        # torch rounds fp64 -> fp32 -> bf16 (double rounding); allow rare tie flips
-        tol = 1e-12 if mode == "exact" else 1e-2
-        assert np.allclose(ours, h.numpy(), rtol=tol, atol=tol)
+        if mode == "exact":
+            assert np.allclose(ours, h.numpy(), rtol=1e-12, atol=1e-12)
+        else:
+            # torch rounds fp64 -> fp32 -> bf16 (double rounding), so only the coarse
+            # agreement is checked here; test_mlp_emulate_rounding_points_exact pins
+            # the emulate mode exactly against a bit-level single rounding
+            assert np.allclose(ours, h.numpy(), rtol=1e-2, atol=1e-2)
+
+
+def _bf16_rne_bits(t):
+    """Independent fp64 -> bf16 round-to-nearest-even on the IEEE bit pattern:
+    keep the sign, exponent and top 7 of the 52 stored mantissa bits, add half an
+    ulp minus one plus the kept lsb, truncate (the carry runs into the exponent as
+    it should).  Also returns, per element, the distance of the dropped bits from
+    the tie point 2^44 (small = a rounding decision within summation-order noise)."""
+    b = t.contiguous().view(torch.int64)
+    drop = b & ((1 << 45) - 1)
+    lsb = (b >> 45) & 1
+    r = (b + ((1 << 44) - 1) + lsb) & ~((1 << 45) - 1)
+    return r.view(torch.float64), (drop - (1 << 44)).abs()
+
+
+def _emulate_torch(u, Ws, bs, where="after_elu", round_input=False):
+    """The emulate-mode MLP (reading #20) in torch fp64 with the rounding points
+    written out: u -> a_1 = W_1 u + b_1 -> h_1 = ELU(a_1) -> r(h_1) -> a_2 ... ->
+    y = W_L r(h_{L-1}) + b_L.  `where` / `round_input` move the rounding points
+    (mutations used to show that the pin below detects them)."""
+    h = torch.from_numpy(np.asarray(u, np.float64))
+    near = torch.full((h.shape[0],), 1 << 62, dtype=torch.int64)
+    L = len(Ws)
+
+    def rnd(t):
+        nonlocal near
+        r, d = _bf16_rne_bits(t)
+        near = torch.minimum(near, d.reshape(t.shape[0], -1).min(dim=1).values)
+        return r
+
+    for k in range(L):
+        W = torch.from_numpy(np.asarray(Ws[k], np.float64))
+        b = torch.from_numpy(np.asarray(bs[k], np.float64))
+        inp = h
+        if (k > 0 and where == "after_elu") or (k == 0 and round_input):
+            inp = rnd(h)
+        a = torch.nn.functional.linear(inp, W, b)
+        if k < L - 1:
+            if where == "before_elu":
+                a = rnd(a)
+            h = torch.nn.functional.elu(a)
+        else:
+            h = a
+    return h.numpy(), near.numpy()
+
+
+def test_mlp_emulate_rounding_points_exact():
+    """The emulate mode's rounding points, pinned exactly: mlp_forward(emulate) equals
+    an independent torch fp64 implementation with a bit-level fp64 -> bf16 RNE to
+    1e-12 on every row whose rounding decisions are not within 2^-40 relative of a
+    tie (summation-order noise could flip those; they must be rare).  Moving a
+    rounding point (before the ELU, on the layer-1 input, or dropping one) changes
+    the result by far more than the pin allows."""
+    sc = scenes.c5_small()
+    Ws, bs = sc.mlp["W"], sc.mlp["b"]
+    rng = np.random.default_rng(7)
+    X = rng.uniform(0.3, 0.7, size=(2000, 3))
+    u = np.concatenate([X, rng.normal(size=(2000, 6))], axis=1)
+    ours = mlp_forward(u, Ws, bs, "emulate")
+    ref, near = _emulate_torch(u, Ws, bs)
+    clean = near > (1 << 12)
+    assert clean.mean() >= 0.99, clean.mean()
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(ours[clean] - ref[clean])) <= 1e-12 * scale
+    # the round_bf16 used by the oracle agrees with the bit-level rounding everywhere
+    t = torch.from_numpy(rng.normal(size=100000) * np.exp(rng.normal(size=100000) * 5))
+    assert np.array_equal(round_bf16(t.numpy()), _bf16_rne_bits(t)[0].numpy())
+    # sensitivity: each misplaced rounding point moves the output by >> 1e-12
+    for kw in ({"where": "before_elu"}, {"round_input": True}, {"where": "none"}):
+        mut, _ = _emulate_torch(u, Ws, bs, **kw)
+        assert np.max(np.abs(mut - ref)) > 1e-6 * scale, kw
 
 
 def test_mlp_special_cases():
