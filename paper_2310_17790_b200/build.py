@@ -20,6 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libnsf_mpm.so")
+LIB_CHECKED = os.path.join(PKG, "libnsf_mpm_checked.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -53,7 +54,18 @@ def _compile(src: str, force: bool, log: list) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: the bounds-checked variant libnsf_mpm_checked.so (-DNSF_CHECKED=1,
+    csrc/params.cuh NSF_CHECK), used by tests/test_gpu_checked.py only."""
+    global BUILD, LIB, NVCC_FLAGS
+    if checked:
+        saved = (BUILD, LIB, NVCC_FLAGS)
+        BUILD, LIB = BUILD + "_checked", LIB_CHECKED
+        NVCC_FLAGS = NVCC_FLAGS + ["-DNSF_CHECKED=1"]
+        try:
+            return build(force, verbose)
+        finally:
+            BUILD, LIB, NVCC_FLAGS = saved
     os.makedirs(BUILD, exist_ok=True)
     stamp = os.path.join(BUILD, "flags.txt")     # a change of flags (NSF_DEFINES) forces a rebuild
     flags = " ".join(NVCC_FLAGS)
@@ -82,4 +94,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

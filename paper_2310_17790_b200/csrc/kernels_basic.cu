@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
     if (packed != kNoBase) {   // previous stencil, in the accumulator P2G(step + 1) will use
       const int pb_[3] = {packed >> 20, (packed >> 10) & 1023, packed & 1023};
       stencil_offsets(pb_, P, X, Y, Z);
+      NSF_CHECK(X[0] + Y[0] + Z[0] >= 0 && X[2] + Y[2] + Z[2] < P.nodes_per_scene && pb_[0] + 2 < P.N[0] &&
+                pb_[1] + 2 < P.N[1] && pb_[2] + 2 < P.N[2]);
       float4* clr = ((step & 1) ? acc0 : acc1) + so;
       // each z-run of 3 nodes as a 32-byte pair at an even node index plus one node
       const int zp = pb_[2] & 1;
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
         }
     }
     stencil_offsets(base, P, X, Y, Z);
+    NSF_CHECK(X[0] + Y[0] + Z[0] >= 0 && X[2] + Y[2] + Z[2] < P.nodes_per_scene);
     const float4* ab = ((step & 1) ? acc1 : acc0) + so;
     // interior stencil (no wall band, no plate): the node update is v = mv/m + dt g
     bool simple = !(P.plate_enabled && (float)(base[1] + 2) * P.dx >= y_pl);

@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(128) k_copy_cells(int64_t n, const float* __re
   const int id = __ldcs(ids_in + j);
   const int cell = cell_of_x(v[PX + 0], v[PX + 1], v[PX + 2], P);
   const int64_t dst = cellcnt[64 * ne_of[keys[j]] + cell] + rank[j];
+  NSF_CHECK(dst >= 0 && dst < n);
   float* dp = Sout + pbase(dst);
 #pragma unroll
   for (int k = 0; k < kPlanes; ++k) dp[k * 32] = v[k];

@@ -163,8 +163,13 @@ __device__ __forceinline__ void p2g_stage_values(const float x[3], const float v
 // block, and for cells with more than kRows particles)
 // mark grid block `b` as touched; the first marker appends it to the work list of
 // the next grid update
-__device__ __forceinline__ void touch_block(int* flags, int* list, int* list_count, int b) {
-  if (flags[b] == 0 && atomicExch(&flags[b], 1) == 0) list[atomicAdd(list_count, 1)] = b;
+__device__ __forceinline__ void touch_block(int* flags, int* list, int* list_count, int b, const DevParams& P) {
+  NSF_CHECK(b >= 0 && b < P.blocks_per_scene * P.n_scenes);
+  if (flags[b] == 0 && atomicExch(&flags[b], 1) == 0) {
+    const int e = atomicAdd(list_count, 1);
+    NSF_CHECK(e < P.blocks_per_scene * P.n_scenes);
+    list[e] = b;
+  }
 }
 
 __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float v[3], const float Cm[9],
@@ -192,6 +197,7 @@ __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float
         const float mv0 = W * (m * v[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
         const float mv1 = W * (m * v[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
         const float mv2 = W * (m * v[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
+        NSF_CHECK(node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P) < P.nodes_per_scene);
         red_add_v4_t(gbase + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
       }
   // touched blocks: per axis the blocks of base and base+2
@@ -202,7 +208,7 @@ __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int b0 = (ax[0].base + 2 * a) >> 2, b1 = (ax[1].base + 2 * b) >> 2, b2 = (ax[2].base + 2 * c) >> 2;
-        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
       }
 }
 
@@ -251,13 +257,14 @@ __device__ __forceinline__ void p2g_scatter_warp(bool direct, const float x[3], 
       const float mv0 = W * (m * pv[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
       const float mv1 = W * (m * pv[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
       const float mv2 = W * (m * pv[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
+      NSF_CHECK(node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P) < P.nodes_per_scene);
       red_add_v4_t(gbase + node_index(ax[0].base + a, ax[1].base + b, ax[2].base + c, P), W * m, mv0, mv1, mv2);
     }
     // touched blocks: per axis the blocks of base and base+2
     for (int k = r; k < 8; k += nact) {
       const int b0 = (ax[0].base + 2 * (k >> 2)) >> 2, b1 = (ax[1].base + 2 * ((k >> 1) & 1)) >> 2,
                 b2 = (ax[2].base + 2 * (k & 1)) >> 2;
-      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
     }
   }
 }
@@ -894,6 +901,8 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
   Axis ax[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) ax[a] = bspline_axis(x[a], P.inv_dx);
+  NSF_CHECK(ax[0].base - o[0] >= 0 && ax[0].base - o[0] <= kVT - 3 && ax[1].base - o[1] >= 0 &&
+            ax[1].base - o[1] <= kVT - 3 && ax[2].base - o[2] >= 0 && ax[2].base - o[2] <= kVT - 3);
   const float4* tp = vt + (ax[0].base - o[0]) * kVTx + (ax[1].base - o[1]) * kVTy + (ax[2].base - o[2]);
   float wyz[9];
 #pragma unroll
@@ -1108,11 +1117,12 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
       const float ux = fmaf(fc, s[18], fmaf(fb, s[15], fmaf(fa, s[12], s[9])));
       const float uy = fmaf(fc, s[19], fmaf(fb, s[16], fmaf(fa, s[13], s[10])));
       const float uz = fmaf(fc, s[20], fmaf(fb, s[17], fmaf(fa, s[14], s[11])));
+      NSF_CHECK(node_index(bx + a, by + b, bz + c, P) < P.nodes_per_scene);
       red_add_v4_t(gacc + node_index(bx + a, by + b, bz + c, P), W * P.mass, W * ux, W * uy, W * uz);
     } else {
       const int k = q - 27;
       const int b0 = (bx + 2 * (k >> 2)) >> 2, b1 = (by + 2 * ((k >> 1) & 1)) >> 2, b2 = (bz + 2 * (k & 1)) >> 2;
-      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
     }
   }
 }
@@ -1161,6 +1171,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         const int e = (int)blockIdx.x + (i >> 6) * (int)gridDim.x;
         if (e >= nz) break;
         const int key = zl[e];
+        NSF_CHECK(nz <= TB && key >= 0 && key < TB);
         zbuf[(int64_t)key * kBlockNodes + (i & 63)] = make_float4(0.f, 0.f, 0.f, 0.f);
         if ((i & 63) == 0) zf[key] = 0;
       }
@@ -1270,6 +1281,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       }
       bool inline_scatter = false;
       if (rank < ROWS) {
+        NSF_CHECK(cell >= 0 && cell < 64 && (cell + 1) * FusedSlots<ROWS>::kCellStride4 > rank * kRowF4 + 5);
         p2g_stage_row(xn, vn, Cn, tau, sm.slot + cell * FusedSlots<ROWS>::kCellStride4 + rank * kRowF4, P);
       } else {
         const int e = atomicAdd(&sm.nsc, 1);
@@ -1317,13 +1329,14 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       for (int k = 0; k < 9; ++k) {
         const int gj = cy + k / 3, gk = cz + k % 3;
         const int off = x_part + ((gj >> 2) * P.NB[2] + (gk >> 2)) * kBlockNodes + ((gj & 3) << 2) + (gk & 3);
+        NSF_CHECK(off >= 0 && off < P.nodes_per_scene);
         red_add_v4_t(gacc + off, accm[k] * m, accp[k][0], accp[k][1], accp[k][2]);
       }
     }
     if (tid < 8) {
       const int b0 = bc.b[0] + (tid >> 2), b1 = bc.b[1] + ((tid >> 1) & 1), b2 = bc.b[2] + (tid & 1);
       if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])
-        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)));
+        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
     }
   }
   if (ROT && tid == 0) {
@@ -1367,8 +1380,10 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
   const int nl = s ? c1 : c0;
   const float y_plate = plate_y_at(P, n);
   const int bps = (int)P.blocks_per_scene;
+  NSF_CHECK(nl >= 0 && nl <= P.blocks_per_scene * P.n_scenes);
   for (int e = warp; e < nl; e += nwarps) {
     const int key = key_next;
+    NSF_CHECK(key >= 0 && key < P.blocks_per_scene * P.n_scenes);
     if (e + nwarps < nl) key_next = list[e + nwarps];
     const int scene = key / bps;
     const BlockCoord bc = decode_block(key, P);

@@ -6,6 +6,30 @@
 //   particles: SoA component planes, float32, each plane `pitch` floats long.
 #pragma once
 #include <cstdint>
+#include <cstdio>
+
+// Device-side bounds checks of the checked build (libnsf_mpm_checked.so, built
+// with -DNSF_CHECKED=1; tests/test_gpu_checked.py): every shared-memory slot,
+// grid node, block id and list index the kernels write is asserted in range and a
+// violation traps the kernel (the pool offers no compute-sanitizer).  Compiled out
+// of the product library.
+#ifndef NSF_CHECKED
+#define NSF_CHECKED 0
+#endif
+#if NSF_CHECKED
+#define NSF_CHECK(cond)                                                                  \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("NSF_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define NSF_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 namespace nsf {
 

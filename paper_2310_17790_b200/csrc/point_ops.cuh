@@ -138,6 +138,7 @@ __device__ __forceinline__ void nsf_p2g_point(const NsfP2G& q, int scene, const 
         const float mv0 = W * (m * vp[0] + Q[0] * d0 + Q[1] * d1 + Q[2] * d2);
         const float mv1 = W * (m * vp[1] + Q[3] * d0 + Q[4] * d1 + Q[5] * d2);
         const float mv2 = W * (m * vp[2] + Q[6] * d0 + Q[7] * d1 + Q[8] * d2);
+        NSF_CHECK(X[a] + Y[b] + Z[c] >= 0 && X[a] + Y[b] + Z[c] < P.nodes_per_scene);
         red_add_v4(out + (X[a] + Y[b] + Z[c]), W * m, mv0, mv1, mv2);
       }
 }

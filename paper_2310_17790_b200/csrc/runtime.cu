@@ -1030,6 +1030,15 @@ int64_t nsf_mpm_launch_count(const nsf_mpm* h) {
   return pipeline_launch_total(const_cast<nsf_mpm*>(h), const_cast<PipelineBuffers*>(&h->pb));
 }
 
+#if NSF_CHECKED
+// checked build only: a kernel whose NSF_CHECK fails, to show the checks trap
+__global__ void k_checked_selftest(int v) { NSF_CHECK(v == 0); }
+int32_t nsf_mpm_checked_selftest(int32_t fail) {
+  k_checked_selftest<<<1, 1>>>(fail);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
+#endif
+
 }  // extern "C"
 
 // ---- accessors used by the pipeline (pipeline.cu) -----------------------------

@@ -1,11 +1,15 @@
-"""Small end-to-end runs for compute-sanitizer (memcheck / racecheck / synccheck).
+"""Small end-to-end runs of the hot path for the bounds-checked library build.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_run.py c1_spin
-Scenes: c1_spin (fused full-order path, 40 substeps: crosses a re-binning),
-dense_cluster (~90 particles per cell: several staged rounds, >1 segment per
-block, scatter-list overflow), c5_small (reduced path: tcgen05 MLP + P2G
-epilogue, reduced G2P, re-binning), det (deterministic fixed-point path),
-gradw (split pipeline).  Prints one line per scene; exits non-zero on an API error.
+    NSF_MPM_LIB=paper_2310_17790_b200/libnsf_mpm_checked.so python tools/checked_run.py c1_spin
+(tests/test_gpu_checked.py runs it).  compute-sanitizer is closed on the GPU pool
+(runs under it left GPUs needing a reset), so memory safety is checked by the
+library's own device asserts (NSF_CHECK, csrc/params.cuh) on these scenes:
+c1_spin (fused full-order path, 40 substeps: crosses a re-binning), dense_cluster
+(~90 particles per cell: several staged rounds, >1 segment per block, scatter-list
+overflow), c5_small (reduced path: tcgen05 MLP + P2G epilogue, reduced G2P,
+re-binning), det (deterministic fixed-point path), gradw (split pipeline), sparse
+(the sparse fused variant).  Prints one line per scene; a failed check traps the
+kernel and the next call raises NSF_ERR_CUDA.
 """
 import os
 import sys
@@ -41,6 +45,9 @@ def run(name, steps):
     elif name == "det":
         sc = scenes.c1_spin()
         sc.cfg.deterministic = 1
+    elif name == "sparse":
+        os.environ["NSF_FUSED_VARIANT"] = "sparse"
+        sc = scenes.c1_spin()
     elif name == "gradw":
         sc = scenes.block_scene("FCg", 32, (9, 6, 10), (20, 15, 19), scenes.FIXED_COROTATED, 14,
                                 keep=3333, vnoise=0.3, Fnoise=0.02, Cnoise=3.0, force_mode=scenes.FORCE_GRADW)
