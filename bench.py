@@ -12,9 +12,17 @@ quoted on.  Inputs are synthetic and seeded (scenes/), resident in HBM when
 the timed region starts; the state (2 x 120 MB) and the bytes moved per
 substep (~268 MB) exceed the 126 MB L2, so no explicit flush is needed.
 
+Timed window: the scene is first advanced --preroll substeps (default: half the
+config's run, e.g. C3 to substep 250 of 500) and warmed up outside the timed
+region; the window is then placed so that it contains the periodic re-binning at
+least at its true rate (one every 32 substeps; a 20-substep window holds one).
+L2 is flushed before every timed substep by READING a 256 MB buffer (a write
+flush would leave dirty lines to be written back inside the next substep).
+
 Multi-GPU: replicas only: each rank simulates its own
 replica of the workload, no data-path collective; value = all particles x K /
-max-over-ranks time; "scaling": "weak".
+max-over-ranks time; "scaling": "weak".  `--gpus N` without a torchrun
+environment re-launches itself under torch.distributed.run with N ranks.
 
 --impl reference: the fp64 CPU oracle (oracle/, test infrastructure), timed on
 the host cores, each step one oracle substep on a bounded contiguous sample of
@@ -69,6 +77,7 @@ STEP_DESC = {
           "(+ re-binning every 32)",
 }
 L2_FLUSH_BYTES = 256 << 20              # > 2x the 126 MB L2
+REBIN_EVERY = int(os.environ.get("NSF_REBIN_EVERY", "32"))   # the library's re-binning period (pipeline.cu)
 B_ALG_PER_PARTICLE_SUBSTEP = 268.0   # 84 + 48 + 120 + 16
 
 
@@ -204,11 +213,25 @@ def run_reference(args):
                        "step": STEP_DESC[args.config == "C5"],
                        "sample": f"first {S} particles (cell order) of the workload, one oracle substep per step"},
             "cpu_baseline": {"value": value, "unit": "particle-substeps/s", "cores": 1, "kind": "oracle",
+                             "cpu_model": host_cpu()[0], "nproc": host_cpu()[1],
                              "sample": f"{S} particles x {args.steps} substeps"},
             "e2e": {"value": value, "unit": "particle-substeps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
+
+
+def host_cpu():
+    """CPU model and logical core count of the machine running the oracle legs."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
 
 
 def cpu_baseline(sc, budget_s=15.0, sample=50000):
@@ -238,7 +261,9 @@ def cpu_baseline(sc, budget_s=15.0, sample=50000):
         if time.perf_counter() - t0 > budget_s or k >= 50:
             break
     dt = time.perf_counter() - t0
+    model, nproc = host_cpu()
     return {"value": S * k / dt, "unit": "particle-substeps/s", "cores": 1, "kind": "oracle",
+            "cpu_model": model, "nproc": nproc,
             "sample": f"first {S} particles of the workload x {k} substeps ({dt:.1f} s, fp64 numpy, 1 thread)"}
 
 
@@ -268,9 +293,20 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     sim = nsf.Simulator(sc.cfg, stream=stream.cuda_stream)
     sim.load_scene(sc)            # state (+ MLP and latents for C5) resident in HBM
-    # warm-up (also captures the CUDA graph)
-    sim.substep(args.warmup)
+    # state preparation outside the timed region: pre-roll to mid-run, warm-up (also
+    # captures the CUDA graphs), then extra untimed substeps so that the re-binning
+    # substeps (indices 31, 63, ... since the load) fall inside the timed window at
+    # least at their true rate (the middle of the window is one)
+    preroll = sc.cfg.substeps // 2 if args.preroll < 0 else args.preroll
+    s0 = preroll + args.warmup
+    align = 0
+    if REBIN_EVERY > 0:
+        mid = s0 + args.steps // 2
+        align = (REBIN_EVERY - 1 - mid) % REBIN_EVERY
+    sim.substep(s0 + align)
     sim.sync()
+    window = (s0 + align, s0 + align + args.steps)
+    rebins_in_window = sum(1 for i in range(*window) if (i + 1) % REBIN_EVERY == 0) if REBIN_EVERY > 0 else 0
 
     def barrier():
         torch.cuda.synchronize()
@@ -280,17 +316,23 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     # ---- timed region: K substeps, inputs resident in HBM ----
-    # L2 (126 MB) is flushed before every timed substep by a 256 MB write on the
-    # same stream, outside the substep's own event pair; the K per-substep device
-    # times are summed.
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    # L2 (126 MB) is flushed before every timed substep by reading a 256 MB buffer
+    # on the same stream, outside the substep's own event pair (reading evicts and
+    # writes back the substep's dirty lines there; a write flush would leave its own
+    # dirty lines to be written back inside the timed substep); the K per-substep
+    # device times are summed.
+    flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    flush_out = torch.empty((), dtype=torch.float32, device=dev)
+
+    def l2_flush():
+        with torch.cuda.stream(stream):
+            torch.sum(flush, dim=0, out=flush_out)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     with ClockSampler(local) as clk:
         launches0 = nsf.nsf_mpm_launch_count(sim.h)
         for a, b in ev:
-            with torch.cuda.stream(stream):
-                flush.fill_(1.0)
+            l2_flush()
             a.record(stream)
             sim.substep(1)
             b.record(stream)
@@ -306,8 +348,7 @@ def run_ours(args):
     # ---- per-kernel timing pass (CUDA events around each launch, same stream) ----
     nsf.nsf_mpm_set_profiling(sim.h, True)
     for _ in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.fill_(1.0)
+        l2_flush()
         sim.substep(1)
     sim.sync()
     kt = nsf.nsf_mpm_kernel_times(sim.h)
@@ -453,8 +494,14 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (scenes/, seeded)",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}",
                        "particles_per_gpu": n, "grid": sc.cfg.grid_res, "dt": sc.cfg.dt,
-                       "replicas": world, "deterministic": bool(sc.cfg.deterministic), "l2": "flushed before every timed substep (256 MB write outside the per-substep CUDA events)",
-                       "step": STEP_DESC[args.config == "C5"]},
+                       "replicas": world, "deterministic": bool(sc.cfg.deterministic),
+                       "l2": "flushed before every timed substep (256 MB read outside the per-substep CUDA events)",
+                       "step": STEP_DESC[args.config == "C5"],
+                       "window": {"first_substep": window[0], "preroll": preroll, "warmup": args.warmup,
+                                  "rebin_every": REBIN_EVERY, "rebins_in_window": rebins_in_window,
+                                  "note": "state prepared outside the timed region: the scene is advanced to "
+                                          "substep first_substep (pre-roll + warm-up + alignment), so the "
+                                          "window holds the periodic re-binning at least at its true rate"}},
             "hbm_alg_gbs_whole_step": step_gbs,
             "hbm_alg_frac_whole_step": step_gbs / peak,
             "roofline": roof,
@@ -481,6 +528,19 @@ def run_ours(args):
     return 0
 
 
+def spawn(n):
+    """`--gpus N` outside torchrun: re-launch this command under torch.distributed.run
+    with N ranks on this node (rendezvous on 127.0.0.1); rank 0 prints the line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -493,9 +553,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--deterministic", action="store_true",
                     help="fixed-point (bitwise reproducible) P2G; reported in config")
+    ap.add_argument("--preroll", type=int, default=-1,
+                    help="untimed substeps before warm-up (default: half the config's substeps)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
