@@ -894,8 +894,18 @@ __device__ __forceinline__ void cp_async16_f(void* smem, const void* gmem, int s
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
 }
 
+#ifndef NSF_F2_G2P
+#define NSF_F2_G2P 1   // G2P gather on paired fp32 FMA (FFMA2, sm_100)
+#endif
+#ifndef NSF_F2_P2G
+#define NSF_F2_P2G 1   // P2G accumulation on paired fp32 FMA / MUL / ADD (sm_100)
+#endif
+
 // G2P gather (MLS) from the shared 8^3 velocity tile whose node (0,0,0) is grid
 // node o[]; the 27 reads are one shared base address plus immediate offsets.
+// NSF_F2_G2P: the x, y components of every sum run as one paired FMA (the weight is a
+// broadcast scalar operand, the pair is the node's (v_x, v_y) straight from its
+// 16-byte shared load); the same operations per component as the scalar form.
 __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* vt, const int o[3], const DevParams& P,
                                                 float v[3], float Cn[9]) {
   Axis ax[3];
@@ -909,6 +919,52 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
   for (int b = 0; b < 3; ++b)
 #pragma unroll
     for (int c = 0; c < 3; ++c) wyz[b * 3 + c] = ax[1].w[b] * ax[2].w[c];
+#if NSF_F2_G2P
+  // M[i][j] = sum W v_i o_j as pairs over i = (x, y) plus the z scalar
+  float2 v01 = make_float2(0.f, 0.f), M01[3] = {v01, v01, v01};
+  float v2 = 0.f, M2[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float2 T01 = make_float2(0.f, 0.f), Ty01 = T01, Tz01 = T01;
+    float T2 = 0.f, Ty2 = 0.f, Tz2 = 0.f;
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float4 vi = tp[a * kVTx + b * kVTy + c];
+        const float2 vxy = make_float2(vi.x, vi.y);
+        const float wgt = wyz[b * 3 + c];
+        T01 = __ffma2_rn(make_float2(wgt, wgt), vxy, T01);
+        T2 = fmaf(wgt, vi.z, T2);
+        if (b) {
+          const float wb = (float)b * wgt;
+          Ty01 = __ffma2_rn(make_float2(wb, wb), vxy, Ty01);
+          Ty2 = fmaf(wb, vi.z, Ty2);
+        }
+        if (c) {
+          const float wc = (float)c * wgt;
+          Tz01 = __ffma2_rn(make_float2(wc, wc), vxy, Tz01);
+          Tz2 = fmaf(wc, vi.z, Tz2);
+        }
+      }
+    const float wx = ax[0].w[a];
+    v01 = __ffma2_rn(make_float2(wx, wx), T01, v01);
+    v2 = fmaf(wx, T2, v2);
+    if (a) {
+      const float awx = (float)a * wx;
+      M01[0] = __ffma2_rn(make_float2(awx, awx), T01, M01[0]);
+      M2[0] = fmaf(awx, T2, M2[0]);
+    }
+    M01[1] = __ffma2_rn(make_float2(wx, wx), Ty01, M01[1]);
+    M2[1] = fmaf(wx, Ty2, M2[1]);
+    M01[2] = __ffma2_rn(make_float2(wx, wx), Tz01, M01[2]);
+    M2[2] = fmaf(wx, Tz2, M2[2]);
+  }
+  v[0] = v01.x; v[1] = v01.y; v[2] = v2;
+  float M[9];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) { M[0 * 3 + j] = M01[j].x; M[1 * 3 + j] = M01[j].y; M[2 * 3 + j] = M2[j]; }
+#else
   float M[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   v[0] = v[1] = v[2] = 0.f;
 #pragma unroll
@@ -939,6 +995,7 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
       M[i * 3 + 2] = fmaf(wx, Tz[i], M[i * 3 + 2]);
     }
   }
+#endif
   const float cC = 4.0f * P.inv_dx;
   const float f[3] = {ax[0].f, ax[1].f, ax[2].f};
 #pragma unroll
@@ -946,6 +1003,15 @@ __device__ __forceinline__ void g2p_gather_tile(const float x[3], const float4* 
 #pragma unroll
     for (int jj = 0; jj < 3; ++jj) Cn[i * 3 + jj] = cC * fmaf(-v[i], f[jj], M[i * 3 + jj]);
 }
+
+// Staged P2G row of one particle (6 float4), laid out so that every pair the
+// paired-FMA accumulation needs sits 8-byte aligned:
+//   [0] w_x0 w_x1 w_x2 w_y0   [1] u_x u_y u_z w_y1   [2] q0_x q0_y q0_z w_y2
+//   [3] q1_x q1_y q1_z w_z2   [4] q2_x q2_y w_z0 w_z1   [5] 0 q2_z base 0
+// u = m v - dx Q f, q_a = dx Q e_a (Q = m C - dt V0 4/dx^2 tau, MLS), base = the
+// packed stencil base (scatter list only).
+enum RowIdx : int { kRwWx = 0, kRwWy0 = 3, kRwU = 4, kRwWy1 = 7, kRwQ0 = 8, kRwWy2 = 11, kRwQ1 = 12, kRwWz2 = 15,
+                    kRwQ2 = 16, kRwWz0 = 18, kRwWz1 = 19, kRwQ2z = 21, kRwBase = 22 };
 
 __device__ __forceinline__ void p2g_stage_row(const float x[3], const float v[3], const float Cm[9], const float T[6],
                                               float4* row, const DevParams& P, float packed_base = 0.0f) {
@@ -957,30 +1023,80 @@ __device__ __forceinline__ void p2g_stage_row(const float x[3], const float v[3]
   for (int k = 0; k < 9; ++k) Q[k] = P.mC * Cm[k] - P.mls_coef * Tm[k];
   const float f0 = a0.f, f1 = a1.f, f2 = a2.f;
   row[0] = make_float4(a0.w[0], a0.w[1], a0.w[2], a1.w[0]);
-  row[1] = make_float4(a1.w[1], a1.w[2], a2.w[0], a2.w[1]);
-  row[2] = make_float4(a2.w[2], m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2),
+  row[1] = make_float4(m * v[0] - P.dx * (Q[0] * f0 + Q[1] * f1 + Q[2] * f2),
                        m * v[1] - P.dx * (Q[3] * f0 + Q[4] * f1 + Q[5] * f2),
-                       m * v[2] - P.dx * (Q[6] * f0 + Q[7] * f1 + Q[8] * f2));
-  row[3] = make_float4(P.dx * Q[0], P.dx * Q[3], P.dx * Q[6], P.dx * Q[1]);
-  row[4] = make_float4(P.dx * Q[4], P.dx * Q[7], P.dx * Q[2], P.dx * Q[5]);
-  row[5] = make_float4(P.dx * Q[8], packed_base, 0.0f, 0.0f);
+                       m * v[2] - P.dx * (Q[6] * f0 + Q[7] * f1 + Q[8] * f2), a1.w[1]);
+  row[2] = make_float4(P.dx * Q[0], P.dx * Q[3], P.dx * Q[6], a1.w[2]);
+  row[3] = make_float4(P.dx * Q[1], P.dx * Q[4], P.dx * Q[7], a2.w[2]);
+  row[4] = make_float4(P.dx * Q[2], P.dx * Q[5], a2.w[0], a2.w[1]);
+  row[5] = make_float4(0.0f, P.dx * Q[8], packed_base, 0.0f);
 }
 
 // Thread (cell, ox): sums, over the cell's staged rows, the P2G contributions to
 // its 9 nodes (ox, oy, oz) -- mass weight and affine momentum W (u + ox q0 + oy q1 + oz q2).
+// NSF_F2_P2G: (p_x, p_y) of each node is one paired FMA with the node weight as a
+// broadcast operand; the z momenta and the masses of nodes oz = 0, 1 of a row pair
+// up across the two nodes (weights (W_0, W_1) from one paired multiply); every
+// lane performs the scalar form's operation, so the sums are the same.
 template <int ROWS>
 __device__ __forceinline__ void p2g_accumulate_rows(const float4* slot, int my_cell, int ox, int rows, float accm[9],
                                                     float accp[9][3]) {
   const float fox = (float)ox;
   const float4* rp = slot + my_cell * FusedSlots<ROWS>::kCellStride4;
+#if NSF_F2_P2G
+  float2 pxy[9], pz01[3], m01[3];
+  float pz2[3], m2[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) pxy[k] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { pz01[k] = m01[k] = make_float2(0.f, 0.f); pz2[k] = m2[k] = 0.f; }
   for (int r = 0; r < rows; ++r, rp += kRowF4) {
-    const float4 A = rp[0], B = rp[1], Cv = rp[2], D = rp[3], E = rp[4], G = rp[5];
+    const float4 A = rp[0], U = rp[1], Q0 = rp[2], Q1 = rp[3], Q2 = rp[4], Z = rp[5];
     const float wx = ox == 0 ? A.x : (ox == 1 ? A.y : A.z);
-    const float wyv[3] = {A.w, B.x, B.y};
-    const float wzv[3] = {B.z, B.w, Cv.x};
-    const float ux = fmaf(fox, D.x, Cv.y), uy = fmaf(fox, D.y, Cv.z), uz = fmaf(fox, D.z, Cv.w);
-    const float q1x = D.w, q1y = E.x, q1z = E.y;
-    const float q2x = E.z, q2y = E.w, q2z = G.x;
+    const float wyv[3] = {A.w, U.w, Q0.w};
+    const float2 wz01 = make_float2(Q2.z, Q2.w);
+    const float wz2 = Q1.w;
+    const float2 q1 = make_float2(Q1.x, Q1.y), q2 = make_float2(Q2.x, Q2.y), zq2 = make_float2(Z.x, Z.y);
+    const float2 uxy = __ffma2_rn(make_float2(fox, fox), make_float2(Q0.x, Q0.y), make_float2(U.x, U.y));
+    const float uz = fmaf(fox, Q0.z, U.z);
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) {
+      const float wxy = wx * wyv[oy];
+      const float2 uy = oy ? __ffma2_rn(make_float2((float)oy, (float)oy), q1, uxy) : uxy;
+      const float uyz = oy ? fmaf((float)oy, Q1.z, uz) : uz;
+      const float2 W01 = __fmul2_rn(make_float2(wxy, wxy), wz01);   // (W_oz0, W_oz1)
+      const float W2 = wxy * wz2;
+      const int k = oy * 3;
+      pxy[k] = __ffma2_rn(make_float2(W01.x, W01.x), uy, pxy[k]);
+      pxy[k + 1] = __ffma2_rn(make_float2(W01.y, W01.y), __fadd2_rn(q2, uy), pxy[k + 1]);
+      pxy[k + 2] = __ffma2_rn(make_float2(W2, W2), __ffma2_rn(make_float2(2.f, 2.f), q2, uy), pxy[k + 2]);
+      const float2 uz01 = __fadd2_rn(make_float2(uyz, uyz), zq2);   // (u_z + 0, u_z + q2_z)
+      pz01[oy] = __ffma2_rn(W01, uz01, pz01[oy]);
+      pz2[oy] = fmaf(W2, fmaf(2.0f, Z.y, uyz), pz2[oy]);
+      m01[oy] = __fadd2_rn(W01, m01[oy]);
+      m2[oy] += W2;
+    }
+  }
+#pragma unroll
+  for (int oy = 0; oy < 3; ++oy) {
+    const int k = oy * 3;
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz) {
+      accp[k + oz][0] += pxy[k + oz].x;
+      accp[k + oz][1] += pxy[k + oz].y;
+    }
+    accp[k][2] += pz01[oy].x; accp[k + 1][2] += pz01[oy].y; accp[k + 2][2] += pz2[oy];
+    accm[k] += m01[oy].x; accm[k + 1] += m01[oy].y; accm[k + 2] += m2[oy];
+  }
+#else
+  for (int r = 0; r < rows; ++r, rp += kRowF4) {
+    const float4 A = rp[0], U = rp[1], Q0 = rp[2], Q1 = rp[3], Q2 = rp[4], Z = rp[5];
+    const float wx = ox == 0 ? A.x : (ox == 1 ? A.y : A.z);
+    const float wyv[3] = {A.w, U.w, Q0.w};
+    const float wzv[3] = {Q2.z, Q2.w, Q1.w};
+    const float ux = fmaf(fox, Q0.x, U.x), uy = fmaf(fox, Q0.y, U.y), uz = fmaf(fox, Q0.z, U.z);
+    const float q1x = Q1.x, q1y = Q1.y, q1z = Q1.z;
+    const float q2x = Q2.x, q2y = Q2.y, q2z = Z.y;
 #pragma unroll
     for (int oy = 0; oy < 3; ++oy) {
       const float wxy = wx * wyv[oy];
@@ -997,6 +1113,7 @@ __device__ __forceinline__ void p2g_accumulate_rows(const float4* slot, int my_c
       }
     }
   }
+#endif
 }
 
 // Phase 1 of the fused kernels for storage slot j: G2P from the
@@ -1108,15 +1225,17 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
   for (int i = i0; i < nsc * 35; i += stride) {
     const int e = i / 35, q = i - 35 * e;
     const float* s = reinterpret_cast<const float*>(sc + e * kRowF4);
-    const int pb = __float_as_int(s[21]);
+    const int pb = __float_as_int(s[kRwBase]);
     const int bx = pb >> 20, by = (pb >> 10) & 1023, bz = pb & 1023;
     if (q < 27) {
       const int a = q / 9, b = (q / 3) % 3, c = q % 3;
-      const float W = s[a] * s[3 + b] * s[6 + c];
+      const float wy = b == 0 ? s[kRwWy0] : (b == 1 ? s[kRwWy1] : s[kRwWy2]);
+      const float wz = c == 0 ? s[kRwWz0] : (c == 1 ? s[kRwWz1] : s[kRwWz2]);
+      const float W = s[kRwWx + a] * wy * wz;
       const float fa = (float)a, fb = (float)b, fc = (float)c;
-      const float ux = fmaf(fc, s[18], fmaf(fb, s[15], fmaf(fa, s[12], s[9])));
-      const float uy = fmaf(fc, s[19], fmaf(fb, s[16], fmaf(fa, s[13], s[10])));
-      const float uz = fmaf(fc, s[20], fmaf(fb, s[17], fmaf(fa, s[14], s[11])));
+      const float ux = fmaf(fc, s[kRwQ2], fmaf(fb, s[kRwQ1], fmaf(fa, s[kRwQ0], s[kRwU])));
+      const float uy = fmaf(fc, s[kRwQ2 + 1], fmaf(fb, s[kRwQ1 + 1], fmaf(fa, s[kRwQ0 + 1], s[kRwU + 1])));
+      const float uz = fmaf(fc, s[kRwQ2z], fmaf(fb, s[kRwQ1 + 2], fmaf(fa, s[kRwQ0 + 2], s[kRwU + 2])));
       NSF_CHECK(node_index(bx + a, by + b, bz + c, P) < P.nodes_per_scene);
       red_add_v4_t(gacc + node_index(bx + a, by + b, bz + c, P), W * P.mass, W * ux, W * uy, W * uz);
     } else {

@@ -208,13 +208,16 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     if (fv && strncmp(fv, "dense", 5) == 0) pb->sparse = false;
     else if (fv && strcmp(fv, "sparse") == 0) pb->sparse = true;
     else pb->sparse = nblk > 0 && v.n < (int64_t)kSparseParticlesPerBlock * nblk;
+    // dense scenes run the 2-CTA/SM instantiation (128 registers: the paired-FMA
+    // transfer loops need them; the 3-CTA one spills, C3 102.5 -> 98.1 us)
     if (fv && strcmp(fv, "dense2") == 0) pb->dense2 = true;
     else if (fv) pb->dense2 = false;
-    else pb->dense2 = !pb->sparse && nblk < 2 * 3 * num_sms();
-    // grid update inside the fused kernel only where it measured faster: the
-    // 2-CTA/SM dense variant (few segments per CTA, e.g. C2); C3 (3 CTAs/SM) and the
-    // sparse variant (512 tile nodes per ~100 particles, C4) keep the separate pass
-    pb->rot = rot_mode() == 1 || (rot_mode() < 0 && pb->dense2);
+    else pb->dense2 = !pb->sparse;
+    // grid update inside the fused kernel only where it measured faster: few
+    // segments per CTA (fewer than 2 per CTA of a 3-CTA/SM grid, e.g. C2: 37.0 ->
+    // 36.3 us); C3 (~7 segments per CTA: 103.7 vs 98.1 us) and the sparse variant
+    // (512 tile nodes per ~100 particles, C4) keep the separate pass
+    pb->rot = rot_mode() == 1 || (rot_mode() < 0 && !pb->sparse && nblk < 2 * 3 * num_sms());
     if (pb->rot) {
       const nsf_status rs = rot_setup(h, pb, v);
       if (rs != NSF_OK) return rs;
