@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define NSF_MPM_ABI_VERSION 4
+#define NSF_MPM_ABI_VERSION 5
 
 typedef struct nsf_mpm nsf_mpm; /* opaque; owns all device state */
 
@@ -85,7 +85,9 @@ typedef enum {
 /* Particle-grid transfer of P2G's momentum. */
 typedef enum {
   NSF_TRANSFER_APIC = 0,   /* m_i v_i = sum w m_p (v_p + C_p (x_i - x_p)) */
-  NSF_TRANSFER_PIC = 1     /* m_i v_i = sum w m_p v_p (C_p still updated and used for F)  */
+  NSF_TRANSFER_PIC = 1,    /* m_i v_i = sum w m_p v_p (C_p still updated and used for F)  */
+  NSF_TRANSFER_RPIC = 2    /* APIC with C_p = skew part of the G2P affine matrix (the
+                              damping variant; F_trial still uses the full gradient) (ABI 5) */
 } nsf_transfer;
 
 /* Wall boundary condition on the nodes within bc_width of a face (#11, #12). */

@@ -65,7 +65,7 @@ class Params:
     plate_y0: float = 0.0
     plate_velocity: tuple = (0.0, 0.0, 0.0)
     force_mode: int = 0        # 0 MLS, 1 GRADW
-    transfer: int = 0          # 0 APIC, 1 PIC
+    transfer: int = 0          # 0 APIC, 1 PIC, 2 RPIC (reading #38)
     hardening: float = 0.0     # VM xi   (#30)
     softening: float = 0.0     # VM theta (#30)
 
@@ -198,6 +198,11 @@ def g2p(x, F, uid, vi, P: Params, want_F=True):
     if want_F:
         G = C_new if P.force_mode == 0 else np.einsum("pni,pnj->pij", vn, gW)
         F_tr = (np.eye(3) + P.dt * G) @ np.asarray(F, np.float64)
+    if P.transfer == 2:
+        # RPIC ("RPIC can be added in the computation of C_p", reading #38):
+        # C_p keeps only its skew-symmetric (rigid-rotation) part; F_trial above
+        # used the full velocity gradient
+        C_new = 0.5 * (C_new - np.transpose(C_new, (0, 2, 1)))
     return x_new, v_new, C_new, F_tr
 
 

@@ -24,7 +24,7 @@ NSF_OK, NSF_ERR_INVALID_ARGUMENT, NSF_ERR_OUT_OF_DOMAIN, NSF_ERR_NONFINITE, NSF_
 STATUS_NAMES = ["NSF_OK", "NSF_ERR_INVALID_ARGUMENT", "NSF_ERR_OUT_OF_DOMAIN", "NSF_ERR_NONFINITE",
                 "NSF_ERR_CUDA", "NSF_ERR_OUT_OF_MEMORY", "NSF_ERR_BAD_STATE"]
 NSF_FIXED_COROTATED, NSF_DRUCKER_PRAGER, NSF_VON_MISES, NSF_NEURAL_STRESS, NSF_HENCKY = range(5)
-NSF_TRANSFER_APIC, NSF_TRANSFER_PIC = range(2)
+NSF_TRANSFER_APIC, NSF_TRANSFER_PIC, NSF_TRANSFER_RPIC = range(3)
 NSF_BC_NONE, NSF_BC_STICKY, NSF_BC_SLIP = range(3)
 NSF_FORCE_MLS, NSF_FORCE_GRADW = range(2)
 NSF_FIELD_X, NSF_FIELD_V, NSF_FIELD_C, NSF_FIELD_F, NSF_FIELD_TAU, NSF_FIELD_TAU_Y = 1, 2, 4, 8, 16, 32

@@ -218,6 +218,11 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
   float Cn[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) Cn[k] = cC * Bm[k];
+  if (FORCE == 0) {   // MLS: the F update's gradient is the full C
+#pragma unroll
+    for (int k = 0; k < 9; ++k) G[k] = Cn[k];
+  }
+  if (P.rpic) skew_part(Cn);   // RPIC (#38): the stored / transferred C_p
   float xn[3];
   bool ok = true;
 #pragma unroll
@@ -238,10 +243,6 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
     float Fp[9], Ft[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) Fp[k] = S[pbase(p) + (PF + k) * 32];
-    if (FORCE == 0) {
-#pragma unroll
-      for (int k = 0; k < 9; ++k) G[k] = Cn[k];
-    }
     // F_trial = (I + dt G) F
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -421,7 +422,10 @@ __global__ void __launch_bounds__(128, NSF_G2P_NSF_MINB) k_g2p_nsf(int64_t n, fl
       S[pbase(p) + (PV + a) * 32] = v[a];
     }
 #pragma unroll
-    for (int k = 0; k < 9; ++k) S[pbase(p) + (PC + k) * 32] = cC * Bm[k];
+    for (int k = 0; k < 9; ++k) Bm[k] *= cC;
+    if (P.rpic) skew_part(Bm);   // RPIC (#38)
+#pragma unroll
+    for (int k = 0; k < 9; ++k) S[pbase(p) + (PC + k) * 32] = Bm[k];
     if (!ok) flag_error(err, ERR_OUT_OF_DOMAIN, ids[p]);
     if (!finite) flag_error(err, ERR_NONFINITE, ids[p]);
   }

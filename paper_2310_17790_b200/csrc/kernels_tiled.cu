@@ -662,6 +662,7 @@ __device__ __forceinline__ void g2p_gather(const float x[3], const float4* __res
 #pragma unroll
     for (int k = 0; k < 9; ++k) G[k] = Cn[k];
   }
+  if (P.rpic) skew_part(Cn);   // RPIC: the transfer's C_p; G keeps the full gradient
 }
 
 #ifndef NSF_G2P_FLAT_MIN_BLOCKS
@@ -1169,6 +1170,7 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       g2p_gather_tile(x, vt, o, P, vn, Cn);
 #pragma unroll
       for (int k = 0; k < 9; ++k) G[k] = Cn[k];
+      if (P.rpic) skew_part(Cn);   // RPIC: the transfer's C_p; G keeps the full gradient
     } else {
       g2p_gather<0, ROT>(x, gvel, P, vn, Cn, G, y_plate);   // ROT: gvel holds raw P2G sums
     }

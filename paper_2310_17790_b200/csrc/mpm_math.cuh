@@ -24,6 +24,15 @@ struct Axis {
   float dw[3];   // d w / d x  (only used by GRADW)
 };
 
+// RPIC (reading #38): C <- (C - C^T) / 2, the rigid-rotation part
+__device__ __forceinline__ void skew_part(float C[9]) {
+  const float a = 0.5f * (C[1] - C[3]), b = 0.5f * (C[2] - C[6]), c = 0.5f * (C[5] - C[7]);
+  C[0] = C[4] = C[8] = 0.0f;
+  C[1] = a; C[3] = -a;
+  C[2] = b; C[6] = -b;
+  C[5] = c; C[7] = -c;
+}
+
 __device__ __forceinline__ Axis bspline_axis(float x, float inv_dx) {
   Axis a;
   float t = x * inv_dx;

@@ -89,7 +89,8 @@ struct DevParams {
   float gradw_coef;  // dt V0
   float stress_scale;
   int deterministic;  // 1: fixed-point P2G (kernels_det.cu), bitwise reproducible
-  float mC;           // affine mass of P2G: m_p (APIC) or 0 (PIC)
+  float mC;           // affine mass of P2G: m_p (APIC, RPIC) or 0 (PIC)
+  int rpic;           // 1: G2P keeps the skew part of C_p (RPIC, reading #38)
   int vm_hs;          // 1: von Mises with a per-particle yield stress (plane PTY, #30-#32)
   float vm_hard_k;    //   2 mu xi (hardening)
   float vm_soft;      //   theta (softening; tau_Y <= 0 is damage)

@@ -32,7 +32,7 @@ import numpy as np
 # ---------------------------------------------------------------------------
 # model / bc / force-mode codes (mirror include/nsf_mpm.h enums; plain ints)
 FIXED_COROTATED, DRUCKER_PRAGER, VON_MISES, NEURAL_STRESS, HENCKY = 0, 1, 2, 3, 4
-TRANSFER_APIC, TRANSFER_PIC = 0, 1
+TRANSFER_APIC, TRANSFER_PIC, TRANSFER_RPIC = 0, 1, 2
 BC_NONE, BC_STICKY, BC_SLIP = 0, 1, 2
 FORCE_MLS, FORCE_GRADW = 0, 1
 

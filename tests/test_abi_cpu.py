@@ -52,7 +52,7 @@ def test_abi_version(built_lib):
     import paper_2310_17790_b200 as nsf
     hdr = open(os.path.join(ROOT, "include", "nsf_mpm.h")).read()
     ver = int(hdr.split("#define NSF_MPM_ABI_VERSION")[1].split()[0])
-    assert nsf.nsf_mpm_abi_version() == ver == 4
+    assert nsf.nsf_mpm_abi_version() == ver == 5
 
 
 def test_material_struct_layout_matches_header(built_lib, tmp_path):

@@ -85,9 +85,14 @@ def _reduced_parity(nsf, sc, steps_before):
     return e_tau, errs
 
 
+@pytest.mark.parametrize("transfer", [0, 2])
 @pytest.mark.parametrize("steps_before", [0, 5])
-def test_reduced_substep_parity_small(nsf, steps_before):
+def test_reduced_substep_parity_small(nsf, steps_before, transfer):
+    """transfer 2: RPIC (reading #38) in the reduced G2P."""
     sc = scenes.c5_small(n_scenes=3, per_scene=300)
+    sc.cfg.transfer = transfer
+    if transfer:   # non-zero C so that the skew projection matters
+        sc.C = (np.random.default_rng(5).normal(size=sc.C.shape) * 2.0).astype(np.float32)
     e_tau, errs = _reduced_parity(nsf, sc, steps_before)
     assert e_tau <= BAR_MLP, e_tau
     assert all(e <= BAR_STEP for e in errs.values()), errs

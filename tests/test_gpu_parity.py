@@ -58,6 +58,12 @@ def small_scenes():
                                 keep=5000, vnoise=0.2, Fnoise=0.1, Cnoise=2.0),
         "FC_pic": S.block_scene("FCp", 32, (9, 6, 10), (22, 17, 19), S.FIXED_COROTATED, 19,
                                 keep=5000, vnoise=0.3, Fnoise=0.02, Cnoise=3.0, transfer=S.TRANSFER_PIC),
+        # RPIC (reading #38): fused MLS path and split GRADW path
+        "FC_rpic": S.block_scene("FCr", 32, (9, 6, 10), (22, 17, 19), S.FIXED_COROTATED, 21,
+                                 keep=5000, vnoise=0.3, Fnoise=0.02, Cnoise=3.0, transfer=S.TRANSFER_RPIC),
+        "VM_rpic_gradw": S.block_scene("VMrg", 32, (9, 3, 8), (21, 13, 22), S.VON_MISES, 22,
+                                       keep=4000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0, transfer=S.TRANSFER_RPIC,
+                                       force_mode=S.FORCE_GRADW),
         "VM_pic_gradw": S.block_scene("VMpg", 32, (9, 3, 8), (21, 13, 22), S.VON_MISES, 20,
                                       keep=4000, vnoise=0.2, Fnoise=0.05, Cnoise=2.0, transfer=S.TRANSFER_PIC,
                                       force_mode=S.FORCE_GRADW),

@@ -328,3 +328,65 @@ def test_pic_transfer(fm):
     assert np.array_equal(gnode, gnode_a) and np.allclose(gm, gm_a, rtol=1e-14)
     _, _, _, gp_c = p2g(x, np.zeros_like(v), C, zero, P)   # APIC with v = 0: the affine term alone
     assert np.allclose(gp_a - gp, gp_c, rtol=1e-10, atol=1e-14)
+
+
+def _grid_field(P, x, fn):
+    node, _, _, _ = mpm._stencil(x, P)
+    uid = np.unique(mpm._linear_id(node, P))
+    Nn = P.grid_res[0]
+    gnode = np.stack([uid // Nn ** 2, (uid // Nn) % Nn, uid % Nn], -1)
+    return uid, fn(gnode * P.dx)
+
+
+@pytest.mark.parametrize("fm", [0, 1])
+def test_rpic_rigid_rotation_and_symmetric_part(fm):
+    """RPIC (reading #38): G2P keeps only the skew-symmetric part
+    of C_p.  A rigid rotation v_i = W x_i + b (W skew) is reproduced exactly (C_p = W,
+    as under APIC); a pure strain rate v_i = S x_i (S symmetric) leaves C_p = 0 under
+    RPIC and S under APIC, while F_trial uses the full velocity gradient in both
+    (reading #38: the projection only feeds the transfer)."""
+    import dataclasses
+    rng = np.random.default_rng(11)
+    P = P_free(fm)
+    Pr = dataclasses.replace(P, transfer=2)
+    x, v, C, F, tau = rand_state(rng, 100)
+    w = rng.normal(size=3)
+    Wsk = np.array([[0.0, -w[2], w[1]], [w[2], 0.0, -w[0]], [-w[1], w[0], 0.0]])
+    b = rng.normal(size=3)
+    uid, vi = _grid_field(P, x, lambda xi: xi @ Wsk.T + b)
+    xn, vn, Cn, Ftr = g2p(x, F, uid, vi, Pr)
+    assert np.allclose(vn, x @ Wsk.T + b, atol=1e-12) and np.allclose(Cn, Wsk, atol=1e-9)
+    assert np.allclose(Cn + np.transpose(Cn, (0, 2, 1)), 0.0, atol=0)          # exactly skew
+    A = rng.normal(size=(3, 3))
+    S = A + A.T
+    uid, vi = _grid_field(P, x, lambda xi: xi @ S.T)
+    _, _, Cr, Fr = g2p(x, F, uid, vi, Pr)
+    _, _, Ca, Fa = g2p(x, F, uid, vi, P)
+    assert np.allclose(Cr, 0.0, atol=1e-9) and np.allclose(Ca, S, atol=1e-9)
+    assert np.allclose(Fr, (np.eye(3) + P.dt * S) @ F, atol=1e-12) and np.array_equal(Fr, Fa)
+
+
+def test_rpic_keeps_apic_angular_momentum():
+    """The particles' angular momentum depends on C only through its skew part
+    (test_p2g_angular_momentum), so after any G2P the RPIC state carries exactly the
+    grid angular momentum and linear momentum the APIC state does, while its P2G
+    momenta differ from APIC's by the symmetric part of C alone."""
+    import dataclasses
+    rng = np.random.default_rng(12)
+    P = P_free(0)
+    Pr = dataclasses.replace(P, transfer=2)
+    x, v, C, F, tau = rand_state(rng, 200)
+    uid, vi = _grid_field(P, x, lambda xi: np.sin(3.0 * xi) + xi @ rng.normal(size=(3, 3)))
+    _, va, Ca, _ = g2p(x, F, uid, vi, P)
+    _, vr, Cr, _ = g2p(x, F, uid, vi, Pr)
+    assert np.array_equal(va, vr)
+    zero = np.zeros_like(tau)
+    _, gna, gma, gpa = p2g(x, va, Ca, zero, P)
+    _, gnr, gmr, gpr = p2g(x, vr, Cr, zero, P)
+    assert np.allclose(gpa.sum(0), gpr.sum(0), rtol=1e-12, atol=1e-13)
+    La, Lr = np.cross(gna * P.dx, gpa).sum(0), np.cross(gnr * P.dx, gpr).sum(0)
+    assert np.allclose(La, Lr, rtol=1e-11, atol=1e-13)
+    Csym = 0.5 * (Ca + np.transpose(Ca, (0, 2, 1)))
+    _, _, _, gps = p2g(x, np.zeros_like(va), Csym, zero, P)
+    assert np.allclose(gpa - gpr, gps, rtol=1e-10, atol=1e-13)
+    assert np.linalg.norm(Csym) > 1e-3     # the case is not degenerate
