@@ -79,7 +79,9 @@ typedef enum {
   NSF_DRUCKER_PRAGER = 1,  /* sand return map */
   NSF_VON_MISES = 2,       /* perfect plasticity, radial return          (#4) */
   NSF_NEURAL_STRESS = 3,   /* tau = sigma_tau h(X, z) */
-  NSF_HENCKY = 4           /* the appendix's "StVK elasticity": Hencky, no return map (#3) */
+  NSF_HENCKY = 4,          /* the appendix's "StVK elasticity": Hencky, no return map (#3) */
+  NSF_HERSCHEL_BULKLEY = 5 /* viscoplastic, h = 1 (#39): yield_stress = sigma_Y, viscosity
+                              = eta; tau = kappa/2 (J^2-1) I + mu dev(bbar) (ABI 5)               */
 } nsf_model;
 
 /* Particle-grid transfer of P2G's momentum. */
@@ -132,6 +134,8 @@ typedef struct {
    * Both >= 0 and finite (else INVALID_ARGUMENT); ignored for other models. */
   double hardening;             /* xi                                                */
   double softening;             /* theta (1/Pa * Pa: tau_Y units per unit log strain) */
+  double viscosity;             /* Herschel-Bulkley eta >= 0 (Pa s; ABI 5); the
+                                   relaxation factor is 1 / (1 + eta / (2 mu dt))    */
 } nsf_material;
 
 /* read_state field mask; dst[k] is the k-th requested field in bit order. */

@@ -10,6 +10,10 @@ SURVEY.md §8(c) readings, recorded in DESIGN.md:
   #6  d = 3 in the Drucker-Prager delta-gamma
   #21 rotation-safe SVD (det U = det V = +1, sign folded into sigma_3);
       log-strain models clamp sigma >= 1e-4 before the log.
+  #39 Herschel-Bulkley (lines 546-552): the deviatoric relaxation acts on
+      s = mu dev(bbar), bbar = det(b)^(-1/3) b; the elastic state keeps the
+      rotation and J of F_trial, and bbar_new = s_new / mu + I_bar 1 with I_bar
+      chosen so that det(bbar_new) = 1 (isochoric plastic flow).
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
 import numpy as np
@@ -164,17 +168,21 @@ def return_map_von_mises_hs(sigma, mu, tau_Y, hardening=0.0, softening=0.0):
     return Z, tY, damaged
 
 
-def elastoplastic_update(F_trial, model, mu, lam, alpha=0.0, tau_Y=0.0):
+def elastoplastic_update(F_trial, model, mu, lam, alpha=0.0, tau_Y=0.0, kappa=None, eta=0.0, dt=1.0):
     """F^E = returnMap(F_trial), tau = tau(F^E).
 
     model 0 fixed-corotated (F^E = F_trial), 1 Drucker-Prager, 2 von Mises,
     4 the appendix's "StVK elasticity": tau = U (2 mu eps + lambda sum(eps) 1) U^T with
-    eps = log(Sigma) and F^E = F_trial, i.e. Hencky elasticity without a return map (reading #3 for U^T).
+    eps = log(Sigma) and F^E = F_trial, i.e. Hencky elasticity without a return map (reading #3 for U^T),
+    5 Herschel-Bulkley (reading #39; sigma_Y = tau_Y, viscosity eta, substep dt,
+    bulk modulus kappa).
     Returns (F_E, tau).
     """
     F_trial = np.asarray(F_trial, dtype=np.float64)
     if model == 0:
         return F_trial.copy(), tau_fixed_corotated(F_trial, mu, lam)
+    if model == 5:
+        return return_map_herschel_bulkley(F_trial, mu, kappa, tau_Y, eta, dt)
     U, s, V = svd_rotation_safe(F_trial)
     if model == 4:
         return F_trial.copy(), tau_hencky(U, s, mu, lam)
@@ -199,3 +207,58 @@ def elastoplastic_update_vm_hs(F_trial, mu, lam, tau_Y, hardening=0.0, softening
     tau = tau_hencky(U, Z, mu, lam)
     tau[damaged] = 0.0
     return F_E, tau, tY
+
+
+def tau_herschel_bulkley(F, mu, kappa):
+    """tau = kappa/2 (J^2 - 1) I + mu dev[det(b)^(-1/3) b], b = F F^T
+    (b^E of the elastic state), J = det F.  (J = 0: the deviatoric term is dropped.)"""
+    F = np.asarray(F, dtype=np.float64)
+    J = np.linalg.det(F)
+    b = F @ np.swapaxes(F, -1, -2)
+    detb = np.linalg.det(b)
+    scale = np.where(detb > 0.0, np.abs(detb) ** (-1.0 / 3.0), 0.0)
+    bbar = scale[:, None, None] * b
+    dev = bbar - (np.trace(bbar, axis1=1, axis2=2) / 3.0)[:, None, None] * np.eye(3)
+    return 0.5 * kappa * (J * J - 1.0)[:, None, None] * np.eye(3) + mu * dev
+
+
+def return_map_herschel_bulkley(F_trial, mu, kappa, sigma_Y, eta, dt):
+    """PAPER.md lines 546-552 (Yue et al. 2015 with h = 1) and reading #39.
+
+    s^trial = dev(tau^trial) = mu dev(bbar^trial), s^trial = ||s^trial||.  If
+    s^trial - sqrt(2/3) sigma_Y > 0:
+        s = s^trial - (s^trial - sqrt(2/3) sigma_Y) / (1 + eta / (2 mu dt)),
+        s (tensor) = s * s^trial / ||s^trial||.
+    Elastic state (#39): bbar_new = s / mu + I_bar 1 with det(bbar_new) = 1, J and the
+    rotation of F_trial kept: in the principal frame of F_trial = U diag(sigma) V^T,
+    F^E = U diag(sign * sqrt(|J|^(2/3) bbar_new_i)) V^T.  Returns (F_E, tau(F_E)).
+    """
+    F_trial = np.asarray(F_trial, dtype=np.float64)
+    U, sg, V = svd_rotation_safe(F_trial)
+    J = np.prod(sg, axis=1)
+    aJ = np.abs(J)
+    j23 = aJ ** (2.0 / 3.0)
+    ok = aJ > 0.0
+    bbar = np.where(ok[:, None], sg * sg / np.where(ok, j23, 1.0)[:, None], 1.0)
+    mean = bbar.mean(axis=1)
+    d = bbar - mean[:, None]                       # dev(bbar) (principal)
+    st = mu * np.linalg.norm(d, axis=1)            # s^trial
+    y = np.sqrt(2.0 / 3.0) * sigma_Y
+    plastic = ok & (st - y > 0.0)
+    F_E = F_trial.copy()
+    if np.any(plastic):
+        s_new = st - (st - y) / (1.0 + eta / (2.0 * mu * dt))
+        dn = d[plastic] * (s_new[plastic] / st[plastic])[:, None]   # s / mu
+        # I_bar: the root of prod(dn_i + I) = 1 (Newton from the trial mean; the
+        # product is increasing and convex there and >= 1 at the start)
+        Ib = mean[plastic].copy()
+        for _ in range(60):
+            f = np.prod(dn + Ib[:, None], axis=1) - 1.0
+            fp = ((dn[:, 1] + Ib) * (dn[:, 2] + Ib) + (dn[:, 0] + Ib) * (dn[:, 2] + Ib)
+                  + (dn[:, 0] + Ib) * (dn[:, 1] + Ib))
+            Ib = Ib - f / fp
+        bnew = dn + Ib[:, None]
+        sig = np.sqrt(j23[plastic][:, None] * bnew)
+        sig[:, 2] *= np.sign(J[plastic])
+        F_E[plastic] = _diag_sandwich(U[plastic], sig, V[plastic])
+    return F_E, tau_herschel_bulkley(F_E, mu, kappa)

@@ -32,7 +32,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .constitutive import lame, dp_alpha, elastoplastic_update, elastoplastic_update_vm_hs, tau_fixed_corotated, \
-    svd_rotation_safe, tau_hencky
+    svd_rotation_safe, tau_hencky, tau_herschel_bulkley
 
 OFFSETS = np.array([(a, b, c) for a in range(3) for b in range(3) for c in range(3)],
                    dtype=np.int64)  # (27,3), lexicographic
@@ -51,7 +51,7 @@ class Params:
     grid_res: tuple            # (Nx, Ny, Nz) nodes per axis
     dx: float
     dt: float
-    model: int                 # 0 FC, 1 DP, 2 VM, 3 NSF
+    model: int                 # 0 FC, 1 DP, 2 VM, 3 NSF, 4 Hencky ("StVK"), 5 Herschel-Bulkley
     mu: float
     lam: float
     alpha: float = 0.0         # DP
@@ -68,6 +68,8 @@ class Params:
     transfer: int = 0          # 0 APIC, 1 PIC, 2 RPIC (reading #38)
     hardening: float = 0.0     # VM xi   (#30)
     softening: float = 0.0     # VM theta (#30)
+    kappa: float = 0.0         # bulk modulus E / (3 (1 - 2 nu)) (Table, Herschel-Bulkley)
+    viscosity: float = 0.0     # Herschel-Bulkley eta (#39)
 
     @property
     def inv_dx(self):
@@ -77,7 +79,7 @@ class Params:
 def params_from_config(cfg) -> Params:
     """Derive the method constants from a scenes.Config (Lame: lines 504-512;
     V0 default dx^3/8 for 8 ppc (reading #16); m_p = rho V0)."""
-    mu, lam, _ = lame(cfg.E, cfg.nu)
+    mu, lam, kappa = lame(cfg.E, cfg.nu)
     dx = 1.0 / cfg.grid_res
     V0 = cfg.particle_volume if cfg.particle_volume > 0 else dx ** 3 / 8.0
     return Params(grid_res=(cfg.grid_res,) * 3, dx=dx, dt=cfg.dt, model=cfg.model,
@@ -87,7 +89,8 @@ def params_from_config(cfg) -> Params:
                   plate_enabled=cfg.plate_enabled, plate_y0=cfg.plate_y0,
                   plate_velocity=tuple(cfg.plate_velocity), force_mode=cfg.force_mode,
                   transfer=getattr(cfg, "transfer", 0), hardening=getattr(cfg, "hardening", 0.0),
-                  softening=getattr(cfg, "softening", 0.0))
+                  softening=getattr(cfg, "softening", 0.0), kappa=kappa,
+                  viscosity=getattr(cfg, "viscosity", 0.0))
 
 
 # ---------------------------------------------------------------------------
@@ -211,6 +214,8 @@ def initial_tau(F, P: Params):
     F = np.asarray(F, np.float64)
     if P.model == 0:
         return tau_fixed_corotated(F, P.mu, P.lam)
+    if P.model == 5:
+        return tau_herschel_bulkley(F, P.mu, P.kappa)
     U, s, V = svd_rotation_safe(F)
     return tau_hencky(U, s, P.mu, P.lam)
 
@@ -229,7 +234,7 @@ def substep(state: dict, P: Params, step: int, check=True) -> dict:
         tY = np.asarray(state.get("tau_Y", np.full(x.shape[0], P.tau_Y)), np.float64)
         F_E, tau_new, out["tau_Y"] = elastoplastic_update_vm_hs(F_tr, P.mu, P.lam, tY, P.hardening, P.softening)
     else:
-        F_E, tau_new = elastoplastic_update(F_tr, P.model, P.mu, P.lam, P.alpha, P.tau_Y)
+        F_E, tau_new = elastoplastic_update(F_tr, P.model, P.mu, P.lam, P.alpha, P.tau_Y, P.kappa, P.viscosity, P.dt)
     if check:
         check_domain(x_new, P)
     out.update({"x": x_new, "v": v_new, "C": C_new, "F": F_E, "tau": tau_new,

@@ -23,7 +23,7 @@ NSF_OK, NSF_ERR_INVALID_ARGUMENT, NSF_ERR_OUT_OF_DOMAIN, NSF_ERR_NONFINITE, NSF_
     NSF_ERR_OUT_OF_MEMORY, NSF_ERR_BAD_STATE = range(7)
 STATUS_NAMES = ["NSF_OK", "NSF_ERR_INVALID_ARGUMENT", "NSF_ERR_OUT_OF_DOMAIN", "NSF_ERR_NONFINITE",
                 "NSF_ERR_CUDA", "NSF_ERR_OUT_OF_MEMORY", "NSF_ERR_BAD_STATE"]
-NSF_FIXED_COROTATED, NSF_DRUCKER_PRAGER, NSF_VON_MISES, NSF_NEURAL_STRESS, NSF_HENCKY = range(5)
+NSF_FIXED_COROTATED, NSF_DRUCKER_PRAGER, NSF_VON_MISES, NSF_NEURAL_STRESS, NSF_HENCKY, NSF_HERSCHEL_BULKLEY = range(6)
 NSF_TRANSFER_APIC, NSF_TRANSFER_PIC, NSF_TRANSFER_RPIC = range(3)
 NSF_BC_NONE, NSF_BC_STICKY, NSF_BC_SLIP = range(3)
 NSF_FORCE_MLS, NSF_FORCE_GRADW = range(2)
@@ -49,7 +49,7 @@ class nsf_material(C.Structure):
                 ("plate_velocity", C.c_double * 3), ("force_mode", C.c_int32),
                 ("deterministic", C.c_int32), ("n_scenes", C.c_int32),
                 ("particle_volume", C.c_double), ("stress_scale", C.c_double), ("transfer", C.c_int32),
-                ("hardening", C.c_double), ("softening", C.c_double)]
+                ("hardening", C.c_double), ("softening", C.c_double), ("viscosity", C.c_double)]
 
 
 class NsfError(RuntimeError):
@@ -169,6 +169,7 @@ def make_material(cfg) -> nsf_material:
     m.transfer = int(getattr(cfg, "transfer", 0))
     m.hardening = float(getattr(cfg, "hardening", 0.0))
     m.softening = float(getattr(cfg, "softening", 0.0))
+    m.viscosity = float(getattr(cfg, "viscosity", 0.0))
     return m
 
 

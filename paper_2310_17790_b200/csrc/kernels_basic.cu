@@ -42,7 +42,7 @@ __global__ void k_unpack(int64_t n, const float* __restrict__ x, const float* __
   if (!ok && finite) flag_error(err, ERR_OUT_OF_DOMAIN, (int)p);
   if (with_F) {
     float tau[6];
-    elastic_tau(Fp, P.model, P.mu, P.lam, tau);
+    elastic_tau(Fp, P.model, P.mu, P.lam, tau, P.kappa);
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
       S[pbase(p) + (PT + k) * 32] = tau[k];
@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(128) k_g2p_direct(int64_t n, float* S, int64_t
       J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
       S[pbase(p) + PTY * 32] = tY;
     } else {
-      J = elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+      J = P.model == 5 ? hb_update(Ft, P.mu, P.kappa, P.hb_yield, P.hb_relax, FE, tau)
+                       : elastoplastic(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
     }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
 #pragma unroll

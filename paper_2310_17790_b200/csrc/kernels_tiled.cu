@@ -740,7 +740,8 @@ k_g2p_flat(const float* __restrict__ Sin, float* __restrict__ Sout, int64_t n,
   if (P.vm_hs) {   // per-particle yield stress
     J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
   } else {
-    J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+    J = P.model == 5 ? hb_update(Ft, P.mu, P.kappa, P.hb_yield, P.hb_relax, FE, tau)
+                     : elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
   }
   ob[PTY * 32] = tY;
 #pragma unroll
@@ -1199,7 +1200,8 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
       base[PTY * 32] = tY;
     } else {
-      J = elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
+      J = P.model == 5 ? hb_update(Ft, P.mu, P.kappa, P.hb_yield, P.hb_relax, FE, tau)
+                       : elastoplastic_fast(Ft, P.model, P.mu, P.lam, P.alpha, P.tau_Y, FE, tau);
     }
     float chk = xn[0] + xn[1] + xn[2] + vn[0] + vn[1] + vn[2];
 #pragma unroll

@@ -618,8 +618,87 @@ __device__ __forceinline__ float vm_hs_update(const float Ft[9], float mu, float
   return J;
 }
 
-__device__ __forceinline__ void elastic_tau(const float F[9], int model, float mu, float lam, float tau[6]) {
+// Herschel-Bulkley (Yue et al. 2015 with h = 1; reading #39), in the
+// principal frame of F_trial = U diag(sigma) V^T (rotation-safe SVD):
+//   bbar_i = |J|^(-2/3) sigma_i^2, s = mu dev(bbar), s^trial = ||s||;
+//   if s^trial > yield (= sqrt(2/3) sigma_Y):
+//     s <- s (s^trial - (s^trial - yield) relax) / s^trial, relax = 1 / (1 + eta / (2 mu dt)),
+//     bbar_new = s / mu + I 1 with det(bbar_new) = 1 (Newton on the cubic from the trial
+//     mean), F^E = U diag(sqrt(|J|^(2/3) bbar_new)) V^T (J and the rotation kept);
+//   tau = kappa/2 (J^2 - 1) I + mu dev(bbar_E) = U diag(.) U^T.
+// relax < 0: no return map (the elastic stress of F at load).  Returns det F^E.
+__device__ __forceinline__ float hb_update(const float Ft[9], float mu, float kappa, float yield, float relax,
+                                           float FE[9], float tau[6]) {
+  float U[3][3], V[3][3], s[3];
+  svd3(Ft, U, s, V);
+  const float J = det3(Ft);   // from F itself: the product of the Jacobi singular values is biased low
+  const float aJ = fabsf(J);
+  float t[3] = {0.f, 0.f, 0.f};
+  bool plastic = false;
+  float sg[3] = {s[0], s[1], s[2]};
+  if (aJ > 0.0f) {
+    const float j23 = cbrtf(aJ * aJ), ij23 = 1.0f / j23;
+    float bb[3] = {s[0] * s[0] * ij23, s[1] * s[1] * ij23, s[2] * s[2] * ij23};
+    const float mean = (bb[0] + bb[1] + bb[2]) * (1.0f / 3.0f);
+    // dev(bbar) from pairwise differences (s_i^2 - s_j^2 = (s_i - s_j)(s_i + s_j)): no
+    // cancellation against the mean when the stretches are close
+    const float q01 = (s[0] - s[1]) * (s[0] + s[1]), q02 = (s[0] - s[2]) * (s[0] + s[2]),
+                q12 = (s[1] - s[2]) * (s[1] + s[2]);
+    const float c3 = ij23 * (1.0f / 3.0f);
+    float d[3] = {(q01 + q02) * c3, (q12 - q01) * c3, -(q02 + q12) * c3};
+    const float st = mu * sqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (relax >= 0.0f && st > yield) {
+      plastic = true;
+      const float k = (st - (st - yield) * relax) / st;
+      d[0] *= k; d[1] *= k; d[2] *= k;
+      float I = mean;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {   // monotone Newton on prod(d_i + I) = 1
+        const float a0 = d[0] + I, a1 = d[1] + I, a2 = d[2] + I;
+        I -= (a0 * a1 * a2 - 1.0f) / (a1 * a2 + a0 * a2 + a0 * a1);
+      }
+      bb[0] = d[0] + I; bb[1] = d[1] + I; bb[2] = d[2] + I;
+      sg[0] = sqrtf(j23 * bb[0]);
+      sg[1] = sqrtf(j23 * bb[1]);
+      sg[2] = J / (sg[0] * sg[1]);   // det F^E = J exactly up to one rounding (isochoric flow)
+      // dev(bbar_E) = the relaxed deviator (bbar_E = d + I 1, det 1)
+    }
+    const float vol = 0.5f * kappa * (J * J - 1.0f);
+    t[0] = vol + mu * d[0]; t[1] = vol + mu * d[1]; t[2] = vol + mu * d[2];
+  } else {
+    t[0] = t[1] = t[2] = -0.5f * kappa;
+  }
+  if (plastic) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        FE[i * 3 + j] = U[i][0] * sg[0] * V[j][0] + U[i][1] * sg[1] * V[j][1] + U[i][2] * sg[2] * V[j][2];
+    // isochoric flow: det F^E = J (the fp32 U, V are orthogonal only to ~1e-7, with a
+    // bias that would otherwise drift the volume substep after substep)
+    const float c = cbrtf(J / det3(FE));
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] *= c;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) FE[k] = Ft[k];
+  }
+  tau[0] = U[0][0] * U[0][0] * t[0] + U[0][1] * U[0][1] * t[1] + U[0][2] * U[0][2] * t[2];
+  tau[1] = U[1][0] * U[1][0] * t[0] + U[1][1] * U[1][1] * t[1] + U[1][2] * U[1][2] * t[2];
+  tau[2] = U[2][0] * U[2][0] * t[0] + U[2][1] * U[2][1] * t[1] + U[2][2] * U[2][2] * t[2];
+  tau[3] = U[1][0] * U[2][0] * t[0] + U[1][1] * U[2][1] * t[1] + U[1][2] * U[2][2] * t[2];
+  tau[4] = U[0][0] * U[2][0] * t[0] + U[0][1] * U[2][1] * t[1] + U[0][2] * U[2][2] * t[2];
+  tau[5] = U[0][0] * U[1][0] * t[0] + U[0][1] * U[1][1] * t[1] + U[0][2] * U[1][2] * t[2];
+  return J;
+}
+
+__device__ __forceinline__ void elastic_tau(const float F[9], int model, float mu, float lam, float tau[6],
+                                            float kappa = 0.0f) {
   float FE[9];
+  if (model == 5) {   // Herschel-Bulkley elasticity of F itself
+    hb_update(F, mu, kappa, 0.0f, -1.0f, FE, tau);
+    return;
+  }
   // FC: same formula; DP/VM: Hencky of F itself (no return map at load)
   if (model == 0) {
     elastoplastic(F, 0, mu, lam, 0.0f, 0.0f, FE, tau);

@@ -91,6 +91,9 @@ struct DevParams {
   int deterministic;  // 1: fixed-point P2G (kernels_det.cu), bitwise reproducible
   float mC;           // affine mass of P2G: m_p (APIC, RPIC) or 0 (PIC)
   int rpic;           // 1: G2P keeps the skew part of C_p (RPIC, reading #38)
+  float kappa;        // bulk modulus E / (3 (1 - 2 nu)) (Herschel-Bulkley)
+  float hb_yield;     // sqrt(2/3) sigma_Y (Herschel-Bulkley yield condition)
+  float hb_relax;     // 1 / (1 + eta / (2 mu dt))
   int vm_hs;          // 1: von Mises with a per-particle yield stress (plane PTY, #30-#32)
   float vm_hard_k;    //   2 mu xi (hardening)
   float vm_soft;      //   theta (softening; tau_Y <= 0 is damage)

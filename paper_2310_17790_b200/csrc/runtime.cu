@@ -275,7 +275,9 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   if (!grid_res || !m) return NSF_ERR_INVALID_ARGUMENT;
   if (!(dx > 0) || !(dt > 0) || !std::isfinite(dx) || !std::isfinite(dt)) return NSF_ERR_INVALID_ARGUMENT;
   if (!(m->E > 0) || !(m->nu >= 0 && m->nu < 0.5) || !(m->rho > 0)) return NSF_ERR_INVALID_ARGUMENT;
-  if (m->model < 0 || m->model > 4) return NSF_ERR_INVALID_ARGUMENT;
+  if (m->model < 0 || m->model > 5) return NSF_ERR_INVALID_ARGUMENT;
+  if (m->model == NSF_HERSCHEL_BULKLEY && !(m->viscosity >= 0 && std::isfinite(m->viscosity)))
+    return NSF_ERR_INVALID_ARGUMENT;
   if (m->transfer != NSF_TRANSFER_APIC && m->transfer != NSF_TRANSFER_PIC && m->transfer != NSF_TRANSFER_RPIC)
     return NSF_ERR_INVALID_ARGUMENT;
   if (m->model == NSF_DRUCKER_PRAGER && !(m->friction_angle_deg > 0 && m->friction_angle_deg < 90))
@@ -349,6 +351,9 @@ nsf_status nsf_mpm_create(const int32_t grid_res[3], double dx, double dt, const
   }
   P.mC = m->transfer == NSF_TRANSFER_PIC ? 0.0f : P.mass;
   P.rpic = m->transfer == NSF_TRANSFER_RPIC ? 1 : 0;
+  P.kappa = (float)(m->E / (3.0 * (1.0 - 2.0 * m->nu)));
+  P.hb_yield = (float)(std::sqrt(2.0 / 3.0) * m->yield_stress);
+  P.hb_relax = (float)(1.0 / (1.0 + m->viscosity / (2.0 * mu * dt)));
   P.vm_hs = m->model == NSF_VON_MISES && (m->hardening > 0 || m->softening > 0);
   P.vm_hard_k = (float)(2.0 * mu * m->hardening);
   P.vm_soft = (float)m->softening;

@@ -31,7 +31,7 @@ import numpy as np
 
 # ---------------------------------------------------------------------------
 # model / bc / force-mode codes (mirror include/nsf_mpm.h enums; plain ints)
-FIXED_COROTATED, DRUCKER_PRAGER, VON_MISES, NEURAL_STRESS, HENCKY = 0, 1, 2, 3, 4
+FIXED_COROTATED, DRUCKER_PRAGER, VON_MISES, NEURAL_STRESS, HENCKY, HERSCHEL_BULKLEY = 0, 1, 2, 3, 4, 5
 TRANSFER_APIC, TRANSFER_PIC, TRANSFER_RPIC = 0, 1, 2
 BC_NONE, BC_STICKY, BC_SLIP = 0, 1, 2
 FORCE_MLS, FORCE_GRADW = 0, 1
@@ -54,6 +54,7 @@ class Config:
     yield_stress: float = 0.0
     hardening: float = 0.0         # VM hardening coefficient xi
     softening: float = 0.0         # VM softening coefficient theta
+    viscosity: float = 0.0         # Herschel-Bulkley eta (Pa s); sigma_Y = yield_stress
     gravity: tuple = (0.0, -9.8, 0.0)
     bc: tuple = (BC_STICKY,) * 6   # faces -x,+x,-y,+y,-z,+z
     bc_width: int = 3
@@ -346,7 +347,7 @@ def block_scene(name: str, grid_res: int, lo, hi, model: int, seed: int,
     """Stratified block of cells [lo,hi) on a grid_res^3 grid with optional
     seeded perturbations of v, C and F (used to exercise every branch)."""
     base = {FIXED_COROTATED: config("C1"), DRUCKER_PRAGER: config("C2"),
-            VON_MISES: config("C3"), HENCKY: config("C3")}[model]
+            VON_MISES: config("C3"), HENCKY: config("C3"), HERSCHEL_BULKLEY: config("C3")}[model]
     cfg = Config(**{**base.as_dict(), "name": name, "grid_res": grid_res, "model": model})
     if model == VON_MISES:
         cfg.plate_y0 = hi[1] / grid_res

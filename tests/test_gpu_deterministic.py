@@ -31,7 +31,7 @@ def det(sc):
     return sc
 
 
-@pytest.mark.parametrize("name", ["C1spin", "FC_ragged", "DP", "VM", "VM_gradw", "FC_rpic"])
+@pytest.mark.parametrize("name", ["C1spin", "FC_ragged", "DP", "VM", "VM_gradw", "FC_rpic", "HB"])
 def test_deterministic_parity(nsf, name):
     sc = det(small_scenes()[name])
     sim = nsf.Simulator(sc.cfg)

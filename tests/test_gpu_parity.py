@@ -58,6 +58,14 @@ def small_scenes():
                                 keep=5000, vnoise=0.2, Fnoise=0.1, Cnoise=2.0),
         "FC_pic": S.block_scene("FCp", 32, (9, 6, 10), (22, 17, 19), S.FIXED_COROTATED, 19,
                                 keep=5000, vnoise=0.3, Fnoise=0.02, Cnoise=3.0, transfer=S.TRANSFER_PIC),
+        # Herschel-Bulkley (reading #39), sigma_Y = 5e4 Pa with strains beyond yield:
+        # viscous relaxation (eta = 1.5 x 2 mu dt) on the fused path, eta = 0 on the split path
+        "HB": S.block_scene("HB", 32, (9, 3, 8), (21, 13, 22), S.HERSCHEL_BULKLEY, 23,
+                            keep=6000, vnoise=0.2, Fnoise=0.08, Cnoise=2.0, yield_stress=5e4,
+                            viscosity=1.5 * 2 * 3.846e5 * 2e-5, plate_enabled=0),
+        "HB_gradw_eta0": S.block_scene("HBg", 32, (9, 3, 8), (21, 13, 22), S.HERSCHEL_BULKLEY, 24,
+                                       keep=4000, vnoise=0.2, Fnoise=0.08, Cnoise=2.0, yield_stress=5e4,
+                                       viscosity=0.0, plate_enabled=0, force_mode=S.FORCE_GRADW),
         # RPIC (reading #38): fused MLS path and split GRADW path
         "FC_rpic": S.block_scene("FCr", 32, (9, 6, 10), (22, 17, 19), S.FIXED_COROTATED, 21,
                                  keep=5000, vnoise=0.3, Fnoise=0.02, Cnoise=3.0, transfer=S.TRANSFER_RPIC),

@@ -268,3 +268,107 @@ def test_stvk_as_printed_is_elastic_hencky():
             q[:, 0] *= -1
         _, tq = elastoplastic_update((q @ F)[None], 4, mu, lam)
         assert np.allclose(tq[0], q @ tau[0] @ q.T, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# Herschel-Bulkley (reading #39)
+from oracle.constitutive import return_map_herschel_bulkley, tau_herschel_bulkley  # noqa: E402
+
+HB_MU, HB_KAPPA, HB_SY, HB_DT = 3.0e4, 8.0e4, 2.0e3, 1.0e-4
+
+
+def _hb_trials(rng, n, scale=0.3):
+    return np.eye(3) + rng.normal(size=(n, 3, 3)) * scale
+
+
+def _dev_norm(t):
+    dev = t - (np.trace(t, axis1=1, axis2=2) / 3.0)[:, None, None] * np.eye(3)
+    return np.linalg.norm(dev, axis=(1, 2)), dev
+
+
+def test_hb_stress_is_energy_derivative():
+    """tau = kappa/2 (J^2 - 1) I + mu dev(bbar) is (dpsi/dF) F^T of the compressible
+    neo-Hookean energy psi = mu/2 (tr(bbar) - 3) + kappa/2 ((J^2 - 1)/2 - ln J)
+    (central differences on random F with J > 0)."""
+    rng = np.random.default_rng(21)
+    F = _hb_trials(rng, 20, 0.2)
+    F = F[np.linalg.det(F) > 0.2]
+    mu, kappa = 1.3, 2.9
+
+    def psi(G):
+        J = np.linalg.det(G)
+        b = G @ G.T
+        return mu / 2 * (np.trace(b) * J ** (-2.0 / 3.0) - 3.0) + kappa / 2 * ((J * J - 1) / 2 - np.log(J))
+    h = 1e-6
+    for Fk, tk in zip(F, tau_herschel_bulkley(F, mu, kappa)):
+        P = np.zeros((3, 3))
+        for i in range(3):
+            for j in range(3):
+                E = np.zeros((3, 3))
+                E[i, j] = h
+                P[i, j] = (psi(Fk + E) - psi(Fk - E)) / (2 * h)
+        assert np.allclose(P @ Fk.T, tk, rtol=1e-6, atol=1e-7)
+
+
+def test_hb_inside_yield_and_infinite_viscosity_unchanged():
+    rng = np.random.default_rng(22)
+    F = _hb_trials(rng, 300, 0.002)                     # small strain: s < sqrt(2/3) sigma_Y
+    st, _ = _dev_norm(tau_herschel_bulkley(F, HB_MU, HB_KAPPA))
+    assert np.all(st < np.sqrt(2 / 3) * HB_SY)
+    FE, _ = return_map_herschel_bulkley(F, HB_MU, HB_KAPPA, HB_SY, 0.0, HB_DT)
+    assert np.array_equal(FE, F)
+    F = _hb_trials(rng, 300)
+    FE, _ = return_map_herschel_bulkley(F, HB_MU, HB_KAPPA, HB_SY, 1e30, HB_DT)   # eta -> infinity
+    assert np.allclose(FE, F, rtol=0, atol=1e-12)
+
+
+def test_hb_zero_viscosity_lands_on_yield_surface():
+    """eta = 0: s = sqrt(2/3) sigma_Y exactly; the flow is isochoric (det F^E = det
+    F_trial), keeps the deviator's direction and the rotation, and the map is
+    idempotent."""
+    rng = np.random.default_rng(23)
+    F = _hb_trials(rng, 500)
+    F[np.linalg.det(F) < 0, :, 0] *= -1.0                 # include only J > 0 here
+    st, dev_t = _dev_norm(tau_herschel_bulkley(F, HB_MU, HB_KAPPA))
+    plastic = st > np.sqrt(2 / 3) * HB_SY
+    assert plastic.mean() > 0.9
+    FE, tau = return_map_herschel_bulkley(F, HB_MU, HB_KAPPA, HB_SY, 0.0, HB_DT)
+    sn, dev_n = _dev_norm(tau)
+    assert np.allclose(sn[plastic], np.sqrt(2 / 3) * HB_SY, rtol=1e-10)
+    assert np.allclose(np.linalg.det(FE), np.linalg.det(F), rtol=1e-12)
+    cos = np.einsum("pij,pij->p", dev_n, dev_t) / (sn * st)
+    assert np.allclose(cos[plastic], 1.0, atol=1e-12)
+    # same rotation: F^E F_trial^-1 is symmetric positive definite (a pure stretch)
+    Sx = FE @ np.linalg.inv(F)
+    assert np.allclose(Sx, np.swapaxes(Sx, 1, 2), atol=1e-10)
+    FE2, tau2 = return_map_herschel_bulkley(FE, HB_MU, HB_KAPPA, HB_SY, 0.0, HB_DT)
+    assert np.allclose(FE2, FE, atol=1e-10) and np.allclose(tau2, tau, rtol=1e-9, atol=1e-6)
+
+
+def test_hb_viscous_relaxation_magnitude():
+    """0 < eta < inf: ||dev tau(F^E)|| = s - (s - sqrt(2/3) sigma_Y) / (1 + eta/(2 mu dt))
+    (PAPER.md line 548), between the yield surface and the trial value."""
+    rng = np.random.default_rng(24)
+    F = _hb_trials(rng, 300)
+    F[np.linalg.det(F) < 0, :, 0] *= -1.0
+    eta = 2.0 * HB_MU * HB_DT * 1.5                      # relaxation factor 1 / 2.5
+    st, _ = _dev_norm(tau_herschel_bulkley(F, HB_MU, HB_KAPPA))
+    y = np.sqrt(2 / 3) * HB_SY
+    _, tau = return_map_herschel_bulkley(F, HB_MU, HB_KAPPA, HB_SY, eta, HB_DT)
+    sn, _ = _dev_norm(tau)
+    p = st > y
+    assert np.allclose(sn[p], st[p] - (st[p] - y) / 2.5, rtol=1e-10)
+    assert np.all((sn[p] > y) & (sn[p] < st[p]))
+
+
+def test_hb_rotation_equivariance():
+    rng = np.random.default_rng(25)
+    F = _hb_trials(rng, 100)
+    A = rng.normal(size=(100, 3, 3))
+    Q, R = np.linalg.qr(A)
+    Q = Q * np.sign(np.diagonal(R, axis1=1, axis2=2))[:, None, :]
+    Q[np.linalg.det(Q) < 0, :, 0] *= -1.0
+    FE, tau = return_map_herschel_bulkley(F, HB_MU, HB_KAPPA, HB_SY, 0.3, HB_DT)
+    FEr, taur = return_map_herschel_bulkley(Q @ F, HB_MU, HB_KAPPA, HB_SY, 0.3, HB_DT)
+    assert np.allclose(FEr, Q @ FE, atol=1e-10)
+    assert np.allclose(taur, Q @ tau @ np.swapaxes(Q, 1, 2), rtol=1e-9, atol=1e-5)
