@@ -270,6 +270,21 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
                                          const float* z_prev, int64_t* counts_out,
                                          int32_t on_device);
 
+/* One latent-space time step of the reduced model (§5; ABI 5):
+ *   (1) build_integration_set(n_ref, X_all, n_sample, sample_idx) at z_n, with
+ *       network inference of x, v, C on N; z_{n-1} = z_prev if given (n_scenes x r),
+ *       else the z_n of the previous rom_step, else (first call after set_latents)
+ *       the infer_state default,
+ *   (2) one MPM substep on N (the sample particles' states are those of the
+ *       full-order MPM, line 256),
+ *   (3) invert_latents(n_sample, gn_iters): z_{n+1} from Eq. (10) on S.
+ * z_out (n_scenes x r, host or device per on_device, or NULL) receives z_{n+1};
+ * counts_out (host, n_scenes, or NULL) |N_s|.  Synchronous.  Errors as for the three
+ * calls; 1 <= gn_iters <= 16. */
+nsf_status nsf_mpm_rom_step(nsf_mpm* h, int64_t n_ref, const float* X_all, int32_t n_sample,
+                            const int32_t* sample_idx, const float* z_prev, int32_t gn_iters, float* z_out,
+                            int64_t* counts_out, int32_t on_device);
+
 /* Enqueue n >= 0 substeps on the handle's stream (a cached CUDA graph of the
  * substep is replayed).  Asynchronous.  NSF_ERR_BAD_STATE before
  * load_particles, or for NSF without load_stress_field / set_latents. */

@@ -38,7 +38,7 @@ EXPORTS = ["nsf_mpm_abi_version", "nsf_mpm_create", "nsf_mpm_set_stream", "nsf_m
            "nsf_mpm_substep", "nsf_mpm_eval_stress_field", "nsf_mpm_read_state", "nsf_mpm_sync",
            "nsf_mpm_step_count", "nsf_mpm_inverted_count", "nsf_mpm_last_error", "nsf_mpm_destroy",
            "nsf_mpm_debug_bins", "nsf_mpm_debug_grid", "nsf_mpm_set_profiling",
-           "nsf_mpm_kernel_times", "nsf_mpm_launches_per_substep", "nsf_mpm_launch_count"]
+           "nsf_mpm_kernel_times", "nsf_mpm_launches_per_substep", "nsf_mpm_launch_count", "nsf_mpm_rom_step"]
 
 
 class nsf_material(C.Structure):
@@ -86,6 +86,7 @@ def lib():
         "nsf_mpm_load_affine_field": (i32, [vp, i32, i32, i32, i32, vp, vp, i32]),
         "nsf_mpm_infer_state": (i32, [vp, vp, i32]),
         "nsf_mpm_build_integration_set": (i32, [vp, i64, vp, i32, vp, vp, dp(i64), i32]),
+        "nsf_mpm_rom_step": (i32, [vp, i64, vp, i32, vp, vp, i32, vp, dp(i64), i32]),
         "nsf_mpm_substep": (i32, [vp, i32]),
         "nsf_mpm_eval_stress_field": (i32, [vp, vp, i64, vp, vp, i32]),
         "nsf_mpm_read_state": (i32, [vp, u32, dp(vp), i32]),
@@ -262,6 +263,21 @@ def nsf_mpm_build_integration_set(h, X_all, sample_idx, z_prev=None, n_scenes=1)
     return np.array(counts[:], dtype=np.int64)
 
 
+def nsf_mpm_rom_step(h, X_all, sample_idx, gn_iters: int, n_scenes: int, r: int, z_prev=None):
+    """One reduced-model time step (inference on N -> substep -> inversion; header).
+    X_all: n_ref x 3, sample_idx: n_scenes x n_sample (numpy).  Returns (z_{n+1}
+    (n_scenes, r) float32, |N_s| (n_scenes,) int64)."""
+    X_all = np.ascontiguousarray(X_all, dtype=np.float32)
+    sidx = np.ascontiguousarray(sample_idx, dtype=np.int32)
+    n_sample = int(np.prod(sidx.shape)) // n_scenes
+    z = np.empty((n_scenes, r), dtype=np.float32)
+    counts = (C.c_int64 * n_scenes)()
+    zp = None if z_prev is None else np.ascontiguousarray(z_prev, dtype=np.float32)
+    _check(h, lib().nsf_mpm_rom_step(h, X_all.shape[0], X_all.ctypes.data, n_sample, sidx.ctypes.data,
+                                     None if zp is None else zp.ctypes.data, gn_iters, z.ctypes.data, counts, 0))
+    return z, np.array(counts[:], dtype=np.int64)
+
+
 def nsf_mpm_invert_latents(h, n_sample: int, n_iters: int, z_out=None):
     """Gauss-Newton network inversion (header).  z_out: None, a float32 numpy array
     (n_scenes x r) or a CUDA tensor, filled with z_hat."""
@@ -427,6 +443,12 @@ class Simulator:
         counts = nsf_mpm_build_integration_set(self.h, X_all, sample_idx, z_prev, self.cfg.n_scenes)
         self.n = int(counts.sum())
         return counts
+
+    def rom_step(self, X_all, sample_idx, gn_iters=3, z_prev=None):
+        """One latent-space step: returns z_{n+1}, |N_s|."""
+        z, counts = nsf_mpm_rom_step(self.h, X_all, sample_idx, gn_iters, self.cfg.n_scenes, self._r, z_prev)
+        self.n = int(counts.sum())
+        return z, counts
 
     def invert_latents(self, n_sample, n_iters=3):
         """Network inversion; returns z_hat (n_scenes x r)."""

@@ -66,6 +66,8 @@ struct nsf_mpm {
   float* lb = nullptr;
   bool ldef_loaded = false;
   float* zprev = nullptr;             // z_{n-1} of inference (n_scenes x r)
+  float* zrom = nullptr;              // rom_step: the latent the last step started from (its z_{n-1})
+  bool zrom_valid = false;
   uint16_t* gW = nullptr;
   float* gb = nullptr;
   bool gdef_loaded = false;
@@ -660,9 +662,19 @@ nsf_status nsf_mpm_infer_state(nsf_mpm* h, const float* z_prev, int32_t on_devic
   return enqueue_infer(h);
 }
 
+static nsf_status build_set_impl(nsf_mpm* h, int64_t n_ref, const float* X_all, int32_t n_sample,
+                                 const int32_t* sample_idx, const float* z_prev, int32_t zprev_on_device,
+                                 int64_t* counts_out, int32_t on_device);
+
 nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float* X_all, int32_t n_sample,
                                          const int32_t* sample_idx, const float* z_prev, int64_t* counts_out,
                                          int32_t on_device) {
+  return build_set_impl(h, n_ref, X_all, n_sample, sample_idx, z_prev, on_device, counts_out, on_device);
+}
+
+static nsf_status build_set_impl(nsf_mpm* h, int64_t n_ref, const float* X_all, int32_t n_sample,
+                                 const int32_t* sample_idx, const float* z_prev, int32_t zprev_on_device,
+                                 int64_t* counts_out, int32_t on_device) {
   if (!h) return NSF_ERR_INVALID_ARGUMENT;
   if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
   nsf_status s;
@@ -770,7 +782,7 @@ nsf_status nsf_mpm_build_integration_set(nsf_mpm* h, int64_t n_ref, const float*
   pipeline_aos_to_planes(h->stream, n_new, Xnew, 3, h->X, h->pitch);
   pipeline_on_mlp(h, &h->pb);
   invalidate_graph(h);
-  TRY(set_zprev(h, z_prev, on_device));
+  TRY(set_zprev(h, z_prev, zprev_on_device));
   TRY(enqueue_infer(h));
   TRYCU(cudaStreamSynchronize(h->stream));
   if (counts_out) memcpy(counts_out, counts.data(), sizeof(int64_t) * ns);
@@ -808,6 +820,37 @@ nsf_status nsf_mpm_invert_latents(nsf_mpm* h, int32_t n_sample, int32_t n_iters,
   return NSF_OK;
 }
 
+// One latent-space time step of the reduced model (§5):
+// (1) sample / integration particles and network inference at z_n (lines 251-254,
+// 265-269), (2) one MPM substep on N (lines 255-256), (3) network inversion of
+// Eq. (10) on S (lines 257-263): z_{n+1} becomes the handle's latent (dz = 0).  The
+// previous call's z_n is kept on the device and serves as this call's z_{n-1}
+// unless the caller passes z_prev.
+nsf_status nsf_mpm_rom_step(nsf_mpm* h, int64_t n_ref, const float* X_all, int32_t n_sample,
+                            const int32_t* sample_idx, const float* z_prev, int32_t gn_iters, float* z_out,
+                            int64_t* counts_out, int32_t on_device) {
+  if (!h) return NSF_ERR_INVALID_ARGUMENT;
+  if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
+  if (gn_iters < 1 || gn_iters > 16) return fail(h, NSF_ERR_INVALID_ARGUMENT, "1 <= gn_iters <= 16");
+  nsf_status s;
+  if ((s = inference_ready(h)) != NSF_OK) return s;
+  const size_t zb = sizeof(float) * (size_t)h->mat.n_scenes * h->r;
+  const float* zp = z_prev ? z_prev : (h->zrom_valid ? h->zrom : nullptr);
+  if ((s = build_set_impl(h, n_ref, X_all, n_sample, sample_idx, zp, z_prev ? on_device : 1, counts_out,
+                          on_device)) != NSF_OK)
+    return s;
+  if ((s = nsf_mpm_substep(h, 1)) != NSF_OK) return s;
+  // z_n (the latent of this substep: z + n dz at n = step - 1) is the next call's z_{n-1}
+  if (!h->zrom) {
+    if ((s = alloc_into(h, &h->zrom, zb)) != NSF_OK) return s;
+  }
+  launch_latent_at(h->stream, (int64_t)h->mat.n_scenes * h->r, h->z, h->dz, h->host_step - 1, h->zrom);
+  CK(cudaGetLastError());
+  if ((s = nsf_mpm_invert_latents(h, n_sample, gn_iters, z_out, on_device)) != NSF_OK) return s;
+  h->zrom_valid = true;
+  return NSF_OK;
+}
+
 nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const float* dz, int32_t on_device) {
   if (!h) return NSF_ERR_INVALID_ARGUMENT;
   if (h->poisoned) return fail(h, NSF_ERR_CUDA, "handle poisoned");
@@ -827,6 +870,7 @@ nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const floa
   CK(cudaStreamSynchronize(h->stream));
   h->r = r;
   h->latents_loaded = true;
+  h->zrom_valid = false;
   invalidate_graph(h);
   return NSF_OK;
 }

@@ -83,3 +83,31 @@ def fp32_spread(sc, gnet, x, z_start, n_sample, orders=6, per_order=False):
         OI.g_with_tangents = orig
     gap = float(np.linalg.norm(ze - zo) / step)
     return (out if per_order else max(out)), gap
+
+
+def fp32_objective_spread(XS, targets, z_start, gnet, iters, orders=8):
+    """For one scene: the oracle's Gauss-Newton result z_o from z_start (emulate
+    mode, fp64), the Eq. (10) objective at z_start and z_o, and the largest excess
+    f(z_fp32) - f(z_o) over `orders` fp32-accumulated evaluations of the same
+    network (each running its own Gauss-Newton).  Objectives are evaluated by the
+    fp64 emulating oracle."""
+    XS = np.asarray(XS, np.float64)
+    t = np.asarray(targets, np.float64)
+    off = np.array([0, XS.shape[0]])
+    n = XS.shape[0]
+
+    def f(z):
+        return float(np.sum((OI.g_with_tangents(XS, np.asarray(z, np.float64), gnet, "emulate")[0] - t) ** 2))
+    zo = OI.invert_scenes(XS, t, off, n, np.asarray(z_start, np.float64)[None], gnet, iters, "emulate")[0]
+    f0, fo = f(z_start), f(zo)
+    worst = 0.0
+    orig = OI.g_with_tangents
+    try:
+        for s in range(orders):
+            OI.g_with_tangents = lambda X, z, mlp, mode="emulate", s_=s: _g_tangents_fp32(X, z, mlp, s_)
+            zf = OI.invert_scenes(XS, t, off, n, np.asarray(z_start, np.float64)[None], gnet, iters, "emulate")[0]
+            OI.g_with_tangents = orig
+            worst = max(worst, f(zf) - fo)
+    finally:
+        OI.g_with_tangents = orig
+    return zo, f0, fo, worst
