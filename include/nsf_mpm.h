@@ -146,6 +146,14 @@ typedef struct {
 #define NSF_FIELD_TAU 16u /* n x 6 Voigt (stress used by the NEXT P2G) */
 #define NSF_FIELD_TAU_Y 32u /* n x 1 per-particle von Mises yield stress (ABI 3) */
 
+/* Work counters of the fused full-order kernel since the last call (statistics
+ * build only, -DNSF_STATS=1; else NSF_ERR_BAD_STATE): out[0..n-1] = segments,
+ * particles, staged P2G rows, listed (out-of-block) rows, inline scatters,
+ * out-of-tile gathers, phase-1 passes, and the clock cycles (thread 0 of each CTA)
+ * spent staging the velocity tile, in phase 1 and in phase 2, then out-of-block
+ * particles.  Synchronizes the handle's stream; clears the counters.  (ABI 5) */
+nsf_status nsf_mpm_debug_stats(nsf_mpm* h, int64_t* out, int32_t n);
+
 /* Version of this header's ABI (NSF_MPM_ABI_VERSION). */
 int32_t nsf_mpm_abi_version(void);
 

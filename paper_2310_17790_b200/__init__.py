@@ -38,7 +38,8 @@ EXPORTS = ["nsf_mpm_abi_version", "nsf_mpm_create", "nsf_mpm_set_stream", "nsf_m
            "nsf_mpm_substep", "nsf_mpm_eval_stress_field", "nsf_mpm_read_state", "nsf_mpm_sync",
            "nsf_mpm_step_count", "nsf_mpm_inverted_count", "nsf_mpm_last_error", "nsf_mpm_destroy",
            "nsf_mpm_debug_bins", "nsf_mpm_debug_grid", "nsf_mpm_set_profiling",
-           "nsf_mpm_kernel_times", "nsf_mpm_launches_per_substep", "nsf_mpm_launch_count", "nsf_mpm_rom_step"]
+           "nsf_mpm_kernel_times", "nsf_mpm_launches_per_substep", "nsf_mpm_launch_count", "nsf_mpm_rom_step",
+           "nsf_mpm_debug_stats"]
 
 
 class nsf_material(C.Structure):
@@ -87,6 +88,7 @@ def lib():
         "nsf_mpm_infer_state": (i32, [vp, vp, i32]),
         "nsf_mpm_build_integration_set": (i32, [vp, i64, vp, i32, vp, vp, dp(i64), i32]),
         "nsf_mpm_rom_step": (i32, [vp, i64, vp, i32, vp, vp, i32, vp, dp(i64), i32]),
+        "nsf_mpm_debug_stats": (i32, [vp, dp(i64), i32]),
         "nsf_mpm_substep": (i32, [vp, i32]),
         "nsf_mpm_eval_stress_field": (i32, [vp, vp, i64, vp, vp, i32]),
         "nsf_mpm_read_state": (i32, [vp, u32, dp(vp), i32]),
@@ -276,6 +278,17 @@ def nsf_mpm_rom_step(h, X_all, sample_idx, gn_iters: int, n_scenes: int, r: int,
     _check(h, lib().nsf_mpm_rom_step(h, X_all.shape[0], X_all.ctypes.data, n_sample, sidx.ctypes.data,
                                      None if zp is None else zp.ctypes.data, gn_iters, z.ctypes.data, counts, 0))
     return z, np.array(counts[:], dtype=np.int64)
+
+
+STAT_NAMES = ["segments", "particles", "staged", "listed", "inline", "out_of_tile", "passes", "cyc_tile",
+              "cyc_phase1", "cyc_phase2", "out_of_block"]
+
+
+def nsf_mpm_debug_stats(h) -> dict:
+    """Work counters of the statistics build (header); raises NsfError otherwise."""
+    out = (C.c_int64 * 16)()
+    _check(h, lib().nsf_mpm_debug_stats(h, out, 16))
+    return {k: int(out[i]) for i, k in enumerate(STAT_NAMES)}
 
 
 def nsf_mpm_invert_latents(h, n_sample: int, n_iters: int, z_out=None):

@@ -25,6 +25,10 @@
 
 namespace nsf {
 
+#if NSF_STATS
+__device__ unsigned long long g_nsf_stats[kStCount];
+#endif
+
 __device__ __forceinline__ void red_add_v4_t(float4* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -1173,6 +1177,7 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       for (int k = 0; k < 9; ++k) G[k] = Cn[k];
       if (P.rpic) skew_part(Cn);   // RPIC: the transfer's C_p; G keeps the full gradient
     } else {
+      NSF_STAT_ADD(kStOutOfTile, 1);
       g2p_gather<0, ROT>(x, gvel, P, vn, Cn, G, y_plate);   // ROT: gvel holds raw P2G sums
     }
     bool ok = true;
@@ -1307,19 +1312,31 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
   // segment tickets: the first here, each next one claimed after phase 1 of the
   // current segment (its round trip overlaps phase 2)
   if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
+#if NSF_STATS
+  long long t_mark = clock64();
+#endif
   while (true) {
     __syncthreads();   // also: previous segment's readers of slot are done
+#if NSF_STATS
+    if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycPhase2, t - t_mark); t_mark = t; }
+#endif
     const int bi = sm.next;
     if (bi >= nblk) break;
     const int key = nonempty[bi];
     const BlockCoord bc = decode_block(key, P);
     const int s0 = block_start[key], s1 = block_start[key + 1];
+    if (tid == 0) {
+      NSF_STAT_ADD(kStSegments, 1);
+      NSF_STAT_ADD(kStParticles, s1 - s0);
+      NSF_STAT_ADD(kStPasses, (s1 - s0 + NT - 1) / NT);
+    }
     const int64_t scene_block0 = (int64_t)bc.scene * P.blocks_per_scene;
     float4* gacc = acc + (int64_t)bc.scene * P.nodes_per_scene;
     const float4* gvel = vel + (int64_t)bc.scene * P.nodes_per_scene;
     if (tid < 64) sm.pop[tid] = 0;
     if (tid == 0) sm.nsc = 0;
     const int o[3] = {4 * bc.b[0] - 1, 4 * bc.b[1] - 1, 4 * bc.b[2] - 1};   // tile origin (grid node)
+
     float x0[3], F0[9];   // the first particle's x, F: loaded under the tile copy
     if (DO_G2P && NSF_FUSED_VTILE && ROT) {
       // raw P2G sums of the tile's nodes (L2-resident: reduced by the previous
@@ -1366,6 +1383,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     if (DO_G2P && !ROT && s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+#if NSF_STATS
+    if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycTile, t - t_mark); t_mark = t; }
+#endif
     // ---- phase 1: per particle ----
     for (int j = s0 + tid; j < s1; j += NT) {
       float xn[3], vn[3], Cn[9], tau[6];
@@ -1401,14 +1421,18 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       if (core) {
         cell = (c[0] << 4) | (c[1] << 2) | c[2];
         rank = atomicAdd(&sm.pop[cell], 1);
+      } else {
+        NSF_STAT_ADD(kStOutOfBlock, 1);
       }
       bool inline_scatter = false;
       if (rank < ROWS) {
+        NSF_STAT_ADD(kStStaged, 1);
         NSF_CHECK(cell >= 0 && cell < 64 && (cell + 1) * FusedSlots<ROWS>::kCellStride4 > rank * kRowF4 + 5);
         p2g_stage_row(xn, vn, Cn, tau, sm.slot + cell * FusedSlots<ROWS>::kCellStride4 + rank * kRowF4, P);
       } else {
         const int e = atomicAdd(&sm.nsc, 1);
         if (e < kScatterCap) {
+          NSF_STAT_ADD(kStListed, 1);
           int pb = 0;
 #pragma unroll
           for (int a = 0; a < 3; ++a)
@@ -1416,6 +1440,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
           p2g_stage_row(xn, vn, Cn, tau, sm.sc + e * kRowF4, P, __int_as_float(pb));
         } else {
           inline_scatter = true;
+          NSF_STAT_ADD(kStInline, 1);
         }
       }
 #if NSF_WARP_SCATTER
@@ -1425,11 +1450,23 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
 #endif
     }
     __syncthreads();
+#if NSF_STATS
+    if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycPhase1, t - t_mark); t_mark = t; }
+#endif
     if (tid == 0) sm.next = atomicAdd(&counters[3], 1);   // the next segment (bi is in registers)
     // ---- phase 2: per (cell, stencil plane) register accumulation ----
     float accm[9], accp[9][3];
 #pragma unroll
     for (int k = 0; k < 9; ++k) { accm[k] = 0.f; accp[k][0] = accp[k][1] = accp[k][2] = 0.f; }
+    // the grid blocks the segment's cell sums reduce into (its block and the +1
+    // neighbours) are flagged by the last 8 helper threads, whose flag round trips
+    // then overlap the accumulation instead of trailing it
+    if (NT > 192 && tid >= NT - 8) {
+      const int t8 = tid - (NT - 8);
+      const int b0 = bc.b[0] + (t8 >> 2), b1 = bc.b[1] + ((t8 >> 1) & 1), b2 = bc.b[2] + (t8 & 1);
+      if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])
+        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
+    }
     {
       const int nsc = min(sm.nsc, kScatterCap);
       if (NT > 192) {
@@ -1456,7 +1493,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         red_add_v4_t(gacc + off, accm[k] * m, accp[k][0], accp[k][1], accp[k][2]);
       }
     }
-    if (tid < 8) {
+    if (NT <= 192 && tid < 8) {   // (no helper threads)
       const int b0 = bc.b[0] + (tid >> 2), b1 = bc.b[1] + ((tid >> 1) & 1), b2 = bc.b[2] + (tid & 1);
       if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])
         touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
@@ -1677,4 +1714,22 @@ void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, c
   k_reorder<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Sin, Sout, n, ids_in, ids_out, perm);
 }
 
+}  // namespace nsf
+
+namespace nsf {
+// statistics build: copy out and clear the counters (nsf_mpm_debug_stats)
+int stats_read(cudaStream_t st, int64_t* out, int n) {
+#if NSF_STATS
+  unsigned long long h[kStCount];
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(h, g_nsf_stats, sizeof(h)) != cudaSuccess) return -1;
+  for (int i = 0; i < n && i < kStCount; ++i) out[i] = (int64_t)h[i];
+  const unsigned long long z[kStCount] = {};
+  if (cudaMemcpyToSymbol(g_nsf_stats, z, sizeof(z)) != cudaSuccess) return -1;
+  return kStCount;
+#else
+  (void)st; (void)out; (void)n;
+  return 0;
+#endif
+}
 }  // namespace nsf

@@ -150,6 +150,7 @@ void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_
 void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                                int32_t* ids_out, PipelineBuffers* pb, const DevParams& P);
 int num_sms();
+int stats_read(cudaStream_t st, int64_t* out, int n);   // statistics build only (else 0)
 void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                       int32_t* ids_out, const PipelineBuffers* pb, const float4* vel, const int64_t* scene_off,
                       int n_scenes, const DevParams& P, DevErr* err, int64_t* d_step);

@@ -1071,6 +1071,14 @@ int32_t nsf_mpm_kernel_times(nsf_mpm* h, const char** names, double* total_ms, i
   return k;
 }
 
+nsf_status nsf_mpm_debug_stats(nsf_mpm* h, int64_t* out, int32_t n) {
+  if (!h || !out || n < 1) return NSF_ERR_INVALID_ARGUMENT;
+  const int k = stats_read(h->stream, out, n);
+  if (k < 0) return cuda_fail(h, cudaGetLastError(), "debug_stats");
+  if (k == 0) return fail(h, NSF_ERR_BAD_STATE, "work counters need the statistics build (-DNSF_STATS=1)");
+  return NSF_OK;
+}
+
 int32_t nsf_mpm_launches_per_substep(nsf_mpm* h) {
   if (!h) return -1;
   return pipeline_launches_per_substep(h, &h->pb);

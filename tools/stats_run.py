@@ -1,0 +1,30 @@
+"""Work counters of the fused kernel per substep window (statistics build):
+    NSF_MPM_LIB=paper_2310_17790_b200/_ab/stats.so python tools/stats_run.py C3 [preroll] [steps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2310_17790_b200 as nsf  # noqa: E402
+import scenes  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+pre = int(sys.argv[2]) if len(sys.argv) > 2 else 250
+K = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+sc = scenes.by_name(name)
+sim = nsf.Simulator(sc.cfg)
+sim.load_scene(sc)
+sim.substep(pre)
+sim.sync()
+nsf.nsf_mpm_debug_stats(sim.h)
+sim.substep(K)
+st = nsf.nsf_mpm_debug_stats(sim.h)
+sim.close()
+per = {k: v / K for k, v in st.items()}
+n = sc.n
+print(f"{name} substeps {pre}..{pre + K}: per substep " + ", ".join(f"{k} {v:.0f}" for k, v in per.items()))
+tot = per["cyc_tile"] + per["cyc_phase1"] + per["cyc_phase2"]
+print(f"  cycles share: tile {per['cyc_tile'] / tot:.2f} phase1 {per['cyc_phase1'] / tot:.2f} "
+      f"phase2 {per['cyc_phase2'] / tot:.2f}; per segment: tile {per['cyc_tile'] / per['segments']:.0f} "
+      f"p1 {per['cyc_phase1'] / per['segments']:.0f} p2 {per['cyc_phase2'] / per['segments']:.0f} cycles; "
+      f"listed {per['listed'] / n:.3%} inline {per['inline'] / n:.3%} out-of-tile {per['out_of_tile'] / n:.3%} "
+      f"out-of-block {per['out_of_block'] / n:.3%}")
