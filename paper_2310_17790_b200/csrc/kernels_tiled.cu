@@ -900,6 +900,9 @@ __device__ __forceinline__ void cp_async16_f(void* smem, const void* gmem, int s
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
 }
 
+#ifndef NSF_P2G_ROW_UNROLL
+#define NSF_P2G_ROW_UNROLL 1   // 2: phase-2 row loop unrolled by two
+#endif
 #ifndef NSF_F2_G2P
 #define NSF_F2_G2P 1   // G2P gather on paired fp32 FMA (FFMA2, sm_100)
 #endif
@@ -1056,6 +1059,9 @@ __device__ __forceinline__ void p2g_accumulate_rows(const float4* slot, int my_c
   for (int k = 0; k < 9; ++k) pxy[k] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < 3; ++k) { pz01[k] = m01[k] = make_float2(0.f, 0.f); pz2[k] = m2[k] = 0.f; }
+#if NSF_P2G_ROW_UNROLL == 2
+#pragma unroll 2
+#endif
   for (int r = 0; r < rows; ++r, rp += kRowF4) {
     const float4 A = rp[0], U = rp[1], Q0 = rp[2], Q1 = rp[3], Q2 = rp[4], Z = rp[5];
     const float wx = ox == 0 ? A.x : (ox == 1 ? A.y : A.z);
@@ -1454,6 +1460,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycPhase1, t - t_mark); t_mark = t; }
 #endif
     if (tid == 0) sm.next = atomicAdd(&counters[3], 1);   // the next segment (bi is in registers)
+#if NSF_STATS
+    long long t_p2 = clock64();
+#endif
     // ---- phase 2: per (cell, stencil plane) register accumulation ----
     float accm[9], accp[9][3];
 #pragma unroll
@@ -1493,6 +1502,10 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         red_add_v4_t(gacc + off, accm[k] * m, accp[k][0], accp[k][1], accp[k][2]);
       }
     }
+#if NSF_STATS
+    if (tid == 0) NSF_STAT_ADD(kStCycP2Acc, clock64() - t_p2);
+    if (tid == NT - 1) NSF_STAT_ADD(kStCycP2Help, clock64() - t_p2);
+#endif
     if (NT <= 192 && tid < 8) {   // (no helper threads)
       const int b0 = bc.b[0] + (tid >> 2), b1 = bc.b[1] + ((tid >> 1) & 1), b2 = bc.b[2] + (tid & 1);
       if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])

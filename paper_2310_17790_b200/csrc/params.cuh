@@ -24,7 +24,8 @@
 #define NSF_STATS 0
 #endif
 enum StatIdx : int { kStSegments, kStParticles, kStStaged, kStListed, kStInline, kStOutOfTile, kStPasses,
-                     kStCycTile, kStCycPhase1, kStCycPhase2, kStOutOfBlock, kStCount = 16 };
+                     kStCycTile, kStCycPhase1, kStCycPhase2, kStOutOfBlock, kStCycP2Acc, kStCycP2Help,
+                     kStCount = 16 };
 #if NSF_STATS
 extern __device__ unsigned long long g_nsf_stats[kStCount];
 #define NSF_STAT_ADD(i, v) atomicAdd(&g_nsf_stats[(i)], (unsigned long long)(v))

@@ -27,4 +27,5 @@ print(f"  cycles share: tile {per['cyc_tile'] / tot:.2f} phase1 {per['cyc_phase1
       f"phase2 {per['cyc_phase2'] / tot:.2f}; per segment: tile {per['cyc_tile'] / per['segments']:.0f} "
       f"p1 {per['cyc_phase1'] / per['segments']:.0f} p2 {per['cyc_phase2'] / per['segments']:.0f} cycles; "
       f"listed {per['listed'] / n:.3%} inline {per['inline'] / n:.3%} out-of-tile {per['out_of_tile'] / n:.3%} "
-      f"out-of-block {per['out_of_block'] / n:.3%}")
+      f"out-of-block {per['out_of_block'] / n:.3%}; phase 2 of thread 0 (accumulate) "
+      f"{per['cyc_p2_acc'] / per['segments']:.0f}, of the last helper {per['cyc_p2_help'] / per['segments']:.0f} cycles")
