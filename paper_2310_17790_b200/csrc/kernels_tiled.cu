@@ -1684,6 +1684,10 @@ static void launch_g2p2g_r(cudaStream_t st, bool do_g2p, float* S, const int32_t
                                                                                       d_step);
     return;
   }
+  if (do_g2p && pb->dense3s) {   // dense, 3 CTAs per SM of 192 threads (A/B)
+    launch_g2p2g_t<true, kRowsF, 3, 192, false, ROT>(st, S, ids, vel, acc, pb, P, err, d_step);
+    return;
+  }
   if (do_g2p && pb->dense2) {   // dense, 2 CTAs per SM
     launch_g2p2g_t<true, kRowsF, 2, NSF_DENSE_THREADS, false, ROT>(st, S, ids, vel, acc, pb, P, err, d_step);
     return;

@@ -208,11 +208,15 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     if (fv && strncmp(fv, "dense", 5) == 0) pb->sparse = false;
     else if (fv && strcmp(fv, "sparse") == 0) pb->sparse = true;
     else pb->sparse = nblk > 0 && v.n < (int64_t)kSparseParticlesPerBlock * nblk;
-    // dense scenes run the 2-CTA/SM instantiation (128 registers: the paired-FMA
-    // transfer loops need them; the 3-CTA one spills, C3 102.5 -> 98.1 us)
+    // dense scenes: 3 CTAs/SM of 192 threads (96 registers, no spill with the
+    // paired-FMA loops; a 512-particle segment is three passes either way) when
+    // there are at least 2 segments per CTA of that grid (C3: 95.9 -> 92.3 us),
+    // else 2 CTAs/SM of 256 threads (128 registers; C2: 36.6 vs 40.8 us)
+    const bool many = nblk >= 2 * 3 * num_sms();
+    pb->dense3s = fv ? strcmp(fv, "dense3s") == 0 : (!pb->sparse && many);
     if (fv && strcmp(fv, "dense2") == 0) pb->dense2 = true;
     else if (fv) pb->dense2 = false;
-    else pb->dense2 = !pb->sparse;
+    else pb->dense2 = !pb->sparse && !many;
     // grid update inside the fused kernel only where it measured faster: few
     // segments per CTA (fewer than 2 per CTA of a 3-CTA/SM grid, e.g. C2: 37.0 ->
     // 36.3 us); C3 (~7 segments per CTA: 103.7 vs 98.1 us) and the sparse variant

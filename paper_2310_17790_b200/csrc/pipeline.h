@@ -49,7 +49,8 @@ struct PipelineBuffers {
   bool tiled = false;               // dense tiled path (full-order models)
   bool fused = false;               // fused G2P2G pipeline (full-order, MLS)
   bool sparse = false;
-  bool dense2 = false;      // dense variant at 2 CTAs per SM (128 registers): few segments per CTA
+  bool dense2 = false;      // dense variant at 2 CTAs per SM (128 registers)
+  bool dense3s = false;     // dense variant at 3 CTAs per SM of 192 threads (96 registers): many segments
   bool nsf_sorted = false;          // reduced path: points kept in block order (periodic re-binning)              // fused kernel variant for few particles per block (chosen at load)
   int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
