@@ -1266,12 +1266,19 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
 // rotation instead; the segment's velocity tile is staged from the raw P2G sums
 // with every node updated on the way, the blocks of the cleared buffer
 // are zeroed, and the last CTA to finish advances the step counter.
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, bool ROT = false>
+// GUM: where the grid update of the P2G reduced here runs:
+//   0  in k_grid_update_list before the next substep;
+//   1  (ROT) in the next k_g2p2g as it stages its velocity tiles (three rotating grids);
+//   2  (GUB) at the end of this kernel, after a grid-wide barrier (every CTA of the
+//      persistent grid is resident): all CTAs update the touched blocks, so a substep
+//      is one launch and the next G2P reads `vel` directly.
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int GUM = 0>
 __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
         int64_t* d_step, RotGrid rg) {
+  constexpr bool ROT = GUM == 1, GUB = GUM == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FusedSmemT<ROWS>& sm = *reinterpret_cast<FusedSmemT<ROWS>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -1280,7 +1287,14 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
   const int nblk = *(volatile int32_t*)&counters[0];
   int64_t kstep = 0;
   float y_plate = 0.0f;
-  if (ROT) {
+  int* const cnt2 = list_count;   // GUB: the two count slots (+ [2] sel, [3] barrier generation)
+  if (GUB) {
+    // every CTA reads the step counter before anyone advances it (at the end);
+    // the P2G written here is that of state kw + 1 and appends to slot kw & 1
+    kstep = *(volatile const int64_t*)d_step;
+    const int64_t kw = DO_G2P ? kstep : kstep - 1;
+    list_count = cnt2 + (int)(kw & 1);
+  } else if (ROT) {
     // kernel index kw: the P2G written here is that of state kw + 1 (kw = -1 for
     // the P2G of the loaded state); it reads buffer kw % 3, writes (kw + 1) % 3,
     // clears (kw + 2) % 3
@@ -1315,6 +1329,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     list_count += *(volatile const int*)(list_count + 2);
     if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
   }
+  (void)cnt2;
   // segment tickets: the first here, each next one claimed after phase 1 of the
   // current segment (its round trip overlaps phase 2)
   if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
@@ -1512,6 +1527,57 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
     }
   }
+  if (GUB) {
+    // grid-wide barrier (generation counter; all CTAs are resident: the grid is one
+    // wave of the persistent kernel): every CTA's reductions are complete and visible
+    __syncthreads();
+    if (tid == 0) {
+      volatile int* genp = cnt2 + 3;
+      const int g0 = *genp;
+      __threadfence();
+      if (atomicAdd(&counters[2], 1) == (int)gridDim.x - 1) {
+        counters[2] = 0;
+        __threadfence();
+        atomicAdd(cnt2 + 3, 1);
+      } else {
+        while (*genp == g0) __nanosleep(20);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    // grid update of the touched blocks, warp per block, for the next G2P
+    const int64_t kw = DO_G2P ? kstep : kstep - 1;
+    const int nl = *(volatile const int*)list_count;
+    const float y_next = plate_y_at(P, kw + 1);
+    const int lane = tid & 31;
+    const int gw = (int)((blockIdx.x * NT + tid) >> 5), nw = (int)((gridDim.x * NT) >> 5);
+    const int bps = (int)P.blocks_per_scene;
+    float4* velw = const_cast<float4*>(vel);
+    NSF_CHECK(nl >= 0 && nl <= P.blocks_per_scene * P.n_scenes);
+    for (int e = gw; e < nl; e += nw) {
+      const int key = *(volatile const int*)(list + e);
+      NSF_CHECK(key >= 0 && key < P.blocks_per_scene * P.n_scenes);
+      const int scene = key / bps;
+      const BlockCoord bc = decode_block(key, P);
+      const int64_t gb = (int64_t)scene * P.nodes_per_scene + (int64_t)(key - scene * bps) * kBlockNodes;
+      float4 a[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) a[h] = __ldcg(acc + gb + lane + 32 * h);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = lane + 32 * h;
+        const int i = bc.b[0] * 4 + (l >> 4), j = bc.b[1] * 4 + ((l >> 2) & 3), k = bc.b[2] * 4 + (l & 3);
+        velw[gb + l] = grid_node_update_t(a[h], i, j, k, P, y_next);
+        acc[gb + l] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (lane == 0) flags[key] = 0;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      counters[3] = 0;                     // segment ticket of the next kernel
+      cnt2[(int)((kw + 1) & 1)] = 0;       // the list the next kernel appends to
+      if (DO_G2P) *d_step = kstep + 1;
+    }
+  }
   if (ROT && tid == 0) {
     // every CTA has read the step counter and claimed its last ticket: the last
     // one to finish resets the ticket and the completion counter, and (G2P)
@@ -1658,7 +1724,7 @@ void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_
                                                  pb->n_nonempty, P);
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, bool ROT = false>
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int ROT = 0>
 static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
@@ -1673,7 +1739,7 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const 
       pb->n_nonempty, P, err, d_step, pb->rg);
 }
 
-template <bool ROT>
+template <int ROT>
 static void launch_g2p2g_r(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, const float4* vel, float4* acc,
                            PipelineBuffers* pb, const DevParams& P, DevErr* err, int64_t* d_step) {
   if (do_g2p && P.vm_hs) {   // von Mises with a per-particle yield stress
@@ -1711,8 +1777,9 @@ static void launch_g2p2g_r(cudaStream_t st, bool do_g2p, float* S, const int32_t
 void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, const float4* vel, float4* acc,
                   PipelineBuffers* pb,
                   const DevParams& P, DevErr* err, int64_t* d_step) {
-  if (pb->rot) launch_g2p2g_r<true>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
-  else launch_g2p2g_r<false>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
+  if (pb->gub) launch_g2p2g_r<2>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
+  else if (pb->rot) launch_g2p2g_r<1>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
+  else launch_g2p2g_r<0>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
 }
 
 #ifndef NSF_GU_CTAS_PER_SM

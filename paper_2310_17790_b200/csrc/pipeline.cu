@@ -118,7 +118,8 @@ static bool nsf_sort_enabled() {
 // (read at every load, so a test can run both in one process)
 static int rot_mode() {
   const char* e = getenv("NSF_FUSED_GU");
-  return (e && strcmp(e, "kernel") == 0) ? 0 : (e && strcmp(e, "rot") == 0) ? 1 : -1;
+  return (e && strcmp(e, "kernel") == 0) ? 0 : (e && strcmp(e, "rot") == 0) ? 1
+         : (e && strcmp(e, "barrier") == 0) ? 2 : -1;
 }
 
 static nsf_status rot_setup(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v) {
@@ -217,11 +218,15 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     if (fv && strcmp(fv, "dense2") == 0) pb->dense2 = true;
     else if (fv) pb->dense2 = false;
     else pb->dense2 = !pb->sparse && !many;
-    // grid update inside the fused kernel only where it measured faster: few
-    // segments per CTA (fewer than 2 per CTA of a 3-CTA/SM grid, e.g. C2: 37.0 ->
-    // 36.3 us); C3 (~7 segments per CTA: 103.7 vs 98.1 us) and the sparse variant
-    // (512 tile nodes per ~100 particles, C4) keep the separate pass
-    pb->rot = rot_mode() == 1 || (rot_mode() < 0 && !pb->sparse && nblk < 2 * 3 * num_sms());
+    // where the grid update runs (NSF_FUSED_GU=kernel|rot|barrier forces one): at the
+    // end of k_g2p2g after a grid-wide barrier for dense scenes with few segments per
+    // CTA (C2: 36.5 us with the separate pass or the rotating grids -> 35.5); else
+    // its own pass (C3: 92.5 us vs 97.0 barrier / 109 rotation; C4 1308 vs 1315; C1
+    // 43.8 vs 46.5)
+    const int gm = rot_mode();
+    pb->rot = gm == 1;
+    pb->gub = gm == 2 || (gm < 0 && !pb->sparse && nblk < 2 * 3 * num_sms());
+    if (cudaMemsetAsync(pb->n_nonempty + 2, 0, sizeof(int32_t), v.stream) != cudaSuccess) return NSF_ERR_CUDA;
     if (pb->rot) {
       const nsf_status rs = rot_setup(h, pb, v);
       if (rs != NSF_OK) return rs;
@@ -315,9 +320,10 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
     return cur;
   }
   if (pb->fused) {
-    if (!pb->rot) PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
+    if (!pb->rot && !pb->gub)
+      PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
     PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.ids[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
-    launches = pb->rot ? 1 : 2;
+    launches = (pb->rot || pb->gub) ? 1 : 2;
     int next = cur;
     if (variant) {
       next = enqueue_rebin(h, pb, v, cur);
@@ -420,6 +426,19 @@ int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* count
 
 int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, float* out) {
   HandleView v = view(h);
+  if (pb->fused && pb->gub) {
+    // the kernel already updated and cleared its accumulator: P2G of the current
+    // state again, into scratch grids (MLS form, as the fused kernel)
+    if (!pb->dbg_acc) {
+      pb->dbg_acc = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
+      pb->dbg_vel = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
+      if (!pb->dbg_acc || !pb->dbg_vel) return -1;
+    }
+    if (cudaMemsetAsync(pb->dbg_acc, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess) return -1;
+    launch_p2g_direct(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->dbg_acc, *v.P);
+    launch_grid_debug(v.stream, stage, v.total_nodes, pb->dbg_acc, pb->dbg_vel, out, *v.P, v.d_step);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  }
   if (pb->fused) {
     // the accumulator already holds P2G of the current state; keep it (rotation:
     // buffer step % 3, updated into a scratch grid: the other two are in use)

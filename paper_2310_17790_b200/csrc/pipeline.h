@@ -56,6 +56,7 @@ struct PipelineBuffers {
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
   int* nsf_done = nullptr;          // reduced path: CTA completion counter of the G2P kernel
   bool rot = false;                 // fused pipeline with the in-kernel grid update (RotGrid)
+  bool gub = false;                 // fused pipeline with the grid update at the end of k_g2p2g (barrier)
   float4* grid3 = nullptr;          // its third grid accumulator
   RotGrid rg;
   float4* dbg_acc = nullptr;        // reduced path: scratch grids for debug_grid
