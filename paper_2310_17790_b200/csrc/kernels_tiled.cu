@@ -1563,11 +1563,15 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       float4 a[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) a[h] = __ldcg(acc + gb + lane + 32 * h);
+      bool walls = false;
+#pragma unroll
+      for (int ax_ = 0; ax_ < 3; ++ax_)
+        walls |= (4 * bc.b[ax_] < P.bc_width) || (4 * bc.b[ax_] + 4 > P.N[ax_] - P.bc_width);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int l = lane + 32 * h;
         const int i = bc.b[0] * 4 + (l >> 4), j = bc.b[1] * 4 + ((l >> 2) & 3), k = bc.b[2] * 4 + (l & 3);
-        velw[gb + l] = grid_node_update_t(a[h], i, j, k, P, y_next);
+        velw[gb + l] = grid_node_update_rcp(a[h], i, j, k, P, y_next, walls);
         acc[gb + l] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       if (lane == 0) flags[key] = 0;
@@ -1630,11 +1634,16 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
     float4 a[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) a[h] = acc[gb + lane + 32 * h];
+    // the per-face wall tests only for blocks that reach a wall band (uniform per warp)
+    bool walls = false;
+#pragma unroll
+    for (int ax_ = 0; ax_ < 3; ++ax_)
+      walls |= (4 * bc.b[ax_] < P.bc_width) || (4 * bc.b[ax_] + 4 > P.N[ax_] - P.bc_width);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int l = lane + 32 * h;
       const int i = bc.b[0] * 4 + (l >> 4), j = bc.b[1] * 4 + ((l >> 2) & 3), k = bc.b[2] * 4 + (l & 3);
-      vel[gb + l] = grid_node_update_t(a[h], i, j, k, P, y_plate);
+      vel[gb + l] = grid_node_update_rcp(a[h], i, j, k, P, y_plate, walls);
       acc[gb + l] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (lane == 0) flags[key] = 0;
