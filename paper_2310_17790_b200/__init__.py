@@ -281,7 +281,7 @@ def nsf_mpm_rom_step(h, X_all, sample_idx, gn_iters: int, n_scenes: int, r: int,
 
 
 STAT_NAMES = ["segments", "particles", "staged", "listed", "inline", "out_of_tile", "passes", "cyc_tile",
-              "cyc_phase1", "cyc_phase2", "out_of_block", "cyc_p2_acc", "cyc_p2_help"]
+              "cyc_phase1", "cyc_phase2", "out_of_block", "cyc_p2_acc", "cyc_p2_help", "tail_ns", "kern_ns", "ctas"]
 
 
 def nsf_mpm_debug_stats(h) -> dict:

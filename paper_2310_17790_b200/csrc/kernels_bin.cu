@@ -333,4 +333,50 @@ void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, i
                                                             pb->cellcnt, pb->perm, P);
 }
 
+// Processing order of the fused kernel's segments (longest first): the
+// persistent CTAs claim segments by ticket in list order, so with the largest
+// segments first the last claims are the small (surface) blocks and the CTAs
+// finish closer together (LPT scheduling).  One CTA: counting sort of the
+// non-empty list by descending particle count (buckets of 4).  The storage
+// order and ne_of are not affected (ne_of is only used inside the re-binning).
+__global__ void __launch_bounds__(1024) k_lpt_order(int32_t* __restrict__ nonempty,
+                                                    const int32_t* __restrict__ n_nonempty,
+                                                    const int32_t* __restrict__ block_start, int32_t* __restrict__ tmp) {
+  __shared__ int hist[256];
+  const int tid = threadIdx.x;
+  const int nblk = *n_nonempty;
+  auto bucket = [&](int key) { return 255 - min((block_start[key + 1] - block_start[key]) >> 2, 255); };
+  for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int e = tid; e < nblk; e += blockDim.x) {
+    const int key = nonempty[e];
+    tmp[e] = key;
+    atomicAdd(&hist[bucket(key)], 1);
+  }
+  __syncthreads();
+  if (tid < 32) {   // exclusive scan of the 256 buckets, 8 per lane
+    int v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { v[k] = hist[8 * tid + k]; sum += v[k]; }
+    int incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (tid >= d) incl += y;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { hist[8 * tid + k] = run; run += v[k]; }
+  }
+  __syncthreads();
+  for (int e = tid; e < nblk; e += blockDim.x) {
+    const int key = tmp[e];
+    nonempty[atomicAdd(&hist[bucket(key)], 1)] = key;
+  }
+}
+
+void launch_lpt_order(cudaStream_t st, PipelineBuffers* pb) {
+  k_lpt_order<<<1, 1024, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->block_start, pb->ne_tmp);
+}
+
 }  // namespace nsf

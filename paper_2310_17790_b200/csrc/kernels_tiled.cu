@@ -27,6 +27,30 @@ namespace nsf {
 
 #if NSF_STATS
 __device__ unsigned long long g_nsf_stats[kStCount];
+__device__ unsigned long long g_tail_sum = 0, g_tail_start = ~0ull;
+__device__ unsigned int g_tail_done = 0;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// per-launch tail statistics: called by thread 0 of every CTA at its start / exit
+__device__ __forceinline__ void tail_stat_begin() { atomicMin(&g_tail_start, gtimer()); }
+__device__ __forceinline__ void tail_stat_end() {
+  const unsigned long long t = gtimer();
+  atomicAdd(&g_tail_sum, t);
+  __threadfence();
+  if (atomicAdd(&g_tail_done, 1u) == gridDim.x - 1) {
+    __threadfence();
+    const unsigned long long s = atomicAdd(&g_tail_sum, 0ull), t0 = atomicAdd(&g_tail_start, 0ull);
+    NSF_STAT_ADD(kStTailNs, (unsigned long long)gridDim.x * t - s);
+    NSF_STAT_ADD(kStKernNs, t - t0);
+    NSF_STAT_ADD(kStCtas, gridDim.x);
+    g_tail_sum = 0;
+    g_tail_start = ~0ull;
+    g_tail_done = 0;
+  }
+}
 #endif
 
 __device__ __forceinline__ void red_add_v4_t(float4* addr, float a, float b, float c, float d) {
@@ -1285,6 +1309,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
   const int my_cell = tid & 63;
   const int ox = tid >> 6;
   const int nblk = *(volatile int32_t*)&counters[0];
+#if NSF_STATS
+  if (tid == 0) tail_stat_begin();
+#endif
   int64_t kstep = 0;
   float y_plate = 0.0f;
   int* const cnt2 = list_count;   // GUB: the two count slots (+ [2] sel, [3] barrier generation)
@@ -1582,6 +1609,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       if (DO_G2P) *d_step = kstep + 1;
     }
   }
+#if NSF_STATS
+  if (tid == 0) tail_stat_end();
+#endif
   if (ROT && tid == 0) {
     // every CTA has read the step counter and claimed its last ticket: the last
     // one to finish resets the ticket and the completion counter, and (G2P)

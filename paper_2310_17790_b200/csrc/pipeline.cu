@@ -37,6 +37,7 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   pb->block_start = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * (total_blocks + 1));
   pb->cursor = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
   pb->nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
+  pb->ne_tmp = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
   if (reorder_mode() == 1) {
     pb->ne_of = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
     if (!pb->ne_of) return -1;
@@ -44,7 +45,7 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   pb->n_nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 4);
   pb->scan_status = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * pb->scan_tiles);
   pb->scan_ticket = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * 4);
-  if (!pb->counts || !pb->block_start || !pb->cursor || !pb->nonempty || !pb->n_nonempty || !pb->scan_status ||
+  if (!pb->counts || !pb->block_start || !pb->cursor || !pb->nonempty || !pb->ne_tmp || !pb->n_nonempty || !pb->scan_status ||
       !pb->scan_ticket)
     return -1;
   HandleView v = view(h);
@@ -85,7 +86,32 @@ nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
 
 // Re-binning with a physical reorder of buffer `cur` into 1 - cur (fused pipeline):
 // keys + histogram, scan (block_start, non-empty list), scatter (perm), reorder.
+static bool lpt_enabled() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_LPT");
+    f = (e && e[0] == '0') ? 0 : 1;
+  }
+  return f == 1;
+}
+
+static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur);
+
+// kernels one re-binning launches: keys + histogram, scan, reorder (flat: rank,
+// cell scan, copy; else scatter + copy), and the longest-first order (fused)
+static int rebin_launches(const PipelineBuffers* pb, int64_t n) {
+  if (n == 0) return 1;
+  return 2 + (reorder_mode() == 1 ? 3 : 2) + ((pb->fused && lpt_enabled()) ? 1 : 0);
+}
+
+// the fused kernel then processes its segments longest first (k_lpt_order)
 static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
+  const int nxt = enqueue_rebin_body(h, pb, v, cur);
+  if (pb->fused && lpt_enabled() && v.n > 0) PLAUNCH(h, "bin_lpt", launch_lpt_order(v.stream, pb));
+  return nxt;
+}
+
+static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
   const int nxt = 1 - cur;
   PLAUNCH(h, "bin_keys_hist",
           launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
@@ -327,7 +353,7 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
     int next = cur;
     if (variant) {
       next = enqueue_rebin(h, pb, v, cur);
-      launches += v.n > 0 ? 4 : 1;
+      launches += rebin_launches(pb, v.n);
     }
     pb->launches = launches;
     return next;
@@ -369,7 +395,7 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
                                        v.d_step, pb->nsf_done, v.ids[cur]));
   launches += (v.n > 0 ? 2 : 1);
   if (variant && v.n > 0) {
-    pb->launches = launches + 4;
+    pb->launches = launches + rebin_launches(pb, v.n);
     return enqueue_rebin(h, pb, v, cur);
   }
   pb->launches = launches;

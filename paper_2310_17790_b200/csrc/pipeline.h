@@ -39,6 +39,7 @@ struct PipelineBuffers {
   int32_t* perm = nullptr;          // [pitch]  sorted slot -> storage slot
   int32_t* nonempty = nullptr;      // [total_blocks] list of non-empty block ids
   int32_t* ne_of = nullptr;         // [total_blocks] list index of a non-empty block (cell-ordered re-binning)
+  int32_t* ne_tmp = nullptr;        // [total_blocks] scratch of the longest-first segment order (fused)
   int32_t* cellcnt = nullptr;       // [64 * min(total_blocks, pitch)] per-cell counts, then starts (idem)
   int32_t* n_nonempty = nullptr;    // [4]: n_nonempty, (unused), (unused), p2g block ticket (reset by scan)
   unsigned long long* scan_status = nullptr;  // [scan tiles]
@@ -125,6 +126,7 @@ void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
                       int n_scenes, int32_t* keys, int32_t* counts, const DevParams& P);
 void launch_scan(cudaStream_t st, PipelineBuffers* pb);
 void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cursor, int32_t* perm);
+void launch_lpt_order(cudaStream_t st, PipelineBuffers* pb);
 void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out);
 void launch_gather_xref(cudaStream_t st, int64_t n, const float* X, int64_t pitch, const int32_t* ids, float* S);
 void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch);

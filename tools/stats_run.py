@@ -29,3 +29,7 @@ print(f"  cycles share: tile {per['cyc_tile'] / tot:.2f} phase1 {per['cyc_phase1
       f"listed {per['listed'] / n:.3%} inline {per['inline'] / n:.3%} out-of-tile {per['out_of_tile'] / n:.3%} "
       f"out-of-block {per['out_of_block'] / n:.3%}; phase 2 of thread 0 (accumulate) "
       f"{per['cyc_p2_acc'] / per['segments']:.0f}, of the last helper {per['cyc_p2_help'] / per['segments']:.0f} cycles")
+if per.get("ctas"):
+    print(f"  kernel {per['kern_ns'] / 1e3:.1f} us per launch, CTA idle at the end {per['tail_ns'] / per['ctas'] / 1e3:.2f} us "
+          f"on average ({per['tail_ns'] / (per['ctas'] * per['kern_ns']):.1%} of the CTA-time), "
+          f"{per['ctas'] * K / max(per['segments'] * K, 1):.3f} CTAs per segment")
