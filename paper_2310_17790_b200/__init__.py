@@ -281,14 +281,13 @@ def nsf_mpm_rom_step(h, X_all, sample_idx, gn_iters: int, n_scenes: int, r: int,
 
 
 STAT_NAMES = ["segments", "particles", "staged", "listed", "inline", "out_of_tile", "passes", "cyc_tile",
-              "cyc_phase1", "cyc_phase2", "out_of_block", "cyc_p2_acc", "cyc_p2_help", "tail_ns", "kern_ns", "ctas",
-              "flow_arrive", "flow_fire", "flow_upd", "flow_far"]
+              "cyc_phase1", "cyc_phase2", "out_of_block", "cyc_p2_acc", "cyc_p2_help", "tail_ns", "kern_ns", "ctas"]
 
 
 def nsf_mpm_debug_stats(h) -> dict:
     """Work counters of the statistics build (header); raises NsfError otherwise."""
-    out = (C.c_int64 * 20)()
-    _check(h, lib().nsf_mpm_debug_stats(h, out, 20))
+    out = (C.c_int64 * 16)()
+    _check(h, lib().nsf_mpm_debug_stats(h, out, 16))
     return {k: int(out[i]) for i, k in enumerate(STAT_NAMES)}
 
 

@@ -193,10 +193,6 @@ __device__ __forceinline__ void p2g_stage_values(const float x[3], const float v
 // the next grid update
 __device__ __forceinline__ void touch_block(int* flags, int* list, int* list_count, int b, const DevParams& P) {
   NSF_CHECK(b >= 0 && b < P.blocks_per_scene * P.n_scenes);
-  if (list == nullptr) {   // dataflow grid update: the flags alone (scanned by the next kernel)
-    flags[b] = 1;
-    return;
-  }
   if (flags[b] == 0 && atomicExch(&flags[b], 1) == 0) {
     const int e = atomicAdd(list_count, 1);
     NSF_CHECK(e < P.blocks_per_scene * P.n_scenes);
@@ -918,11 +914,6 @@ struct __align__(16) FusedSmemT {
   int pop[64];
   int next;
   int nsc;                                     // entries of sc this segment
-  long long fkstep;                            // FLOW: step counter at the start
-  int fprev, fcur;                             // FLOW: the previous / current segment
-  float fy;                                    // FLOW: plate height of the update
-  int nfired;                                  // FLOW: blocks completed, updated under the next tile copy
-  int fired[64];
 };
 static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_DENSE_MIN_BLOCKS, "fused kernel: CTAs per SM");
 static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPARSE_MIN_BLOCKS,
@@ -1294,132 +1285,6 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
   }
 }
 
-// ---- dataflow grid update (GUM 3, FlowGrid in pipeline.h) ----
-#ifndef NSF_FLOW_FENCE
-#define NSF_FLOW_FENCE 1   // 1: fence.acq_rel.gpu, 0: __threadfence() (fence.sc.gpu)
-#endif
-#ifndef NSF_FLOW_PROBE
-#define NSF_FLOW_PROBE 0   // timing probes only (wrong results): 1 no arrivals, 2 no clearing,
-                           // 3 no fences, 4 the release fence only
-#endif
-__device__ __forceinline__ void flow_fence() {
-#if NSF_FLOW_PROBE == 3
-  return;
-#endif
-#if NSF_FLOW_FENCE
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#else
-  __threadfence();
-#endif
-}
-// grid update of block `key`: raw sums R -> velocities V, warp-wide (2 nodes per lane)
-__device__ __forceinline__ void flow_update_block(int key, const float4* R, float4* V, const DevParams& P,
-                                                  float y_plate, int lane) {
-  const int bps = (int)P.blocks_per_scene;
-  const BlockCoord bc = decode_block(key, P);
-  const int64_t gb = (int64_t)bc.scene * P.nodes_per_scene + (int64_t)(key - bc.scene * bps) * kBlockNodes;
-  float4 a[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) a[h] = __ldcg(R + gb + lane + 32 * h);
-  bool walls = false;
-#pragma unroll
-  for (int ax_ = 0; ax_ < 3; ++ax_)
-    walls |= (4 * bc.b[ax_] < P.bc_width) || (4 * bc.b[ax_] + 4 > P.N[ax_] - P.bc_width);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int l = lane + 32 * h;
-    const int i = bc.b[0] * 4 + (l >> 4), j = bc.b[1] * 4 + ((l >> 2) & 3), k = bc.b[2] * 4 + (l & 3);
-    V[gb + l] = grid_node_update_rcp(a[h], i, j, k, P, y_plate, walls);
-  }
-}
-
-// One warp, after a barrier that follows segment `key`'s last reduction: the
-// segment arrives at the blocks of its 27-neighbourhood; the touched blocks whose
-// count it completes are appended to the shared list `fired` (<= 27 per call), to
-// be updated by the CTA's warps (flow_update_fired); `fresh` starts a new list.  Every arrival fences its
-// CTA's reductions (release); the update side fences before reading (acquire).
-__device__ __forceinline__ void flow_arrive(int key, const FlowGrid& fg, int* fired, int* nfired,
-                                            const DevParams& P, bool fresh) {
-  const int lane = threadIdx.x & 31;
-  const BlockCoord bc = decode_block(key, P);
-  int B = -1;
-  if (lane < 27) {
-    const int n0 = bc.b[0] + lane / 9 - 1, n1 = bc.b[1] + (lane / 3) % 3 - 1, n2 = bc.b[2] + lane % 3 - 1;
-    if (n0 >= 0 && n1 >= 0 && n2 >= 0 && n0 < P.NB[0] && n1 < P.NB[1] && n2 < P.NB[2])
-      B = (int)((int64_t)bc.scene * P.blocks_per_scene + block_id(n0, n1, n2, P));
-  }
-  const int e = B >= 0 ? __ldcg(fg.expc + B) : 0;
-  flow_fence();   // release: this CTA's reductions (ordered before by the barrier) before the arrival
-  bool fire = false;
-  if (NSF_FLOW_PROBE == 4) return;
-  if (B >= 0) {
-    NSF_CHECK(e > 0 && B < fg.total_blocks);
-    fire = atomicAdd(fg.cnt + B, 1) == e - 1;
-    NSF_STAT_ADD(kStFlowArrive, 1);
-    if (fire) {
-      NSF_STAT_ADD(kStFlowFire, 1);
-      fg.cnt[B] = 0;   // every arrival of this kernel has happened
-      fire = __ldcg(fg.fout + B) != 0;   // untouched blocks: their velocities are never gathered
-    }
-  }
-  // fresh: the list was consumed under this segment's tile copy (the barrier since
-  // orders those reads before these writes)
-  const unsigned m = __ballot_sync(0xffffffffu, fire);
-  const int n0 = fresh ? 0 : *nfired;
-  if (fire) fired[n0 + __popc(m & ((1u << lane) - 1u))] = B;
-  __syncwarp();
-  if (lane == 0) *nfired = n0 + __popc(m);
-}
-
-// the listed blocks' grid update, warp per block
-__device__ __forceinline__ void flow_update_fired(const int* fired, int nfired, const FlowGrid& fg, float y_next,
-                                                  const DevParams& P) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  if (warp < nfired) flow_fence();   // acquire
-  for (int f = warp; f < nfired; f += nwarp) {
-    if (lane == 0) NSF_STAT_ADD(kStFlowUpd, 1);
-    flow_update_block(fired[f], fg.Rout, fg.Vout, P, y_next, lane);
-  }
-}
-
-// grid-wide barrier of the persistent kernel (all CTAs resident): generation ctl[3], count ctl[4]
-__device__ __forceinline__ void flow_grid_barrier(int* ctl) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile int* genp = ctl + 3;
-    const int g0 = *genp;
-    __threadfence();
-    if (atomicAdd(ctl + 4, 1) == (int)gridDim.x - 1) {
-      ctl[4] = 0;
-      __threadfence();
-      atomicAdd(ctl + 3, 1);
-    } else {
-      while (*genp == g0) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// CTA-slice walk over the touched flags of R[p]: fn(block) for each touched block, warp per 32 flags
-template <class Fn>
-__device__ __forceinline__ void flow_for_touched(const FlowGrid& fg, const int* flags, Fn fn) {
-  const int64_t TB = fg.total_blocks;
-  const int64_t per = (TB + gridDim.x - 1) / gridDim.x;
-  const int64_t b0 = (int64_t)blockIdx.x * per, b1 = min(TB, b0 + per);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  for (int64_t c = b0 + 32 * warp; c < b1; c += 32 * nwarp) {
-    const int64_t b = c + lane;
-    const bool t = b < b1 && __ldcg(flags + b) != 0;
-    unsigned m = __ballot_sync(0xffffffffu, t);
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
-      fn((int)(c + src), lane);
-    }
-  }
-}
-
 // ROT: the grid update runs inside this kernel (RotGrid, pipeline.h): `vel`,
 // `acc`, `flags`, `list` and `list_count` are ignored and taken from the
 // rotation instead; the segment's velocity tile is staged from the raw P2G sums
@@ -1436,8 +1301,8 @@ __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
-        int64_t* d_step, RotGrid rg, FlowGrid fg) {
-  constexpr bool ROT = GUM == 1, GUB = GUM == 2, FLOW = GUM == 3;
+        int64_t* d_step, RotGrid rg) {
+  constexpr bool ROT = GUM == 1, GUB = GUM == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FusedSmemT<ROWS>& sm = *reinterpret_cast<FusedSmemT<ROWS>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -1450,29 +1315,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
   int64_t kstep = 0;
   float y_plate = 0.0f;
   int* const cnt2 = list_count;   // GUB: the two count slots (+ [2] sel, [3] barrier generation)
-  if (FLOW) {
-    // vel = V[p], acc = R[p ^ 1], flags = its flags (launch parameters); the step
-    // and the plate height of the update are kept in shared memory (the dense
-    // instantiation has no registers to spare across the segment loop)
-    const int64_t ks = *(volatile const int64_t*)d_step;
-    const int64_t kw = DO_G2P ? ks : ks - 1;
-    if (tid == 0) {
-      sm.fkstep = ks;
-      sm.fprev = sm.fcur = -1;
-      sm.nfired = 0;
-      sm.fy = plate_y_at(P, kw + 1);
-    }
-    list = nullptr;
-    list_count = nullptr;
-    if (DO_G2P && *(volatile const int*)fg.far_in) {
-      // rare: the previous kernel had a far particle, so some of its blocks completed
-      // before every contribution arrived -- recompute all of Vin from Rin
-      const float y_in = plate_y_at(P, kw);
-      if (tid == 0 && blockIdx.x == 0) NSF_STAT_ADD(kStFlowFar, 1);
-      flow_for_touched(fg, fg.fin, [&](int b, int lane) { flow_update_block(b, fg.Rin, fg.Vin, P, y_in, lane); });
-      flow_grid_barrier(fg.ctl);
-    }
-  } else if (GUB) {
+  if (GUB) {
     // every CTA reads the step counter before anyone advances it (at the end);
     // the P2G written here is that of state kw + 1 and appends to slot kw & 1
     kstep = *(volatile const int64_t*)d_step;
@@ -1528,11 +1371,6 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     const int bi = sm.next;
     if (bi >= nblk) break;
     const int key = nonempty[bi];
-    const int nfired = FLOW ? sm.nfired : 0;   // (read before the tile barrier; reset after it)
-    if (FLOW && tid == 0) {
-      sm.fprev = sm.fcur;
-      sm.fcur = key;
-    }
     const BlockCoord bc = decode_block(key, P);
     const int s0 = block_start[key], s1 = block_start[key + 1];
     if (tid == 0) {
@@ -1591,7 +1429,6 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     if (DO_G2P && !ROT && s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
-    if (FLOW && nfired) flow_update_fired(sm.fired, nfired, fg, sm.fy, P);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
 #if NSF_STATS
@@ -1634,10 +1471,6 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         rank = atomicAdd(&sm.pop[cell], 1);
       } else {
         NSF_STAT_ADD(kStOutOfBlock, 1);
-        // stencil outside the segment's 27-block neighbourhood: the dataflow
-        // completion counts do not cover it (fixed up by the next kernel)
-        if (FLOW && (c[0] < -4 || c[0] > 5 || c[1] < -4 || c[1] > 5 || c[2] < -4 || c[2] > 5))
-          *fg.far_out = 1;
       }
       bool inline_scatter = false;
       if (rank < ROWS) {
@@ -1664,11 +1497,6 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       if (inline_scatter) p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
 #endif
     }
-    // the previous segment's arrivals: its reductions precede this segment's loop-top
-    // barrier; the last warp usually idles in the last phase-1 pass (512 particles
-    // on 192 threads), so the fence and the atomics' round trip cost nothing
-    if (FLOW && (tid >> 5) == NT / 32 - 1 && sm.fprev >= 0 && NSF_FLOW_PROBE != 1)
-      flow_arrive(sm.fprev, fg, sm.fired, &sm.nfired, P, true);
     __syncthreads();
 #if NSF_STATS
     if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycPhase1, t - t_mark); t_mark = t; }
@@ -1779,34 +1607,6 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       counters[3] = 0;                     // segment ticket of the next kernel
       cnt2[(int)((kw + 1) & 1)] = 0;       // the list the next kernel appends to
       if (DO_G2P) *d_step = kstep + 1;
-    }
-  }
-  if (FLOW) {
-    // the last segment's arrivals (its reductions precede the loop-exit barrier),
-    // then every completed block still listed, all warps in parallel
-    if (tid < 32 && sm.fcur >= 0 && NSF_FLOW_PROBE != 1) flow_arrive(sm.fcur, fg, sm.fired, &sm.nfired, P, false);
-    __syncthreads();
-    flow_update_fired(sm.fired, sm.nfired, fg, sm.fy, P);
-    // this CTA's slice of Rin: zeroed with its flags for kernel k + 1
-    const int64_t ks = sm.fkstep;
-    float4* Rin = fg.Rin;
-    int* fin = fg.fin;
-    if (NSF_FLOW_PROBE != 2) flow_for_touched(fg, fin, [&](int b, int lane) {
-      const int64_t gb = (int64_t)b * kBlockNodes;   // blocks of all scenes are contiguous
-      Rin[gb + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-      Rin[gb + lane + 32] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (lane == 0) fin[b] = 0;
-    });
-    if (tid == 0) {
-      __threadfence();
-      if (atomicAdd(fg.ctl + 2, 1) == (int)gridDim.x - 1) {
-        fg.ctl[2] = 0;
-        counters[3] = 0;               // segment ticket of the next kernel
-        if (DO_G2P) {
-          *fg.far_in = 0;              // consumed at the start
-          *d_step = ks + 1;
-        }
-      }
     }
   }
 #if NSF_STATS
@@ -1974,9 +1774,8 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const 
     attr = true;
   }
   k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT><<<num_sms() * MINB, NT, smem, st>>>(
-      S, ids, vel, acc, ROT == 3 ? pb->fg.fout : pb->flags, pb->touched, pb->touched + pb->total_blocks,
-      pb->block_start, pb->nonempty,
-      pb->n_nonempty, P, err, d_step, pb->rg, pb->fg);
+      S, ids, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
+      pb->n_nonempty, P, err, d_step, pb->rg);
 }
 
 template <int ROT>
@@ -2017,22 +1816,7 @@ static void launch_g2p2g_r(cudaStream_t st, bool do_g2p, float* S, const int32_t
 void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, const float4* vel, float4* acc,
                   PipelineBuffers* pb,
                   const DevParams& P, DevErr* err, int64_t* d_step) {
-  if (pb->flow) {
-    // parity p of the grids read: the current state's (host bookkeeping), or 1 for
-    // the P2G of a loaded state (written into R[0], V[0])
-    FlowGrid& fg = pb->fg;
-    const int p = do_g2p ? pb->flow_par : 1, q = p ^ 1;
-    fg.Rin = fg.R[p];
-    fg.Vin = fg.V[p];
-    fg.Rout = fg.R[q];
-    fg.Vout = fg.V[q];
-    fg.fin = fg.flags + (int64_t)p * fg.total_blocks;
-    fg.fout = fg.flags + (int64_t)q * fg.total_blocks;
-    fg.far_in = fg.ctl + p;
-    fg.far_out = fg.ctl + q;
-    launch_g2p2g_r<3>(st, do_g2p, S, ids, fg.Vin, fg.Rout, pb, P, err, d_step);
-  }
-  else if (pb->gub) launch_g2p2g_r<2>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
+  if (pb->gub) launch_g2p2g_r<2>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
   else if (pb->rot) launch_g2p2g_r<1>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
   else launch_g2p2g_r<0>(st, do_g2p, S, ids, vel, acc, pb, P, err, d_step);
 }
@@ -2070,28 +1854,5 @@ int stats_read(cudaStream_t st, int64_t* out, int n) {
   (void)st; (void)out; (void)n;
   return 0;
 #endif
-}
-}  // namespace nsf
-
-namespace nsf {
-// Expected arrivals of the dataflow grid update (FlowGrid): every non-empty
-// segment adds 1 to each block of its 27-neighbourhood (expc zeroed before).
-__global__ void k_flow_expect(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty,
-                              int* __restrict__ expc, DevParams P) {
-  const int nblk = *n_nonempty;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int e = (int)(t / 27), d = (int)(t % 27);
-  if (e >= nblk) return;
-  const BlockCoord bc = decode_block(nonempty[e], P);
-  const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
-  if (n0 >= 0 && n1 >= 0 && n2 >= 0 && n0 < P.NB[0] && n1 < P.NB[1] && n2 < P.NB[2])
-    atomicAdd(expc + (int64_t)bc.scene * P.blocks_per_scene + block_id(n0, n1, n2, P), 1);
-}
-
-void launch_flow_expect(cudaStream_t st, PipelineBuffers* pb, const DevParams& P) {
-  cudaMemsetAsync(pb->fg.expc, 0, sizeof(int) * pb->total_blocks, st);
-  const int64_t maxn = pb->total_blocks < pb->pitch ? pb->total_blocks : pb->pitch;   // bound on non-empty blocks
-  const int64_t threads = 27 * (maxn > 0 ? maxn : 1);
-  k_flow_expect<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->fg.expc, P);
 }
 }  // namespace nsf

@@ -21,15 +21,13 @@
 // phase-1 passes, and (thread 0 of each CTA, clock64) the cycles spent from the
 // loop-top barrier to the staged tile, in phase 1 and in phase 2 of the fused kernel;
 // per launch (globaltimer): the CTAs' summed idle time between their own exit and the
-// last CTA's, the first-start-to-last-exit duration, and the CTA count; dataflow grid
-// update: arrivals, completions, blocks updated, far fix-ups.
+// last CTA's, the first-start-to-last-exit duration, and the CTA count.
 #ifndef NSF_STATS
 #define NSF_STATS 0
 #endif
 enum StatIdx : int { kStSegments, kStParticles, kStStaged, kStListed, kStInline, kStOutOfTile, kStPasses,
                      kStCycTile, kStCycPhase1, kStCycPhase2, kStOutOfBlock, kStCycP2Acc, kStCycP2Help,
-                     kStTailNs, kStKernNs, kStCtas, kStFlowArrive, kStFlowFire, kStFlowUpd, kStFlowFar,
-                     kStCount = 20 };
+                     kStTailNs, kStKernNs, kStCtas, kStCount = 16 };
 #if NSF_STATS
 extern __device__ unsigned long long g_nsf_stats[kStCount];
 #define NSF_STAT_ADD(i, v) atomicAdd(&g_nsf_stats[(i)], (unsigned long long)(v))

@@ -101,14 +101,13 @@ static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView&
 // cell scan, copy; else scatter + copy), and the longest-first order (fused)
 static int rebin_launches(const PipelineBuffers* pb, int64_t n) {
   if (n == 0) return 1;
-  return 2 + (reorder_mode() == 1 ? 3 : 2) + ((pb->fused && lpt_enabled()) ? 1 : 0) + ((pb->fused && pb->flow) ? 1 : 0);
+  return 2 + (reorder_mode() == 1 ? 3 : 2) + ((pb->fused && lpt_enabled()) ? 1 : 0);
 }
 
 // the fused kernel then processes its segments longest first (k_lpt_order)
 static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
   const int nxt = enqueue_rebin_body(h, pb, v, cur);
   if (pb->fused && lpt_enabled() && v.n > 0) PLAUNCH(h, "bin_lpt", launch_lpt_order(v.stream, pb));
-  if (pb->fused && pb->flow) PLAUNCH(h, "bin_flow", launch_flow_expect(v.stream, pb, *v.P));
   return nxt;
 }
 
@@ -146,36 +145,7 @@ static bool nsf_sort_enabled() {
 static int rot_mode() {
   const char* e = getenv("NSF_FUSED_GU");
   return (e && strcmp(e, "kernel") == 0) ? 0 : (e && strcmp(e, "rot") == 0) ? 1
-         : (e && strcmp(e, "barrier") == 0) ? 2 : (e && strcmp(e, "flow") == 0) ? 3 : -1;
-}
-
-static nsf_status flow_setup(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v) {
-  FlowGrid& fg = pb->fg;
-  const int64_t TB = pb->total_blocks;
-  if (!pb->grid3) pb->grid3 = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
-  if (!pb->grid4) pb->grid4 = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
-  if (!pb->grid3 || !pb->grid4) return NSF_ERR_OUT_OF_MEMORY;
-  if (!fg.flags) {
-    fg.flags = (int*)pipeline_alloc(h, sizeof(int) * 2 * TB);
-    fg.cnt = (int*)pipeline_alloc(h, sizeof(int) * TB);
-    fg.expc = (int*)pipeline_alloc(h, sizeof(int) * TB);
-    fg.ctl = (int*)pipeline_alloc(h, sizeof(int) * 8);
-    if (!fg.flags || !fg.cnt || !fg.expc || !fg.ctl) return NSF_ERR_OUT_OF_MEMORY;
-  }
-  fg.R[0] = v.acc;
-  fg.R[1] = pb->grid3;
-  fg.V[0] = v.vel;
-  fg.V[1] = pb->grid4;
-  fg.total_blocks = TB;
-  if (cudaMemsetAsync(pb->grid3, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess ||
-      cudaMemsetAsync(v.vel, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess ||
-      cudaMemsetAsync(pb->grid4, 0, sizeof(float4) * v.total_nodes, v.stream) != cudaSuccess ||
-      cudaMemsetAsync(fg.flags, 0, sizeof(int) * 2 * TB, v.stream) != cudaSuccess ||
-      cudaMemsetAsync(fg.cnt, 0, sizeof(int) * TB, v.stream) != cudaSuccess ||
-      cudaMemsetAsync(fg.ctl, 0, sizeof(int) * 8, v.stream) != cudaSuccess)
-    return NSF_ERR_CUDA;
-  launch_flow_expect(v.stream, pb, *v.P);   // the segments of the re-binning just enqueued
-  return NSF_OK;
+         : (e && strcmp(e, "barrier") == 0) ? 2 : -1;
 }
 
 static nsf_status rot_setup(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v) {
@@ -282,16 +252,10 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
     const int gm = rot_mode();
     pb->rot = gm == 1;
     pb->gub = gm == 2 || (gm < 0 && !pb->sparse && nblk < 2 * 3 * num_sms());
-    pb->flow = gm == 3;
     if (cudaMemsetAsync(pb->n_nonempty + 2, 0, sizeof(int32_t), v.stream) != cudaSuccess) return NSF_ERR_CUDA;
     if (pb->rot) {
       const nsf_status rs = rot_setup(h, pb, v);
       if (rs != NSF_OK) return rs;
-    }
-    if (pb->flow) {
-      const nsf_status fs = flow_setup(h, pb, v);
-      if (fs != NSF_OK) return fs;
-      pb->flow_par = 0;   // the P2G below is written into R[0]
     }
     launch_g2p2g(v.stream, false, v.S[cur], v.ids[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step);   // P2G of state 0
   } else if (pb->tiled) {
@@ -342,18 +306,14 @@ static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v
   PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
 }
 
-// bit 0: the substep ends with a re-binning; bit 1 (dataflow grid update): the
-// parity of the grids the substep reads (its kernel's parameters differ)
 int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb) {
   (void)h;
-  const int rebin = ((pb->fused || pb->nsf_sorted) && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
-  return rebin | ((pb->fused && pb->flow) ? (pb->flow_par << 1) : 0);
+  return ((pb->fused || pb->nsf_sorted) && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
 }
 
 void pipeline_advance(nsf_mpm* h, PipelineBuffers* pb, int variant, int launches) {
   (void)h;
-  pb->since_rebin = (variant & 1) ? 0 : pb->since_rebin + 1;
-  if (pb->fused && pb->flow) pb->flow_par ^= 1;
+  pb->since_rebin = variant ? 0 : pb->since_rebin + 1;
   pb->launch_total += launches;
 }
 
@@ -386,12 +346,12 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
     return cur;
   }
   if (pb->fused) {
-    if (!pb->rot && !pb->gub && !pb->flow)
+    if (!pb->rot && !pb->gub)
       PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
     PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.ids[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
-    launches = (pb->rot || pb->gub || pb->flow) ? 1 : 2;
+    launches = (pb->rot || pb->gub) ? 1 : 2;
     int next = cur;
-    if (variant & 1) {
+    if (variant) {
       next = enqueue_rebin(h, pb, v, cur);
       launches += rebin_launches(pb, v.n);
     }
@@ -434,7 +394,7 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
   PLAUNCH(h, "g2p_nsf", launch_g2p_nsf(v.stream, v.n, v.S[cur], v.scene_off, v.n_scenes, v.acc, v.vel, *v.P, v.err,
                                        v.d_step, pb->nsf_done, v.ids[cur]));
   launches += (v.n > 0 ? 2 : 1);
-  if ((variant & 1) && v.n > 0) {
+  if (variant && v.n > 0) {
     pb->launches = launches + rebin_launches(pb, v.n);
     return enqueue_rebin(h, pb, v, cur);
   }
@@ -508,15 +468,7 @@ int pipeline_debug_grid(nsf_mpm* h, PipelineBuffers* pb, int cur, int stage, flo
   if (pb->fused) {
     // the accumulator already holds P2G of the current state; keep it (rotation:
     // buffer step % 3, updated into a scratch grid: the other two are in use)
-    if (pb->flow) {
-      // R[flow_par] holds P2G of the current state (cleared by the next kernel); update into a scratch grid
-      if (!pb->dbg_vel) {
-        pb->dbg_vel = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
-        if (!pb->dbg_vel) return -1;
-      }
-      launch_grid_debug(v.stream, stage, v.total_nodes, pb->fg.R[pb->flow_par], pb->dbg_vel, out, *v.P,
-                        v.d_step);
-    } else if (pb->rot) {
+    if (pb->rot) {
       if (!pb->dbg_vel) {
         pb->dbg_vel = (float4*)pipeline_alloc(h, sizeof(float4) * v.total_nodes);
         if (!pb->dbg_vel) return -1;

@@ -29,40 +29,6 @@ struct RotGrid {
   int64_t total_blocks = 0;
 };
 
-// Fused pipeline with the grid update done by dataflow inside the G2P2G kernel
-// (NSF_FUSED_GU=flow): two raw P2G accumulators R and two velocity grids V by
-// step parity.  Kernel k (k = substeps done; -1 for the P2G of a loaded state)
-// reads the velocities V[k & 1], reduces the next P2G into R[(k + 1) & 1] and,
-// per grid block B, counts the arrivals of the segments whose 27-block
-// neighbourhood holds B: the CTA that completes the count (expc[B], set at every
-// re-binning) updates B into V[(k + 1) & 1], so the update runs inside
-// the kernel, mostly in the CTAs' tails.  A particle whose stencil leaves its
-// segment's neighbourhood ("far", in practice never after 32 substeps) raises
-// ctl[(k + 1) & 1]: the next kernel then recomputes every touched block of that
-// grid before its first segment (grid-wide barrier).  R[k & 1] (read by that
-// fix-up only) is cleared by kernel k from its touched flags.
-// The parity is the host's (PipelineBuffers::flow_par, part of the graph variant),
-// so every grid pointer reaches the kernel as a launch parameter.
-struct FlowGrid {
-  float4* R[2] = {nullptr, nullptr};
-  float4* V[2] = {nullptr, nullptr};
-  int* flags = nullptr;             // [2][total_blocks] touched blocks of R[0], R[1] (plain stores)
-  int* cnt = nullptr;               // [total_blocks] arrivals this kernel (reset by the completing CTA)
-  int* expc = nullptr;              // [total_blocks] expected arrivals (non-empty segments in the neighbourhood)
-  int* ctl = nullptr;               // [8]: [0], [1] far flags of R[0], R[1]; [2] finished CTAs; [3] barrier
-                                    //      generation; [4] barrier arrivals
-  int64_t total_blocks = 0;
-  // resolved per launch: p = the parity of the grids read
-  float4* Rin = nullptr;            // R[p]      raw sums of the current state (fix-up, then cleared)
-  float4* Vin = nullptr;            // V[p]      velocities read by G2P
-  float4* Rout = nullptr;           // R[p ^ 1]  P2G reduced here
-  float4* Vout = nullptr;           // V[p ^ 1]  updated by the completing CTAs
-  int* fin = nullptr;               // flags of Rin
-  int* fout = nullptr;              // flags of Rout
-  int* far_in = nullptr;            // ctl + p
-  int* far_out = nullptr;           // ctl + (p ^ 1)
-};
-
 struct PipelineBuffers {
   // binning: block key per particle slot, per-block counts,
   // start offsets (exclusive scan), scatter cursors, permutation, active list
@@ -94,10 +60,6 @@ struct PipelineBuffers {
   bool gub = false;                 // fused pipeline with the grid update at the end of k_g2p2g (barrier)
   float4* grid3 = nullptr;          // its third grid accumulator
   RotGrid rg;
-  bool flow = false;                // fused pipeline with the dataflow grid update (FlowGrid)
-  int flow_par = 0;                 // flow: parity of the R grid holding the current state's P2G
-  float4* grid4 = nullptr;          // flow: R[1] = grid3, V[1] = grid4
-  FlowGrid fg;
   float4* dbg_acc = nullptr;        // reduced path: scratch grids for debug_grid
   unsigned long long* fx = nullptr; // deterministic mode: fixed-point P2G accumulator [total_nodes][4]
   float4* dbg_vel = nullptr;
@@ -165,7 +127,6 @@ void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
 void launch_scan(cudaStream_t st, PipelineBuffers* pb);
 void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cursor, int32_t* perm);
 void launch_lpt_order(cudaStream_t st, PipelineBuffers* pb);
-void launch_flow_expect(cudaStream_t st, PipelineBuffers* pb, const DevParams& P);
 void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out);
 void launch_gather_xref(cudaStream_t st, int64_t n, const float* X, int64_t pitch, const int32_t* ids, float* S);
 void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch);

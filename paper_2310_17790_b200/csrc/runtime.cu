@@ -87,9 +87,9 @@ struct nsf_mpm {
   size_t staging_bytes = 0;
   // graphs: one captured substep per source buffer (the pipeline may ping-pong
   // particle buffers, so the substep starting from buffer k is graph[k])
-  cudaGraphExec_t graph[2][4] = {};   // [source buffer][variant] (pipeline_variant: re-binning, grid parity)
-  int graph_next[2][4] = {{0, 0, 0, 0}, {1, 1, 1, 1}};
-  int graph_launches[2][4] = {};       // kernels in each captured graph
+  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [source buffer][variant]
+  int graph_next[2][2] = {{0, 0}, {1, 1}};
+  int graph_launches[2][2] = {{0, 0}, {0, 0}};   // kernels in each captured graph
   // profiling
   bool profiling = false;
   struct Pending { std::string name; cudaEvent_t a, b; };
@@ -198,7 +198,7 @@ nsf_status to_device(nsf_mpm* h, const void* src, size_t bytes, int on_device, v
 
 void invalidate_graph(nsf_mpm* h) {
   for (int k = 0; k < 2; ++k)
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 2; ++v) {
       if (h->graph[k][v]) cudaGraphExecDestroy(h->graph[k][v]);
       h->graph[k][v] = nullptr;
     }

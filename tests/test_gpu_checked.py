@@ -41,7 +41,7 @@ def test_checks_trap(lib_checked):
     assert "NSF_CHECK failed" in r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("gu", ["rot", "kernel", "barrier", "flow"])
+@pytest.mark.parametrize("gu", ["rot", "kernel", "barrier"])
 @pytest.mark.parametrize("scene", ["c1_spin", "dense_cluster", "sparse"])
 def test_full_order_checked(lib_checked, scene, gu):
     r = _run([os.path.join("tools", "checked_run.py"), scene], {"NSF_FUSED_GU": gu})

@@ -59,7 +59,7 @@ def edge_scene(model, seed):
 MODELS = {"FC": scenes.FIXED_COROTATED, "DP": scenes.DRUCKER_PRAGER, "VM": scenes.VON_MISES}
 
 
-@pytest.mark.parametrize("gu", ["rot", "kernel", "barrier", "flow"])
+@pytest.mark.parametrize("gu", ["rot", "kernel", "barrier"])
 @pytest.mark.parametrize("model", list(MODELS))
 def test_inverted_and_degenerate_F(nsf, model, gu, monkeypatch):
     monkeypatch.setenv("NSF_FUSED_GU", gu)

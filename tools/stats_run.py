@@ -33,6 +33,3 @@ if per.get("ctas"):
     print(f"  kernel {per['kern_ns'] / 1e3:.1f} us per launch, CTA idle at the end {per['tail_ns'] / per['ctas'] / 1e3:.2f} us "
           f"on average ({per['tail_ns'] / (per['ctas'] * per['kern_ns']):.1%} of the CTA-time), "
           f"{per['ctas'] * K / max(per['segments'] * K, 1):.3f} CTAs per segment")
-if per.get("flow_arrive"):
-    print(f"  flow: arrivals {per['flow_arrive']:.0f} completions {per['flow_fire']:.0f} blocks updated {per['flow_upd']:.0f} "
-          f"far fix-ups {per['flow_far']:.2f} per substep")
