@@ -200,9 +200,36 @@ __device__ __forceinline__ void touch_block(int* flags, int* list, int* list_cou
   }
 }
 
+// Where a scattered particle's grid blocks are marked for the grid update.  With
+// the halo list (HALO, separate grid-update pass): every block in the 27-block
+// neighbourhood of a non-empty segment is updated anyway (k_halo, at each
+// re-binning), so only a block outside it -- reached by a particle that drifted
+// more than 4 cells from its segment -- goes through the flags and the touched list.
+struct TouchCtx {
+  int* flags;
+  int* list;
+  int* list_count;
+  const int* hmark;   // HALO: halo membership per block
+  int seg[3];         // HALO: the segment's block
+  int64_t scene_block0;
+};
+
+template <bool HALO>
+__device__ __forceinline__ void touch(const TouchCtx& t, int b0, int b1, int b2, const DevParams& P) {
+  if (HALO) {
+    if (abs(b0 - t.seg[0]) <= 1 && abs(b1 - t.seg[1]) <= 1 && abs(b2 - t.seg[2]) <= 1) return;
+    const int B = (int)(t.scene_block0 + block_id(b0, b1, b2, P));
+    if (t.hmark[B]) return;
+    touch_block(t.flags, t.list, t.list_count, B, P);
+    return;
+  }
+  touch_block(t.flags, t.list, t.list_count, (int)(t.scene_block0 + block_id(b0, b1, b2, P)), P);
+}
+
+template <bool HALO>
 __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float v[3], const float Cm[9],
-                                                   const float T[6], float4* gbase, int* flags, int* list,
-                                                   int* list_count, int64_t scene_block0, const DevParams& P) {
+                                                   const float T[6], float4* gbase, const TouchCtx& tc,
+                                                   const DevParams& P) {
   const float m = P.mass;
   Axis ax[3];
 #pragma unroll
@@ -236,7 +263,7 @@ __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int b0 = (ax[0].base + 2 * a) >> 2, b1 = (ax[1].base + 2 * b) >> 2, b2 = (ax[2].base + 2 * c) >> 2;
-        touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
+        touch<HALO>(tc, b0, b1, b2, P);
       }
 }
 
@@ -245,9 +272,10 @@ __device__ __forceinline__ void p2g_scatter_direct(const float x[3], const float
 // lanes of the warp each scatter some of its 27 nodes (and touch its 8 corner
 // blocks).  A few direct particles per warp then cost ~21 shuffles + one node
 // each instead of serialising 27 reductions while the other lanes idle.
+template <bool HALO>
 __device__ __forceinline__ void p2g_scatter_warp(bool direct, const float x[3], const float v[3], const float Cm[9],
-                                                 const float T[6], float4* gbase, int* flags, int* list,
-                                                 int* list_count, int64_t scene_block0, const DevParams& P) {
+                                                 const float T[6], float4* gbase, const TouchCtx& tc,
+                                                 const DevParams& P) {
   const unsigned act = __activemask();
   unsigned pend = __ballot_sync(act, direct);
   if (!pend) return;
@@ -292,7 +320,7 @@ __device__ __forceinline__ void p2g_scatter_warp(bool direct, const float x[3], 
     for (int k = r; k < 8; k += nact) {
       const int b0 = (ax[0].base + 2 * (k >> 2)) >> 2, b1 = (ax[1].base + 2 * ((k >> 1) & 1)) >> 2,
                 b2 = (ax[2].base + 2 * (k & 1)) >> 2;
-      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
+      touch<HALO>(tc, b0, b1, b2, P);
     }
   }
 }
@@ -1259,8 +1287,9 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 // Phase-2 scatter of the listed particles: work item i = (entry i / 35; its
 // stencil node i % 35 < 27, else one of its 8 corner blocks to mark touched).
 // Node (a, b, c) gets m W, W (u0 + a q0 + b q1 + c q2) as in p2g_accumulate_rows.
-__device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0, int stride, float4* gacc, int* flags,
-                                               int* list, int* list_count, int64_t scene_block0, const DevParams& P) {
+template <bool HALO>
+__device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0, int stride, float4* gacc,
+                                               const TouchCtx& tc, const DevParams& P) {
   for (int i = i0; i < nsc * 35; i += stride) {
     const int e = i / 35, q = i - 35 * e;
     const float* s = reinterpret_cast<const float*>(sc + e * kRowF4);
@@ -1280,7 +1309,7 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
     } else {
       const int k = q - 27;
       const int b0 = (bx + 2 * (k >> 2)) >> 2, b1 = (by + 2 * ((k >> 1) & 1)) >> 2, b2 = (bz + 2 * (k & 1)) >> 2;
-      touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
+      touch<HALO>(tc, b0, b1, b2, P);
     }
   }
 }
@@ -1301,8 +1330,9 @@ __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
-        int64_t* d_step, RotGrid rg) {
+        int64_t* d_step, RotGrid rg, const int* __restrict__ hmark) {
   constexpr bool ROT = GUM == 1, GUB = GUM == 2;
+  constexpr bool HALO = GUM == 0;   // the grid-update pass visits the halo list (k_halo) + far-touched blocks
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FusedSmemT<ROWS>& sm = *reinterpret_cast<FusedSmemT<ROWS>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -1379,6 +1409,15 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       NSF_STAT_ADD(kStPasses, (s1 - s0 + NT - 1) / NT);
     }
     const int64_t scene_block0 = (int64_t)bc.scene * P.blocks_per_scene;
+    TouchCtx tc;
+    tc.flags = flags;
+    tc.list = list;
+    tc.list_count = list_count;
+    tc.hmark = hmark;
+    tc.seg[0] = bc.b[0];
+    tc.seg[1] = bc.b[1];
+    tc.seg[2] = bc.b[2];
+    tc.scene_block0 = scene_block0;
     float4* gacc = acc + (int64_t)bc.scene * P.nodes_per_scene;
     const float4* gvel = vel + (int64_t)bc.scene * P.nodes_per_scene;
     if (tid < 64) sm.pop[tid] = 0;
@@ -1492,9 +1531,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         }
       }
 #if NSF_WARP_SCATTER
-      p2g_scatter_warp(inline_scatter, xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+      p2g_scatter_warp<HALO>(inline_scatter, xn, vn, Cn, tau, gacc, tc, P);
 #else
-      if (inline_scatter) p2g_scatter_direct(xn, vn, Cn, tau, gacc, flags, list, list_count, scene_block0, P);
+      if (inline_scatter) p2g_scatter_direct<HALO>(xn, vn, Cn, tau, gacc, tc, P);
 #endif
     }
     __syncthreads();
@@ -1512,7 +1551,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     // the grid blocks the segment's cell sums reduce into (its block and the +1
     // neighbours) are flagged by the last 8 helper threads, whose flag round trips
     // then overlap the accumulation instead of trailing it
-    if (NT > 192 && tid >= NT - 8) {
+    if (!HALO && NT > 192 && tid >= NT - 8) {
       const int t8 = tid - (NT - 8);
       const int b0 = bc.b[0] + (t8 >> 2), b1 = bc.b[1] + ((t8 >> 1) & 1), b2 = bc.b[2] + (t8 & 1);
       if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])
@@ -1521,10 +1560,10 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     {
       const int nsc = min(sm.nsc, kScatterCap);
       if (NT > 192) {
-        if (ox >= 3) scatter_listed(sm.sc, nsc, tid - 192, NT - 192, gacc, flags, list, list_count, scene_block0, P);
+        if (ox >= 3) scatter_listed<HALO>(sm.sc, nsc, tid - 192, NT - 192, gacc, tc, P);
         else p2g_accumulate_rows<ROWS>(sm.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
       } else {
-        scatter_listed(sm.sc, nsc, tid, NT, gacc, flags, list, list_count, scene_block0, P);
+        scatter_listed<HALO>(sm.sc, nsc, tid, NT, gacc, tc, P);
         p2g_accumulate_rows<ROWS>(sm.slot, my_cell, ox, min(sm.pop[my_cell], ROWS), accm, accp);
       }
     }
@@ -1548,7 +1587,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     if (tid == 0) NSF_STAT_ADD(kStCycP2Acc, clock64() - t_p2);
     if (tid == NT - 1) NSF_STAT_ADD(kStCycP2Help, clock64() - t_p2);
 #endif
-    if (NT <= 192 && tid < 8) {   // (no helper threads)
+    if (!HALO && NT <= 192 && tid < 8) {   // (no helper threads)
       const int b0 = bc.b[0] + (tid >> 2), b1 = bc.b[1] + ((tid >> 1) & 1), b2 = bc.b[2] + (tid & 1);
       if (b0 < P.NB[0] && b1 < P.NB[1] && b2 < P.NB[2])
         touch_block(flags, list, list_count, (int)(scene_block0 + block_id(b0, b1, b2, P)), P);
@@ -1632,32 +1671,41 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
 // list count alternates between two slots by step parity: this kernel reads slot
 // n & 1, empties slot (n + 1) & 1 and publishes it (sel) for the next G2P2G to
 // append to -- no completion counter or fence is needed.
+//
+// The blocks visited are the halo list (`halo`, `nhalo` entries: every block in
+// the 27-block neighbourhood of a non-empty segment, k_halo) followed by the
+// touched list (blocks outside the halo, flagged by far particles).  Halo blocks
+// nothing reached hold m = 0 and get v = 0 (never gathered).
 __global__ void __launch_bounds__(128)
 k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* __restrict__ cnt2,
+                   const int* __restrict__ halo, const int* __restrict__ nhalo,
                    float4* __restrict__ acc, float4* __restrict__ vel, DevParams P,
                    const int64_t* __restrict__ d_step, int32_t* __restrict__ counters) {
-  // the step, both count slots and this warp's first list entry are loaded
-  // together (the entry speculatively: the list has room for every block)
+  // the step, both count slots and this warp's first halo entry are loaded
+  // together (the entry speculatively: the halo list has room for every block)
   const int lane = threadIdx.x & 31;
   const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
   const int64_t n = *d_step;
   const int c0 = cnt2[0], c1 = cnt2[1];
-  int key_next = warp < P.blocks_per_scene * P.n_scenes ? list[warp] : 0;
+  const int nh = *nhalo;
+  int key_next = warp < P.blocks_per_scene * P.n_scenes ? halo[warp] : 0;
   const int s = (int)(n & 1);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     counters[3] = 0;    // segment ticket of the next k_g2p2g
     cnt2[s ^ 1] = 0;    // the list the next k_g2p2g appends to
     cnt2[2] = s ^ 1;
   }
-  const int nl = s ? c1 : c0;
+  const int nl = nh + (s ? c1 : c0);
   const float y_plate = plate_y_at(P, n);
   const int bps = (int)P.blocks_per_scene;
-  NSF_CHECK(nl >= 0 && nl <= P.blocks_per_scene * P.n_scenes);
+  NSF_CHECK(nl >= 0 && nl <= 2 * P.blocks_per_scene * P.n_scenes);
+  if (warp >= nh && warp < nl) key_next = list[warp - nh];
   for (int e = warp; e < nl; e += nwarps) {
     const int key = key_next;
     NSF_CHECK(key >= 0 && key < P.blocks_per_scene * P.n_scenes);
-    if (e + nwarps < nl) key_next = list[e + nwarps];
+    const int en = e + nwarps;
+    if (en < nl) key_next = en < nh ? halo[en] : list[en - nh];
     const int scene = key / bps;
     const BlockCoord bc = decode_block(key, P);
     const int64_t gb = (int64_t)scene * P.nodes_per_scene + (int64_t)(key - scene * bps) * kBlockNodes;
@@ -1676,8 +1724,45 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
       vel[gb + l] = grid_node_update_rcp(a[h], i, j, k, P, y_plate, walls);
       acc[gb + l] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (lane == 0) flags[key] = 0;
+    if (lane == 0 && e >= nh) flags[key] = 0;
   }
+}
+
+// Halo of the segments (GUM 0), at every re-binning: block B is in it when a
+// non-empty block lies in its 27-neighbourhood (the blocks a segment's P2G can
+// reach while its particles drift <= 4 cells); hmark[B] = membership, and the
+// members are listed for the grid update.  Thread per block (nhalo zeroed before).
+__global__ void __launch_bounds__(256)
+k_halo(const int32_t* __restrict__ block_start, int* __restrict__ hmark, int* __restrict__ halo,
+       int* __restrict__ nhalo, DevParams P) {
+  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t TB = P.blocks_per_scene * P.n_scenes;
+  bool in = false;
+  if (B < TB) {
+    const int bps = (int)P.blocks_per_scene;
+    const int scene = (int)(B / bps);
+    const BlockCoord bc = decode_block((int)B, P);
+    for (int d = 0; d < 27 && !in; ++d) {
+      const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
+      if (n0 < 0 || n1 < 0 || n2 < 0 || n0 >= P.NB[0] || n1 >= P.NB[1] || n2 >= P.NB[2]) continue;
+      const int64_t k = (int64_t)scene * bps + block_id(n0, n1, n2, P);
+      in = block_start[k + 1] > block_start[k];
+    }
+    hmark[B] = in ? 1 : 0;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, in);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(nhalo, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (in) halo[base + __popc(m & ((1u << lane) - 1u))] = (int)B;
+}
+
+void launch_halo(cudaStream_t st, PipelineBuffers* pb, const DevParams& P) {
+  cudaMemsetAsync(pb->nhalo, 0, sizeof(int), st);
+  const int64_t TB = pb->total_blocks;
+  k_halo<<<(unsigned)((TB + 255) / 256), 256, 0, st>>>(pb->block_start, pb->hmark, pb->halo, pb->nhalo, P);
 }
 
 // physical reorder into binned order: out[j] = in[perm[j]] (all 30 fields + id)
@@ -1775,7 +1860,7 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const 
   }
   k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT><<<num_sms() * MINB, NT, smem, st>>>(
       S, ids, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
-      pb->n_nonempty, P, err, d_step, pb->rg);
+      pb->n_nonempty, P, err, d_step, pb->rg, pb->hmark);
 }
 
 template <int ROT>
@@ -1827,8 +1912,8 @@ void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, co
 void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
                               const int64_t* d_step) {
   const int grid = num_sms() * NSF_GU_CTAS_PER_SM;
-  k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks, acc, vel, P,
-                                           d_step, pb->n_nonempty);
+  k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->halo,
+                                           pb->nhalo, acc, vel, P, d_step, pb->n_nonempty);
 }
 
 void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,

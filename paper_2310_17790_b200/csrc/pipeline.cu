@@ -56,7 +56,10 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   if (cudaMemsetAsync(pb->scan_ticket, 0, sizeof(unsigned long long) * 4, v.stream) != cudaSuccess) return -1;
   pb->flags = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
   pb->touched = (int*)pipeline_alloc(h, sizeof(int) * (total_blocks + 4));
-  if (!pb->flags || !pb->touched) return -1;
+  pb->hmark = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
+  pb->halo = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
+  pb->nhalo = (int*)pipeline_alloc(h, sizeof(int) * 4);
+  if (!pb->flags || !pb->touched || !pb->hmark || !pb->halo || !pb->nhalo) return -1;
   if (cudaMemsetAsync(pb->flags, 0, sizeof(int) * total_blocks, v.stream) != cudaSuccess) return -1;
   if (cudaMemsetAsync(pb->touched, 0, sizeof(int) * (total_blocks + 4), v.stream) != cudaSuccess) return -1;
   p2g_tables_init(v.stream);
@@ -101,13 +104,14 @@ static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView&
 // cell scan, copy; else scatter + copy), and the longest-first order (fused)
 static int rebin_launches(const PipelineBuffers* pb, int64_t n) {
   if (n == 0) return 1;
-  return 2 + (reorder_mode() == 1 ? 3 : 2) + ((pb->fused && lpt_enabled()) ? 1 : 0);
+  return 2 + (reorder_mode() == 1 ? 3 : 2) + ((pb->fused && lpt_enabled()) ? 1 : 0) + (pb->fused ? 1 : 0);
 }
 
 // the fused kernel then processes its segments longest first (k_lpt_order)
 static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
   const int nxt = enqueue_rebin_body(h, pb, v, cur);
   if (pb->fused && lpt_enabled() && v.n > 0) PLAUNCH(h, "bin_lpt", launch_lpt_order(v.stream, pb));
+  if (pb->fused) PLAUNCH(h, "bin_halo", launch_halo(v.stream, pb, *v.P));
   return nxt;
 }
 

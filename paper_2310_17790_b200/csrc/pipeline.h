@@ -55,6 +55,9 @@ struct PipelineBuffers {
   bool nsf_sorted = false;          // reduced path: points kept in block order (periodic re-binning)              // fused kernel variant for few particles per block (chosen at load)
   int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
+  int* hmark = nullptr;             // [total_blocks] halo membership (fused, separate grid update; k_halo)
+  int* halo = nullptr;              // [total_blocks] halo list
+  int* nhalo = nullptr;             // [1] its length
   int* nsf_done = nullptr;          // reduced path: CTA completion counter of the G2P kernel
   bool rot = false;                 // fused pipeline with the in-kernel grid update (RotGrid)
   bool gub = false;                 // fused pipeline with the grid update at the end of k_g2p2g (barrier)
@@ -127,6 +130,7 @@ void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
 void launch_scan(cudaStream_t st, PipelineBuffers* pb);
 void launch_scatter(cudaStream_t st, int64_t n, const int32_t* keys, int32_t* cursor, int32_t* perm);
 void launch_lpt_order(cudaStream_t st, PipelineBuffers* pb);
+void launch_halo(cudaStream_t st, PipelineBuffers* pb, const DevParams& P);
 void launch_gather_ids(cudaStream_t st, int64_t n, const int32_t* perm, const int32_t* ids, int32_t* out);
 void launch_gather_xref(cudaStream_t st, int64_t n, const float* X, int64_t pitch, const int32_t* ids, float* S);
 void launch_aos_to_planes(cudaStream_t st, int64_t n, const float* aos, int ncomp, float* planes, int64_t pitch);
