@@ -544,7 +544,7 @@ def spawn(n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=200)   # C3: substeps 261-461 of its 500
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C3", choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -19,6 +19,7 @@
 //              (sort-on-write), with its next block key and the histogram for
 //              the next binning.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <cstdint>
 #include "mpm_math.cuh"
 #include "pipeline.h"
@@ -52,6 +53,12 @@ __device__ __forceinline__ void tail_stat_end() {
   }
 }
 #endif
+
+// Programmatic dependent launch (the grid update and the fused kernel are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization): a dependent grid's CTAs
+// are scheduled before its predecessor completes and wait here for its results.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ void red_add_v4_t(float4* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -1338,6 +1345,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
   const int tid = threadIdx.x;
   const int my_cell = tid & 63;
   const int ox = tid >> 6;
+  pdl_wait();   // the grid update (or the re-binning) before it
   const int nblk = *(volatile int32_t*)&counters[0];
 #if NSF_STATS
   if (tid == 0) tail_stat_begin();
@@ -1686,6 +1694,8 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
   const int lane = threadIdx.x & 31;
   const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  pdl_launch_dependents();   // the fused kernel's CTAs may be scheduled now (they wait for this grid)
+  pdl_wait();                // the previous substep's kernels
   const int64_t n = *d_step;
   const int c0 = cnt2[0], c1 = cnt2[1];
   const int nh = *nhalo;
@@ -1730,39 +1740,29 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
 
 // Halo of the segments (GUM 0), at every re-binning: block B is in it when a
 // non-empty block lies in its 27-neighbourhood (the blocks a segment's P2G can
-// reach while its particles drift <= 4 cells); hmark[B] = membership, and the
-// members are listed for the grid update.  Thread per block (nhalo zeroed before).
+// reach while its particles drift <= 4 cells).  Thread per (segment, neighbour):
+// the first to mark B (hmark zeroed before) lists it for the grid update.
 __global__ void __launch_bounds__(256)
-k_halo(const int32_t* __restrict__ block_start, int* __restrict__ hmark, int* __restrict__ halo,
-       int* __restrict__ nhalo, DevParams P) {
-  const int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t TB = P.blocks_per_scene * P.n_scenes;
-  bool in = false;
-  if (B < TB) {
-    const int bps = (int)P.blocks_per_scene;
-    const int scene = (int)(B / bps);
-    const BlockCoord bc = decode_block((int)B, P);
-    for (int d = 0; d < 27 && !in; ++d) {
-      const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
-      if (n0 < 0 || n1 < 0 || n2 < 0 || n0 >= P.NB[0] || n1 >= P.NB[1] || n2 >= P.NB[2]) continue;
-      const int64_t k = (int64_t)scene * bps + block_id(n0, n1, n2, P);
-      in = block_start[k + 1] > block_start[k];
-    }
-    hmark[B] = in ? 1 : 0;
-  }
-  const unsigned m = __ballot_sync(0xffffffffu, in);
-  if (!m) return;
-  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(nhalo, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (in) halo[base + __popc(m & ((1u << lane) - 1u))] = (int)B;
+k_halo(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty, int* __restrict__ hmark,
+       int* __restrict__ halo, int* __restrict__ nhalo, DevParams P) {
+  const int nblk = *n_nonempty;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int e = (int)(t / 27), d = (int)(t % 27);
+  if (e >= nblk) return;
+  const BlockCoord bc = decode_block(nonempty[e], P);
+  const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
+  if (n0 < 0 || n1 < 0 || n2 < 0 || n0 >= P.NB[0] || n1 >= P.NB[1] || n2 >= P.NB[2]) return;
+  const int B = (int)((int64_t)bc.scene * P.blocks_per_scene + block_id(n0, n1, n2, P));
+  if (atomicExch(hmark + B, 1) == 0) halo[atomicAdd(nhalo, 1)] = B;
 }
 
 void launch_halo(cudaStream_t st, PipelineBuffers* pb, const DevParams& P) {
   cudaMemsetAsync(pb->nhalo, 0, sizeof(int), st);
-  const int64_t TB = pb->total_blocks;
-  k_halo<<<(unsigned)((TB + 255) / 256), 256, 0, st>>>(pb->block_start, pb->hmark, pb->halo, pb->nhalo, P);
+  cudaMemsetAsync(pb->hmark, 0, sizeof(int) * pb->total_blocks, st);
+  const int64_t maxn = pb->total_blocks < pb->pitch ? pb->total_blocks : pb->pitch;   // bound on non-empty blocks
+  const int64_t threads = 27 * (maxn > 0 ? maxn : 1);
+  k_halo<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->hmark, pb->halo,
+                                                          pb->nhalo, P);
 }
 
 // physical reorder into binned order: out[j] = in[perm[j]] (all 30 fields + id)
@@ -1848,6 +1848,16 @@ void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_
                                                  pb->n_nonempty, P);
 }
 
+// NSF_PDL=0 launches without programmatic dependent launch (A/B)
+static bool pdl_enabled() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_PDL");
+    f = (e && e[0] == '0') ? 0 : 1;
+  }
+  return f == 1;
+}
+
 template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int ROT = 0>
 static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
@@ -1858,9 +1868,19 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const 
                          (int)smem);
     attr = true;
   }
-  k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT><<<num_sms() * MINB, NT, smem, st>>>(
-      S, ids, vel, acc, pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->block_start, pb->nonempty,
-      pb->n_nonempty, P, err, d_step, pb->rg, pb->hmark);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(num_sms() * MINB);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT>, S, ids, vel, acc, pb->flags, pb->touched,
+                     pb->touched + pb->total_blocks, pb->block_start, pb->nonempty, pb->n_nonempty, P, err, d_step,
+                     pb->rg, pb->hmark);
 }
 
 template <int ROT>
@@ -1912,8 +1932,17 @@ void launch_g2p2g(cudaStream_t st, bool do_g2p, float* S, const int32_t* ids, co
 void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc, float4* vel, const DevParams& P,
                               const int64_t* d_step) {
   const int grid = num_sms() * NSF_GU_CTAS_PER_SM;
-  k_grid_update_list<<<grid, 128, 0, st>>>(pb->flags, pb->touched, pb->touched + pb->total_blocks, pb->halo,
-                                           pb->nhalo, acc, vel, P, d_step, pb->n_nonempty);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_grid_update_list, pb->flags, (const int*)pb->touched, pb->touched + pb->total_blocks,
+                     (const int*)pb->halo, (const int*)pb->nhalo, acc, vel, P, d_step, pb->n_nonempty);
 }
 
 void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,

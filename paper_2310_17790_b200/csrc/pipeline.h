@@ -52,6 +52,7 @@ struct PipelineBuffers {
   bool sparse = false;
   bool dense2 = false;      // dense variant at 2 CTAs per SM (128 registers)
   bool dense3s = false;     // dense variant at 3 CTAs per SM of 192 threads (96 registers): many segments
+  bool mode_ready = false;  // fused: variant and grid-update mode chosen (pipeline_on_load)
   bool nsf_sorted = false;          // reduced path: points kept in block order (periodic re-binning)              // fused kernel variant for few particles per block (chosen at load)
   int* flags = nullptr;             // [total_blocks] grid blocks touched by P2G (fused pipeline)
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
