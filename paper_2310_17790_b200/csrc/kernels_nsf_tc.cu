@@ -23,7 +23,6 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
-#include <cstdlib>
 #include "kernels.h"
 #include "params.cuh"
 #include "point_ops.cuh"
@@ -214,92 +213,6 @@ __device__ __forceinline__ void store_act32(uint32_t tile, int row, int c0, cons
 
 using namespace tc;
 
-#ifndef NSF_MLP_PAIRED
-#define NSF_MLP_PAIRED 1   // epilogue math two columns at a time (FADD2 / FMUL2)
-#endif
-namespace ws {
-constexpr int kS = 2;                          // streams per CTA
-constexpr int kEpi = 128 * kS;                 // epilogue threads
-constexpr int kThreads = kEpi + 32 * kS;       // + one MMA warp per stream
-struct __align__(1024) Smem {
-  uint8_t wB[kMaxHiddenMMA][kTileBytes];
-  uint8_t wOut[kOutBBytes];
-  uint8_t a[kS][kTileBytes];
-  uint8_t w1t[kW * 128];
-  float bias[kMaxHiddenMMA + 1][kW];
-  float bout[kOutN];
-  unsigned long long bar_in[kS];               // inputs staged (128 arrivals)
-  unsigned long long bar_ch[kS][4];            // activation chunk written (128 arrivals)
-  unsigned long long bar_d[kS];                // MMA group complete (tcgen05.commit)
-  long long tile[kS];                          // the stream's tile (published with bar_in)
-  unsigned int tk[kS];
-  uint32_t tmem_base;
-};
-
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// tcgen05.wait::ld with the destination registers as operands, so no use of them
-// is scheduled before the wait
-__device__ __forceinline__ void tmem_wait32(uint32_t* r) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
-                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
-                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
-               :
-               : "memory");
-}
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
-  return e;
-}
-
-// 32 pre-activations (+ bias b, or none) -> ELU -> bf16 into the A tile, as tc::elu
-template <bool BIAS>
-__device__ __forceinline__ void elu_chunk(const uint32_t* r, uint32_t bias_saddr, uint32_t tile, int row, int c0) {
-  float h[32];
-  float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    float2 t = make_float2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
-    if (BIAS) {
-      if ((q & 1) == 0) b4 = lds_f4(bias_saddr + (uint32_t)(c0 + 2 * q) * 4u);
-      t = __fadd2_rn(t, (q & 1) ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y));
-    }
-    const float2 u = __fmul2_rn(t, make_float2(1.4426950408889634f, 1.4426950408889634f));
-    const float2 e = __fadd2_rn(make_float2(ex2_approx(u.x), ex2_approx(u.y)), make_float2(-1.0f, -1.0f));
-    h[2 * q] = t.x > 0.0f ? t.x : e.x;
-    h[2 * q + 1] = t.y > 0.0f ? t.y : e.y;
-  }
-  store_act32(tile, row, c0, h);
-}
-
-// one ELU layer's epilogue from TMEM columns [dcol, dcol + 128) of this thread's lane
-template <bool BIAS>
-__device__ __forceinline__ void elu_layer(uint32_t dcol, uint32_t bias_saddr, uint32_t tile, int row,
-                                          unsigned long long* bar_ch) {
-  uint32_t ra[32], rb[32];
-  tmem_ld32_nw(dcol, ra);
-  tmem_wait32(ra);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t* cur = (c & 1) ? rb : ra;
-    uint32_t* nxt = (c & 1) ? ra : rb;
-    if (c < 3) tmem_ld32_nw(dcol + 32 * (c + 1), nxt);   // in flight under this chunk's math
-    elu_chunk<BIAS>(cur, bias_saddr, tile, row, 32 * c);
-    fence_async_smem();                                   // the chunk is visible to the MMA (async proxy)
-    fence_before();
-    mbar_arrive(bar_ch + c);
-    if (c < 3) tmem_wait32(nxt);
-  }
-}
-}  // namespace ws
-
 template <bool WIDE>   // WIDE: out_dim in (8, 16] (the affine-velocity field), a second TMEM load
 __global__ void __launch_bounds__(kThreads, 1)
 k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64_t* __restrict__ scene_off,
@@ -470,14 +383,10 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
       tmem_wait();
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-#if NSF_MLP_PAIRED
-        ws::elu_chunk<false>(r2 + 32 * hh, 0u, a_saddr, t, c0 + 32 * hh);
-#else
         float h[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) h[q] = elu(__uint_as_float(r2[32 * hh + q]));
         store_act32(a_saddr, t, c0 + 32 * hh, h);
-#endif
       }
     }
     fence_before();
@@ -511,11 +420,8 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
         tmem_wait();
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          const int cc = c0 + 32 * hh;
-#if NSF_MLP_PAIRED
-          ws::elu_chunk<true>(r2 + 32 * hh, bias_saddr + (uint32_t)((l + 1) * kW) * 4u, a_saddr, t, cc);
-#else
           float h[32];
+          const int cc = c0 + 32 * hh;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 b = lds_f4(bias_saddr + (uint32_t)((l + 1) * kW + cc + 4 * q) * 4u);
@@ -525,7 +431,6 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
             h[4 * q + 3] = elu(__uint_as_float(r2[32 * hh + 4 * q + 3]) + b.w);
           }
           store_act32(a_saddr, t, cc, h);
-#endif
         }
       }
       fence_before();
@@ -575,273 +480,6 @@ k_nsf_mlp_tc(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64
     fence_before();
     stream_barrier(s);   // the A tile and accumulators are free for the next tile
     tile = next;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-  if (mlp.ctr && tid == 0) {   // the last CTA resets the counters for the next launch
-    __threadfence();
-    if (atomicAdd(mlp.ctr + 1, 1u) == gridDim.x - 1) {
-      mlp.ctr[0] = 0u;
-      mlp.ctr[1] = 0u;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-specialised form of the same network (the default; NSF_MLP_WS=0 selects
-// k_nsf_mlp_tc).  Per CTA (one per SM) two streams of 128 points, each with an
-// epilogue warpgroup (thread = point = TMEM lane) and an MMA warp, and two TMEM
-// accumulators per stream used alternately by layer (D[m & 1] for MMA m).  The
-// epilogue of layer m reads D[m & 1] in 32-column chunks (the next chunk's
-// tcgen05.ld in flight under the current chunk's math), writes the bf16
-// activations of the chunk into the A tile and arrives on the chunk's mbarrier;
-// the MMA warp then issues layer m + 1's two K = 16 steps of that chunk into
-// D[(m + 1) & 1].  So the next layer's MMA runs under the current layer's
-// epilogue, and the epilogue warps only wait for the last chunk's MMA.  Bias,
-// ELU and bf16 rounding are those of k_nsf_mlp_tc (reading #20), evaluated two
-// columns at a time with paired fp32 ops (FADD2 / FMUL2: per lane the same
-// operations), so the two kernels agree bit for bit.
-
-template <bool WIDE>
-__global__ void __launch_bounds__(ws::kThreads, 1)
-k_nsf_mlp_ws(int64_t n, const float* __restrict__ X, int64_t xpitch, const int64_t* __restrict__ scene_off,
-             int n_scenes, const float* __restrict__ z, const float* __restrict__ dz, int r,
-             const int64_t* __restrict__ d_step, MlpDev mlp, float stress_scale, float* __restrict__ tau_out,
-             int aos_out, NsfP2G q) {
-  extern __shared__ uint8_t smem_raw[];
-  ws::Smem& sm = *reinterpret_cast<ws::Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int L = mlp.n_hidden + 1;
-  const int nmh = mlp.n_hidden - 1;   // hidden layers on the tensor cores
-  const int in_dim = mlp.in_dim;
-
-  // ---- one-time setup (as k_nsf_mlp_tc): weights, biases, barriers, TMEM ----
-  for (int l = 0; l < nmh; ++l) {
-    const uint16_t* W = mlp.W + mlp.w_off[l + 1];
-    for (int c = tid; c < kW * (kW / 8); c += ws::kThreads) {
-      const int nrow = c >> 4, kc = c & 15;
-      cp_async16(smem_u32(sm.wB[l] + sw128_offset(nrow, kc * 8, kW)), W + nrow * kW + kc * 8, 16);
-    }
-  }
-  {
-    const uint16_t* W = mlp.W + mlp.w_off[L - 1];
-    for (int c = tid; c < kOutN * (kW / 8); c += ws::kThreads) {
-      const int nrow = c >> 4, kc = c & 15;
-      const bool in = nrow < mlp.out_dim;
-      cp_async16(smem_u32(sm.wOut + sw128_offset(nrow, kc * 8, kOutN)), in ? W + nrow * kW + kc * 8 : W, in ? 16 : 0);
-    }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int e = tid; e < kW * 32; e += ws::kThreads) {
-    const int j = e >> 5, k = e & 31, i = k & 15;
-    const float bj = mlp.b[mlp.b_off[0] + j];
-    const float b_hi = __uint_as_float(to_tf32(bj));
-    float w = 0.0f;
-    if (i < in_dim) w = __uint_as_float(((uint32_t)mlp.W[mlp.w_off[0] + j * in_dim + i]) << 16);
-    else if (i == in_dim) w = b_hi;
-    else if (i == in_dim + 1) w = __uint_as_float(to_tf32(bj - b_hi));
-    *reinterpret_cast<float*>(sm.w1t + j * 128 + ((((k >> 2) ^ (j & 7))) << 4) + (k & 3) * 4) = w;
-  }
-  for (int e = tid; e < (kMaxHiddenMMA + 1) * kW; e += ws::kThreads) {
-    const int l = e / kW, j = e % kW;
-    sm.bias[l][j] = l < mlp.n_hidden ? mlp.b[mlp.b_off[l] + j] : 0.0f;
-  }
-  if (tid < kOutN) sm.bout[tid] = tid < mlp.out_dim ? mlp.b[mlp.b_off[L - 1] + tid] : 0.0f;
-  if (tid == 0) {
-    for (int k = 0; k < ws::kS; ++k) {
-      mbar_init(&sm.bar_in[k], 128);
-      for (int c = 0; c < 4; ++c) mbar_init(&sm.bar_ch[k][c], 128);
-      mbar_init(&sm.bar_d[k], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&sm.tmem_base))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  fence_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = sm.tmem_base;
-  const int64_t n_tiles = (n + kM - 1) / kM;
-  const int64_t tile_stride = (int64_t)gridDim.x * ws::kS;
-  constexpr uint32_t kIdesc1 = make_idesc(kM, kW, 2u);
-  constexpr uint32_t kIdescH = make_idesc(kM, kW);
-  constexpr uint32_t kIdescO = make_idesc(kM, kOutN);
-
-  if (tid >= ws::kEpi) {
-    // ================= MMA warp of stream s =================
-    const int s = (tid - ws::kEpi) >> 5;
-    const uint32_t d0 = tmem + (uint32_t)(256 * s);
-    const uint32_t a_saddr = smem_u32(sm.a[s]);
-    const uint32_t w1_saddr = smem_u32(sm.w1t);
-    uint32_t ph_in = 0, ph_ch = 0;
-    while (true) {
-      mbar_wait(&sm.bar_in[s], ph_in);
-      ph_in ^= 1;
-      if (*(volatile long long*)&sm.tile[s] >= n_tiles) break;
-      fence_after();
-      if (lane == 0) {   // layer 1: K = 32 tf32 [hi | lo] inputs (bias in the MMA) -> D[0]
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_tf32(d0, make_desc(a_saddr + kk * 32), make_desc(w1_saddr + kk * 32), kIdesc1, kk > 0 ? 1u : 0u);
-        mma_commit(&sm.bar_d[s]);
-      }
-      __syncwarp();
-      for (int m = 1; m <= nmh + 1; ++m) {   // hidden layers, then the output layer
-        const bool out = m == nmh + 1;
-        const uint32_t dcol = d0 + (uint32_t)(128 * (m & 1));
-        const uint32_t b_saddr = out ? smem_u32(sm.wOut) : smem_u32(sm.wB[m - 1]);
-        const int brows = out ? kOutN : kW;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          mbar_wait(&sm.bar_ch[s][c], ph_ch);
-          fence_after();
-          if (lane == 0) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int kk = 2 * c + h;   // K step of 16 columns
-              const uint32_t koff = (uint32_t)((kk >> 2) * (kM * 128) + (kk & 3) * 32);
-              const uint32_t kofb = (uint32_t)((kk >> 2) * (brows * 128) + (kk & 3) * 32);
-              mma_bf16(dcol, make_desc(a_saddr + koff), make_desc(b_saddr + kofb), out ? kIdescO : kIdescH,
-                       kk > 0 ? 1u : 0u);
-            }
-          }
-          __syncwarp();
-        }
-        ph_ch ^= 1;
-        if (lane == 0) mma_commit(&sm.bar_d[s]);
-        __syncwarp();
-      }
-    }
-  } else {
-    // ================= epilogue warpgroup of stream s (thread = point) =================
-    const int s = tid >> 7;
-    const int t = tid & 127;
-    const uint32_t d0 = tmem + (uint32_t)(256 * s) + (((uint32_t)(32 * (warp & 3))) << 16);
-    const uint32_t a_saddr = smem_u32(sm.a[s]);
-    const int64_t step = d_step ? *d_step : 0;
-    uint32_t ph_d = 0;
-    auto fetch_x = [&](int64_t tile_, float* x_, int& scene_) {
-      const int64_t p_ = tile_ * kM + t;
-      scene_ = -1;
-      x_[0] = x_[1] = x_[2] = 0.0f;
-      if (tile_ >= n_tiles || p_ >= n) return;
-      scene_ = scene_of(p_, scene_off, n_scenes, n);
-      if (xpitch >= 0) {
-        x_[0] = X[0 * xpitch + p_];
-        x_[1] = X[1 * xpitch + p_];
-        x_[2] = X[2 * xpitch + p_];
-      } else {
-        x_[0] = X[pbase(p_) + 0 * 32];
-        x_[1] = X[pbase(p_) + 1 * 32];
-        x_[2] = X[pbase(p_) + 2 * 32];
-      }
-    };
-    int64_t tile = (int64_t)blockIdx.x * ws::kS + s;
-    if (mlp.ctr) {
-      if (t == 0) sm.tk[s] = atomicAdd(mlp.ctr, 1u);
-      stream_barrier(s);
-      tile = sm.tk[s];
-    }
-    float xf[3];
-    int scene_f;
-    fetch_x(tile, xf, scene_f);
-    while (true) {
-      const int64_t p = tile * kM + t;
-      const bool live = tile < n_tiles && p < n;
-      const int scene = scene_f < 0 ? 0 : scene_f;
-      if (tile < n_tiles) {
-        // A row t = [hi(u) | lo(u)] (the previous tile's output MMA, the last reader, is complete)
-        float u[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) u[i] = 0.0f;
-        if (scene_f >= 0) {
-          u[0] = xf[0];
-          u[1] = xf[1];
-          u[2] = xf[2];
-          for (int k = 0; k < r && k < 13; ++k)
-            u[3 + k] = z[scene_f * r + k] + (float)step * (dz ? dz[scene_f * r + k] : 0.0f);
-          u[in_dim] = 1.0f;
-          u[in_dim + 1] = 1.0f;
-        }
-        const uint32_t row = a_saddr + (uint32_t)t * 128u;
-        const uint32_t sw = (uint32_t)(t & 7);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint4 hi, lo;
-          uint32_t* ph = &hi.x;
-          uint32_t* pl = &lo.x;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float x = u[4 * c + e];
-            const uint32_t xh = to_tf32(x);
-            ph[e] = xh;
-            pl[e] = to_tf32(x - __uint_as_float(xh));
-          }
-          sts_u4(row + (((uint32_t)c ^ sw) << 4), hi);
-          sts_u4(row + (((uint32_t)(c + 4) ^ sw) << 4), lo);
-        }
-        if (mlp.ctr && t == 0) sm.tk[s] = atomicAdd(mlp.ctr, 1u);   // the next tile (read after a barrier)
-      }
-      if (t == 0) sm.tile[s] = tile;
-      fence_async_smem();
-      fence_before();
-      ws::mbar_arrive(&sm.bar_in[s]);
-      if (tile >= n_tiles) break;
-      // ---- layer-1 epilogue (bias added by the MMA) ----
-      mbar_wait(&sm.bar_d[s], ph_d);
-      ph_d ^= 1;
-      fence_after();
-      ws::elu_layer<false>(d0, 0u, a_saddr, t, sm.bar_ch[s]);
-      // the next tile: X in flight across the hidden layers
-      stream_barrier(s);
-      const int64_t next = mlp.ctr ? (int64_t)sm.tk[s] : tile + tile_stride;
-      fetch_x(next, xf, scene_f);
-      // ---- hidden-layer epilogues: bias + ELU ----
-      for (int m = 1; m <= nmh; ++m) {
-        mbar_wait(&sm.bar_d[s], ph_d);
-        ph_d ^= 1;
-        fence_after();
-        ws::elu_layer<true>(d0 + (uint32_t)(128 * (m & 1)), smem_u32(&sm.bias[m][0]), a_saddr, t, sm.bar_ch[s]);
-      }
-      // ---- output layer ----
-      float xp[3], vp[3], Cp[9];
-      if (q.enabled && live) nsf_load_point(q.S, p, xp, vp, Cp);
-      mbar_wait(&sm.bar_d[s], ph_d);
-      ph_d ^= 1;
-      fence_after();
-      const uint32_t ocol = d0 + (uint32_t)(128 * ((nmh + 1) & 1));
-      float y[8];
-      tmem_ld8(ocol, y);
-      float y2[8];
-      if (WIDE) tmem_ld8(ocol + 8, y2);
-      fence_before();
-      if (live) {
-        float tau[8];
-#pragma unroll
-        for (int o = 0; o < 8; ++o) tau[o] = stress_scale * (y[o] + sm.bout[o]);
-        for (int o = 0; o < mlp.out_dim && o < 8; ++o) {
-          if (aos_out) tau_out[p * mlp.out_dim + o] = tau[o];
-          else tau_out[pbase(p) + o * 32] = tau[o];
-        }
-        if (q.enabled) nsf_p2g_point(q, scene, xp, vp, Cp, tau, step);   // reduced P2G
-        if (WIDE)
-          for (int o = 8; o < mlp.out_dim; ++o) {
-            const float val = stress_scale * (y2[o - 8] + sm.bout[o]);
-            if (aos_out) tau_out[p * mlp.out_dim + o] = val;
-            else tau_out[pbase(p) + o * 32] = val;
-          }
-      }
-      tile = next;
-    }
   }
   __syncthreads();
   if (warp == 0) {
@@ -1128,16 +766,6 @@ bool nsf_mlp_tc_supported(const MlpDev& mlp) {
          mlp.out_dim <= kOutN;
 }
 
-// NSF_MLP_WS=0: the three-stream kernel without warp specialisation (A/B)
-static bool mlp_ws_enabled() {
-  static int f = -1;
-  if (f < 0) {
-    const char* e = getenv("NSF_MLP_WS");
-    f = (e && e[0] == '0') ? 0 : 1;
-  }
-  return f == 1;
-}
-
 void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitch, const int64_t* scene_off,
                        int n_scenes, const float* z, const float* dz, int r, const int64_t* d_step,
                        const MlpDev& mlp, float stress_scale, float* tau_out, int aos_out, const NsfP2G* qp) {
@@ -1156,24 +784,6 @@ void launch_nsf_mlp_tc(cudaStream_t st, int64_t n, const float* X, int64_t xpitc
     attr = true;
   }
   const int64_t tiles = (n + kM - 1) / kM;
-  if (mlp_ws_enabled()) {
-    static bool attr_ws = false;
-    const size_t smem_ws = sizeof(ws::Smem) + 1024;
-    if (!attr_ws) {
-      cudaFuncSetAttribute(k_nsf_mlp_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
-      cudaFuncSetAttribute(k_nsf_mlp_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ws);
-      attr_ws = true;
-    }
-    int64_t g = (tiles + ws::kS - 1) / ws::kS;
-    if (g > n_sms) g = n_sms;
-    if (mlp.out_dim > 8)
-      k_nsf_mlp_ws<true><<<(unsigned)g, ws::kThreads, smem_ws, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r,
-                                                                   d_step, mlp, stress_scale, tau_out, aos_out, q);
-    else
-      k_nsf_mlp_ws<false><<<(unsigned)g, ws::kThreads, smem_ws, st>>>(n, X, xpitch, scene_off, n_scenes, z, dz, r,
-                                                                    d_step, mlp, stress_scale, tau_out, aos_out, q);
-    return;
-  }
   int64_t grid = (tiles + kStreams - 1) / kStreams;
   if (grid > n_sms) grid = n_sms;
   if (mlp.out_dim > 8)
