@@ -947,7 +947,8 @@ struct __align__(16) FusedSmemT {
   float4 slot[64 * FusedSlots<ROWS>::kCellStride4];
   float4 sc[kScatterCap * kRowF4];             // out-of-block particles: staged rows (+ packed base)
   int pop[64];
-  int next;
+  int next;                                    // the next segment: ticket, block key and storage range
+  int nkey, ns0, ns1;                          //   (fetched by thread NT - 1 during phase 1)
   int nsc;                                     // entries of sc this segment
 };
 static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_DENSE_MIN_BLOCKS, "fused kernel: CTAs per SM");
@@ -1321,6 +1322,23 @@ __device__ __forceinline__ void scatter_listed(const float4* sc, int nsc, int i0
   }
 }
 
+// The fused kernel's next segment: its ticket, and (if any) its block key and
+// storage range, into shared memory.  Called by one thread: at the kernel start,
+// then during phase 1 by the last thread, which usually idles in the last pass, so
+// the three dependent global round trips stay off the segment's critical path.
+template <class SM>
+__device__ __forceinline__ void claim_segment(SM& sm, int32_t* counters, const int32_t* __restrict__ nonempty,
+                                              const int32_t* __restrict__ block_start, int nblk) {
+  const int t = atomicAdd(&counters[3], 1);
+  sm.next = t;
+  if (t < nblk) {
+    const int key = nonempty[t];
+    sm.nkey = key;
+    sm.ns0 = block_start[key];
+    sm.ns1 = block_start[key + 1];
+  }
+}
+
 // ROT: the grid update runs inside this kernel (RotGrid, pipeline.h): `vel`,
 // `acc`, `flags`, `list` and `list_count` are ignored and taken from the
 // rotation instead; the segment's velocity tile is staged from the raw P2G sums
@@ -1395,9 +1413,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     if (DO_G2P && blockIdx.x == 0 && tid == 0) atomicAdd((unsigned long long*)d_step, 1ull);
   }
   (void)cnt2;
-  // segment tickets: the first here, each next one claimed after phase 1 of the
-  // current segment (its round trip overlaps phase 2)
-  if (tid == 0) sm.next = atomicAdd(&counters[3], 1);
+  // segment tickets: the first here, each next one claimed (with its key and
+  // range) during phase 1 of the current segment
+  if (tid == 0) claim_segment(sm, counters, nonempty, block_start, nblk);
 #if NSF_STATS
   long long t_mark = clock64();
 #endif
@@ -1408,9 +1426,9 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
 #endif
     const int bi = sm.next;
     if (bi >= nblk) break;
-    const int key = nonempty[bi];
+    const int key = sm.nkey;
     const BlockCoord bc = decode_block(key, P);
-    const int s0 = block_start[key], s1 = block_start[key + 1];
+    const int s0 = sm.ns0, s1 = sm.ns1;
     if (tid == 0) {
       NSF_STAT_ADD(kStSegments, 1);
       NSF_STAT_ADD(kStParticles, s1 - s0);
@@ -1544,11 +1562,15 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       if (inline_scatter) p2g_scatter_direct<HALO>(xn, vn, Cn, tau, gacc, tc, P);
 #endif
     }
+    // (every thread read the current segment's slots at the loop top, before the tile
+    // barrier).  192 threads: the last one idles in the last phase-1 pass; more: it
+    // is a phase-2 helper, and claims after the barrier
+    if (NT <= 192 && tid == NT - 1) claim_segment(sm, counters, nonempty, block_start, nblk);
     __syncthreads();
+    if (NT > 192 && tid == NT - 1) claim_segment(sm, counters, nonempty, block_start, nblk);
 #if NSF_STATS
     if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycPhase1, t - t_mark); t_mark = t; }
 #endif
-    if (tid == 0) sm.next = atomicAdd(&counters[3], 1);   // the next segment (bi is in registers)
 #if NSF_STATS
     long long t_p2 = clock64();
 #endif
