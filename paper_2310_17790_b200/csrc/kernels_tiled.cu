@@ -1764,27 +1764,42 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
 // non-empty block lies in its 27-neighbourhood (the blocks a segment's P2G can
 // reach while its particles drift <= 4 cells).  Thread per (segment, neighbour):
 // the first to mark B (hmark zeroed before) lists it for the grid update.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
 k_halo(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty, int* __restrict__ hmark,
        int* __restrict__ halo, int* __restrict__ nhalo, DevParams P) {
-  const int nblk = *n_nonempty;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int e = (int)(t / 27), d = (int)(t % 27);
-  if (e >= nblk) return;
-  const BlockCoord bc = decode_block(nonempty[e], P);
-  const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
-  if (n0 < 0 || n1 < 0 || n2 < 0 || n0 >= P.NB[0] || n1 >= P.NB[1] || n2 >= P.NB[2]) return;
-  const int B = (int)((int64_t)bc.scene * P.blocks_per_scene + block_id(n0, n1, n2, P));
-  if (atomicExch(hmark + B, 1) == 0) halo[atomicAdd(nhalo, 1)] = B;
+  // one wave of CTAs, each over a contiguous range of (segment, neighbour) items in
+  // rounds of blockDim; a round's new members are counted in shared memory and
+  // appended with one global atomic (a per-thread append serialised ~3,400 atomics
+  // on one counter, and a thread per item launched 27 x 262,144 threads: 27 us)
+  __shared__ int cnt, base;
+  const int64_t items = 27 * (int64_t)(*n_nonempty);
+  const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = blockIdx.x * per, c1 = min(items, c0 + per);
+  for (int64_t r0 = c0; r0 < c1; r0 += blockDim.x) {
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const int64_t t = r0 + threadIdx.x;
+    int B = -1, slot = -1;
+    if (t < c1) {
+      const int e = (int)(t / 27), d = (int)(t % 27);
+      const BlockCoord bc = decode_block(nonempty[e], P);
+      const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
+      if (n0 >= 0 && n1 >= 0 && n2 >= 0 && n0 < P.NB[0] && n1 < P.NB[1] && n2 < P.NB[2]) {
+        B = (int)((int64_t)bc.scene * P.blocks_per_scene + block_id(n0, n1, n2, P));
+        if (atomicExch(hmark + B, 1) == 0) slot = atomicAdd(&cnt, 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base = cnt ? atomicAdd(nhalo, cnt) : 0;
+    __syncthreads();
+    if (slot >= 0) halo[base + slot] = B;
+  }
 }
 
 void launch_halo(cudaStream_t st, PipelineBuffers* pb, const DevParams& P) {
   cudaMemsetAsync(pb->nhalo, 0, sizeof(int), st);
   cudaMemsetAsync(pb->hmark, 0, sizeof(int) * pb->total_blocks, st);
-  const int64_t maxn = pb->total_blocks < pb->pitch ? pb->total_blocks : pb->pitch;   // bound on non-empty blocks
-  const int64_t threads = 27 * (maxn > 0 ? maxn : 1);
-  k_halo<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->hmark, pb->halo,
-                                                          pb->nhalo, P);
+  k_halo<<<num_sms(), 512, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->hmark, pb->halo, pb->nhalo, P);
 }
 
 // physical reorder into binned order: out[j] = in[perm[j]] (all 30 fields + id)
