@@ -43,6 +43,8 @@ __device__ __forceinline__ int aggregated_increment(int* arr, int key, unsigned 
 __global__ void k_keys_hist(int64_t n, const float* __restrict__ S, int64_t pitch,
                             const int64_t* __restrict__ scene_off, int n_scenes, int32_t* keys,
                             int32_t* counts, DevParams P) {
+  pdl_launch_dependents();
+  pdl_wait();
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned active = __ballot_sync(0xffffffffu, j < n);
   if (j >= n) return;
@@ -64,7 +66,8 @@ void launch_keys_hist(cudaStream_t st, int64_t n, const float* S, int64_t pitch,
                       int n_scenes, int32_t* keys, int32_t* counts, const DevParams& P) {
   if (n == 0) return;
   int bs = 256;
-  k_keys_hist<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(n, S, pitch, scene_off, n_scenes, keys, counts, P);
+  launch_pdl(k_keys_hist, dim3((unsigned)((n + bs - 1) / bs)), dim3(bs), 0, st, n, S, pitch, scene_off, n_scenes, keys,
+             counts, P);
 }
 
 // ---------------------------------------------------------------------------
@@ -92,6 +95,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* c
                                                        int32_t* cursor, int32_t* nonempty, int32_t* n_nonempty,
                                                        unsigned long long* status, unsigned long long* ticket,
                                                        int64_t n_tiles, int32_t* ne_of, int4* cellcnt) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ unsigned long long warp_sums[kScanThreads / 32];
   __shared__ unsigned long long s_prefix;
   __shared__ unsigned long long s_ticket;
@@ -134,7 +139,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* c
     if (tile == 0) {
       if (lane == 0) atomicExch(&status[0], kFlagInc | ep | agg);
       // work counters of the kernels that follow (grid update, P2G, G2P)
-      if (lane >= 1 && lane <= 3) n_nonempty[lane] = 0;
+      // ([4]: the halo list's length, built after this scan)
+      if (lane >= 1 && lane <= 4) n_nonempty[lane] = 0;
     } else {
       if (lane == 0) atomicExch(&status[tile], kFlagAgg | ep | agg);
       int64_t base_t = tile - 1;
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int64_t total, int32_t* c
 }
 
 void launch_scan(cudaStream_t st, PipelineBuffers* pb) {
-  k_scan<<<(unsigned)pb->scan_tiles, kScanThreads, 0, st>>>(pb->total_blocks, pb->counts, pb->block_start,
+  launch_pdl(k_scan, dim3((unsigned)pb->scan_tiles), dim3(kScanThreads), 0, st, pb->total_blocks, pb->counts, pb->block_start,
                                                              pb->cursor, pb->nonempty, pb->n_nonempty,
                                                              pb->scan_status, pb->scan_ticket, pb->scan_tiles,
                                                              pb->ne_of, reinterpret_cast<int4*>(pb->cellcnt));
@@ -274,6 +280,8 @@ __device__ __forceinline__ int cell_of_x(float x0, float x1, float x2, const Dev
 __global__ void k_cell_rank(int64_t n, const float* __restrict__ S, const int32_t* __restrict__ keys,
                             const int32_t* __restrict__ ne_of, int32_t* cellcnt, int32_t* __restrict__ rank,
                             DevParams P) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const unsigned active = __ballot_sync(0xffffffffu, j < n);
   if (j >= n) return;
@@ -285,6 +293,8 @@ __global__ void k_cell_rank(int64_t n, const float* __restrict__ S, const int32_
 
 __global__ void k_cell_scan(int32_t* cellcnt, const int32_t* __restrict__ nonempty,
                             const int32_t* __restrict__ n_nonempty, const int32_t* __restrict__ block_start) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int nblk = *n_nonempty;
   for (int e = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); e < nblk;
@@ -307,6 +317,8 @@ __global__ void __launch_bounds__(128) k_copy_cells(int64_t n, const float* __re
                                                     const int32_t* __restrict__ keys, const int32_t* __restrict__ ne_of,
                                                     const int32_t* __restrict__ cellcnt,
                                                     const int32_t* __restrict__ rank, DevParams P) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   const float* sp = Sin + pbase(j);
@@ -327,10 +339,13 @@ void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, i
                                int32_t* ids_out, PipelineBuffers* pb, const DevParams& P) {
   if (n == 0) return;
   const unsigned g = (unsigned)((n + 255) / 256);
-  k_cell_rank<<<g, 256, 0, st>>>(n, Sin, pb->keys, pb->ne_of, pb->cellcnt, pb->perm, P);
-  k_cell_scan<<<num_sms() * 4, 256, 0, st>>>(pb->cellcnt, pb->nonempty, pb->n_nonempty, pb->block_start);
-  k_copy_cells<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, Sin, Sout, ids_in, ids_out, pb->keys, pb->ne_of,
-                                                            pb->cellcnt, pb->perm, P);
+  launch_pdl(k_cell_rank, dim3(g), dim3(256), 0, st, n, Sin, (const int32_t*)pb->keys, (const int32_t*)pb->ne_of,
+             pb->cellcnt, pb->perm, P);
+  launch_pdl(k_cell_scan, dim3(num_sms() * 4), dim3(256), 0, st, pb->cellcnt, (const int32_t*)pb->nonempty,
+             (const int32_t*)pb->n_nonempty, (const int32_t*)pb->block_start);
+  launch_pdl(k_copy_cells, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, st, n, Sin, Sout, ids_in, ids_out,
+             (const int32_t*)pb->keys, (const int32_t*)pb->ne_of, (const int32_t*)pb->cellcnt,
+             (const int32_t*)pb->perm, P);
 }
 
 // Processing order of the fused kernel's segments (longest first): the
@@ -342,6 +357,8 @@ void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, i
 __global__ void __launch_bounds__(1024) k_lpt_order(int32_t* __restrict__ nonempty,
                                                     const int32_t* __restrict__ n_nonempty,
                                                     const int32_t* __restrict__ block_start, int32_t* __restrict__ tmp) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ int hist[256];
   const int tid = threadIdx.x;
   const int nblk = *n_nonempty;
@@ -376,7 +393,8 @@ __global__ void __launch_bounds__(1024) k_lpt_order(int32_t* __restrict__ nonemp
 }
 
 void launch_lpt_order(cudaStream_t st, PipelineBuffers* pb) {
-  k_lpt_order<<<1, 1024, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->block_start, pb->ne_tmp);
+  launch_pdl(k_lpt_order, dim3(1), dim3(1024), 0, st, pb->nonempty, (const int32_t*)pb->n_nonempty,
+             (const int32_t*)pb->block_start, pb->ne_tmp);
 }
 
 }  // namespace nsf

@@ -54,12 +54,6 @@ __device__ __forceinline__ void tail_stat_end() {
 }
 #endif
 
-// Programmatic dependent launch (the grid update and the fused kernel are launched
-// with cudaLaunchAttributeProgrammaticStreamSerialization): a dependent grid's CTAs
-// are scheduled before its predecessor completes and wait here for its results.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
 __device__ __forceinline__ void red_add_v4_t(float4* addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
@@ -1766,12 +1760,17 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
 // the first to mark B (hmark zeroed before) lists it for the grid update.
 __global__ void __launch_bounds__(512)
 k_halo(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonempty, int* __restrict__ hmark,
-       int* __restrict__ halo, int* __restrict__ nhalo, DevParams P) {
+       int* __restrict__ halo, int* __restrict__ nhalo, const unsigned long long* __restrict__ scan_ticket,
+       int64_t scan_tiles, DevParams P) {
   // one wave of CTAs, each over a contiguous range of (segment, neighbour) items in
   // rounds of blockDim; a round's new members are counted in shared memory and
   // appended with one global atomic (a per-thread append serialised ~3,400 atomics
   // on one counter, and a thread per item launched 27 x 262,144 threads: 27 us)
   __shared__ int cnt, base;
+  pdl_launch_dependents();
+  pdl_wait();
+  // marks carry the re-binning's scan epoch (>= 1), so hmark needs no clearing
+  const int tag = (int)(*scan_ticket / (unsigned long long)scan_tiles);
   const int64_t items = 27 * (int64_t)(*n_nonempty);
   const int64_t per = (items + gridDim.x - 1) / gridDim.x;
   const int64_t c0 = blockIdx.x * per, c1 = min(items, c0 + per);
@@ -1786,7 +1785,7 @@ k_halo(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonem
       const int n0 = bc.b[0] + d / 9 - 1, n1 = bc.b[1] + (d / 3) % 3 - 1, n2 = bc.b[2] + d % 3 - 1;
       if (n0 >= 0 && n1 >= 0 && n2 >= 0 && n0 < P.NB[0] && n1 < P.NB[1] && n2 < P.NB[2]) {
         B = (int)((int64_t)bc.scene * P.blocks_per_scene + block_id(n0, n1, n2, P));
-        if (atomicExch(hmark + B, 1) == 0) slot = atomicAdd(&cnt, 1);
+        if (atomicExch(hmark + B, tag) != tag) slot = atomicAdd(&cnt, 1);
       }
     }
     __syncthreads();
@@ -1796,10 +1795,10 @@ k_halo(const int32_t* __restrict__ nonempty, const int32_t* __restrict__ n_nonem
   }
 }
 
+// (nhalo is reset by the scan of the same re-binning)
 void launch_halo(cudaStream_t st, PipelineBuffers* pb, const DevParams& P) {
-  cudaMemsetAsync(pb->nhalo, 0, sizeof(int), st);
-  cudaMemsetAsync(pb->hmark, 0, sizeof(int) * pb->total_blocks, st);
-  k_halo<<<num_sms(), 512, 0, st>>>(pb->nonempty, pb->n_nonempty, pb->hmark, pb->halo, pb->nhalo, P);
+  launch_pdl(k_halo, dim3(num_sms()), dim3(512), 0, st, (const int32_t*)pb->nonempty, (const int32_t*)pb->n_nonempty,
+             pb->hmark, pb->halo, pb->nhalo, (const unsigned long long*)pb->scan_ticket, pb->scan_tiles, P);
 }
 
 // physical reorder into binned order: out[j] = in[perm[j]] (all 30 fields + id)

@@ -16,6 +16,15 @@
 #ifndef NSF_CHECKED
 #define NSF_CHECKED 0
 #endif
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (launch_pdl, kernels.h) may be
+// scheduled before its predecessor completes; pdl_wait() blocks until the
+// predecessor's results are visible, pdl_launch_dependents() lets the successor
+// be scheduled.  Both are no-ops for a normal launch.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
 // Work counters of the statistics build (-DNSF_STATS=1, nsf_mpm_debug_stats):
 // segments, particles, staged rows, listed, inline-scattered, out-of-tile gathers,
 // phase-1 passes, and (thread 0 of each CTA, clock64) the cycles spent from the

@@ -42,7 +42,7 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
     pb->ne_of = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * total_blocks);
     if (!pb->ne_of) return -1;
   }
-  pb->n_nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 4);
+  pb->n_nonempty = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 8);
   pb->scan_status = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * pb->scan_tiles);
   pb->scan_ticket = (unsigned long long*)pipeline_alloc(h, sizeof(unsigned long long) * 4);
   if (!pb->counts || !pb->block_start || !pb->cursor || !pb->nonempty || !pb->ne_tmp || !pb->n_nonempty || !pb->scan_status ||
@@ -54,12 +54,14 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
   if (cudaMemsetAsync(pb->scan_status, 0, sizeof(unsigned long long) * pb->scan_tiles, v.stream) != cudaSuccess)
     return -1;
   if (cudaMemsetAsync(pb->scan_ticket, 0, sizeof(unsigned long long) * 4, v.stream) != cudaSuccess) return -1;
+  if (cudaMemsetAsync(pb->n_nonempty, 0, sizeof(int32_t) * 8, v.stream) != cudaSuccess) return -1;
   pb->flags = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
   pb->touched = (int*)pipeline_alloc(h, sizeof(int) * (total_blocks + 4));
   pb->hmark = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
   pb->halo = (int*)pipeline_alloc(h, sizeof(int) * total_blocks);
-  pb->nhalo = (int*)pipeline_alloc(h, sizeof(int) * 4);
+  pb->nhalo = pb->n_nonempty ? pb->n_nonempty + 4 : nullptr;   // reset by every scan
   if (!pb->flags || !pb->touched || !pb->hmark || !pb->halo || !pb->nhalo) return -1;
+  if (cudaMemsetAsync(pb->hmark, 0, sizeof(int) * total_blocks, v.stream) != cudaSuccess) return -1;
   if (cudaMemsetAsync(pb->flags, 0, sizeof(int) * total_blocks, v.stream) != cudaSuccess) return -1;
   if (cudaMemsetAsync(pb->touched, 0, sizeof(int) * (total_blocks + 4), v.stream) != cudaSuccess) return -1;
   p2g_tables_init(v.stream);

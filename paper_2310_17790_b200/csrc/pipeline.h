@@ -41,7 +41,8 @@ struct PipelineBuffers {
   int32_t* ne_of = nullptr;         // [total_blocks] list index of a non-empty block (cell-ordered re-binning)
   int32_t* ne_tmp = nullptr;        // [total_blocks] scratch of the longest-first segment order (fused)
   int32_t* cellcnt = nullptr;       // [64 * min(total_blocks, pitch)] per-cell counts, then starts (idem)
-  int32_t* n_nonempty = nullptr;    // [4]: n_nonempty, (unused), (unused), p2g block ticket (reset by scan)
+  int32_t* n_nonempty = nullptr;    // [8]: n_nonempty, (unused), barrier count, segment ticket, halo length
+                                    //      (1-4 reset by the scan)
   unsigned long long* scan_status = nullptr;  // [scan tiles]
   unsigned long long* scan_ticket = nullptr;  // [1] monotone ticket counter
   int64_t scan_tiles = 0;
@@ -58,7 +59,7 @@ struct PipelineBuffers {
   int* touched = nullptr;           // [total_blocks] list of touched blocks, then [count], [done]
   int* hmark = nullptr;             // [total_blocks] halo membership (fused, separate grid update; k_halo)
   int* halo = nullptr;              // [total_blocks] halo list
-  int* nhalo = nullptr;             // [1] its length
+  int* nhalo = nullptr;             // its length (= n_nonempty + 4)
   int* nsf_done = nullptr;          // reduced path: CTA completion counter of the G2P kernel
   bool rot = false;                 // fused pipeline with the in-kernel grid update (RotGrid)
   bool gub = false;                 // fused pipeline with the grid update at the end of k_g2p2g (barrier)
