@@ -335,6 +335,33 @@ __global__ void __launch_bounds__(128) k_copy_cells(int64_t n, const float* __re
   ids_out[dst] = id;
 }
 
+// deferred reorder: only the map of the new order, gmap[dst(j)] = j
+__global__ void __launch_bounds__(256) k_cell_map(int64_t n, const float* __restrict__ S,
+                                                  const int32_t* __restrict__ keys, const int32_t* __restrict__ ne_of,
+                                                  const int32_t* __restrict__ cellcnt, const int32_t* __restrict__ rank,
+                                                  int32_t* __restrict__ gmap, DevParams P) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const float* b = S + pbase(j);
+  const int cell = cell_of_x(b[(PX + 0) * 32], b[(PX + 1) * 32], b[(PX + 2) * 32], P);
+  const int64_t dst = cellcnt[64 * ne_of[keys[j]] + cell] + rank[j];
+  NSF_CHECK(dst >= 0 && dst < n);
+  gmap[dst] = (int32_t)j;
+}
+
+void launch_reorder_map(cudaStream_t st, const float* S, int64_t n, PipelineBuffers* pb, const DevParams& P) {
+  if (n == 0) return;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  launch_pdl(k_cell_rank, dim3(g), dim3(256), 0, st, n, S, (const int32_t*)pb->keys, (const int32_t*)pb->ne_of,
+             pb->cellcnt, pb->perm, P);
+  launch_pdl(k_cell_scan, dim3(num_sms() * 4), dim3(256), 0, st, pb->cellcnt, (const int32_t*)pb->nonempty,
+             (const int32_t*)pb->n_nonempty, (const int32_t*)pb->block_start);
+  launch_pdl(k_cell_map, dim3(g), dim3(256), 0, st, n, S, (const int32_t*)pb->keys, (const int32_t*)pb->ne_of,
+             (const int32_t*)pb->cellcnt, (const int32_t*)pb->perm, pb->gmap, P);
+}
+
 void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                                int32_t* ids_out, PipelineBuffers* pb, const DevParams& P) {
   if (n == 0) return;

@@ -210,7 +210,9 @@ struct TouchCtx {
   int* flags;
   int* list;
   int* list_count;
-  const int* hmark;   // HALO: halo membership per block
+  const int* hmark;   // HALO: per block, the epoch tag of the last halo list that held it
+  const unsigned long long* scan_ticket;   // HALO: the current tag = scan ticket / scan tiles
+  int64_t scan_tiles;
   int seg[3];         // HALO: the segment's block
   int64_t scene_block0;
 };
@@ -220,7 +222,8 @@ __device__ __forceinline__ void touch(const TouchCtx& t, int b0, int b1, int b2,
   if (HALO) {
     if (abs(b0 - t.seg[0]) <= 1 && abs(b1 - t.seg[1]) <= 1 && abs(b2 - t.seg[2]) <= 1) return;
     const int B = (int)(t.scene_block0 + block_id(b0, b1, b2, P));
-    if (t.hmark[B]) return;
+    if (t.hmark[B] == (int)(*(volatile const unsigned long long*)t.scan_ticket / (unsigned long long)t.scan_tiles))
+      return;   // in the current halo (an older tag: a block that left it)
     touch_block(t.flags, t.list, t.list_count, B, P);
     return;
   }
@@ -1211,12 +1214,23 @@ __device__ __forceinline__ void load_xF(const float* __restrict__ S, int j, floa
   for (int k = 0; k < 9; ++k) F[k] = ld_state(base + (PF + k) * 32);
 }
 
-template <bool DO_G2P, bool HS, bool ROT>
+// The substep after a periodic re-binning reorders the store on the way (no copy
+// pass): storage slot j of the new order is particle map[j] of the previous buffer
+// S, whose x, F (and tau_Y, id) are gathered from there; the substep writes its new
+// state to the new buffer in order.  S == nullptr: in place.
+template <bool GATH>
+__device__ __forceinline__ void load_xF_g(const float* __restrict__ S, const GatherIn& gi, int j, float x[3],
+                                          float F[9]) {
+  if (GATH) load_xF(gi.S, gi.map[j], x, F);
+  else load_xF(S, j, x, F);
+}
+
+template <bool DO_G2P, bool HS, bool ROT, bool GATH>
 __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const float xin[3], const float Fin[9],
                                                    const int o[3], const float4* vt, const float4* __restrict__ gvel,
                                                    const DevParams& P, DevErr* err, float xn[3], float vn[3],
                                                    float Cn[9], float tau[6], float y_plate,
-                                                   const int32_t* __restrict__ ids) {
+                                                   const int32_t* __restrict__ ids, const GatherIn& gi) {
   float* base = S + pbase(j);
       if (DO_G2P) {
     float x[3], F[9], G[9];
@@ -1261,7 +1275,7 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
     float FE[9];
     float J;
     if (HS) {   // per-particle yield stress (#30-#32)
-      float tY = base[PTY * 32];
+      float tY = GATH ? gi.S[pbase(gi.map[j]) + PTY * 32] : base[PTY * 32];
       J = vm_hs_update(Ft, P.mu, P.lam, P.vm_hard_k, P.vm_soft, tY, FE, tau);
       base[PTY * 32] = tY;
     } else {
@@ -1274,8 +1288,10 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 #pragma unroll
     for (int k = 0; k < 6; ++k) { st_state(base + (PT + k) * 32, tau[k]); chk += tau[k]; }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
-    if (!ok) { atomicOr(&err->bits, ERR_OUT_OF_DOMAIN); atomicMin(&err->first_index, ids[j]); }
-    if (!isfinite(chk)) { atomicOr(&err->bits, ERR_NONFINITE); atomicMin(&err->first_index, ids[j]); }
+    if (!ok || !isfinite(chk)) {
+      atomicOr(&err->bits, (ok ? 0u : (uint32_t)ERR_OUT_OF_DOMAIN) | (isfinite(chk) ? 0u : (uint32_t)ERR_NONFINITE));
+      atomicMin(&err->first_index, GATH ? gi.ids[gi.map[j]] : ids[j]);
+    }
   } else {
 #pragma unroll
     for (int a = 0; a < 3; ++a) { xn[a] = base[(PX + a) * 32]; vn[a] = base[(PV + a) * 32]; }
@@ -1344,12 +1360,13 @@ __device__ __forceinline__ void claim_segment(SM& sm, int32_t* counters, const i
 //   2  (GUB) at the end of this kernel, after a grid-wide barrier (every CTA of the
 //      persistent grid is resident): all CTAs update the touched blocks, so a substep
 //      is one launch and the next G2P reads `vel` directly.
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int GUM = 0>
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int GUM = 0, bool GATH = false>
 __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
-        int64_t* d_step, RotGrid rg, const int* __restrict__ hmark) {
+        int64_t* d_step, RotGrid rg, const int* __restrict__ hmark, GatherIn gi,
+        const unsigned long long* __restrict__ scan_ticket, int64_t scan_tiles) {
   constexpr bool ROT = GUM == 1, GUB = GUM == 2;
   constexpr bool HALO = GUM == 0;   // the grid-update pass visits the halo list (k_halo) + far-touched blocks
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1434,6 +1451,8 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     tc.list = list;
     tc.list_count = list_count;
     tc.hmark = hmark;
+    tc.scan_ticket = scan_ticket;
+    tc.scan_tiles = scan_tiles;
     tc.seg[0] = bc.b[0];
     tc.seg[1] = bc.b[1];
     tc.seg[2] = bc.b[2];
@@ -1462,7 +1481,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-      if (s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
+      if (s0 + tid < s1) load_xF_g<GATH>(S, gi, s0 + tid, x0, F0);
       // walls: skip the per-face tests when the tile lies inside [w, N - w) on every axis
       bool walls = false;
 #pragma unroll
@@ -1487,7 +1506,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    if (DO_G2P && !ROT && s0 + tid < s1) load_xF(S, s0 + tid, x0, F0);
+    if (DO_G2P && !ROT && s0 + tid < s1) load_xF_g<GATH>(S, gi, s0 + tid, x0, F0);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
 #if NSF_STATS
@@ -1500,11 +1519,17 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       // the next particle's x, F load under this one's G2P (needs the registers of
       // 2 CTAs per SM)
       float x1[3], F1[9];
-      if (DO_G2P && j + NT < s1) load_xF(S, j + NT, x1, F1);
+      if (DO_G2P && j + NT < s1) load_xF_g<GATH>(S, gi, j + NT, x1, F1);
 #else
-      if (DO_G2P && j != s0 + tid) load_xF(S, j, x0, F0);
+      if (DO_G2P && j != s0 + tid) load_xF_g<GATH>(S, gi, j, x0, F0);
 #endif
-      fused_g2p_particle<DO_G2P, HS, ROT>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau, y_plate, ids);
+      fused_g2p_particle<DO_G2P, HS, ROT, GATH>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau, y_plate, ids,
+                                                gi);
+      if (GATH) {   // the rest of the gathered particle: id, and tau_Y unless the update above wrote it
+        const int g = gi.map[j];
+        gi.ids_out[j] = gi.ids[g];
+        if (!HS) S[pbase(j) + PTY * 32] = gi.S[pbase(g) + PTY * 32];
+      }
 #if NSF_PF_NEXT
       if (DO_G2P && j + NT < s1) {
 #pragma unroll
@@ -1702,7 +1727,8 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
 // nothing reached hold m = 0 and get v = 0 (never gathered).
 __global__ void __launch_bounds__(128)
 k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* __restrict__ cnt2,
-                   const int* __restrict__ halo, const int* __restrict__ nhalo,
+                   const int* __restrict__ halo, const int* __restrict__ nhalo, const int* __restrict__ hmark,
+                   const unsigned long long* __restrict__ scan_ticket, int64_t scan_tiles,
                    float4* __restrict__ acc, float4* __restrict__ vel, DevParams P,
                    const int64_t* __restrict__ d_step, int32_t* __restrict__ counters) {
   // the step, both count slots and this warp's first halo entry are loaded
@@ -1732,6 +1758,12 @@ k_grid_update_list(int* __restrict__ flags, const int* __restrict__ list, int* _
     NSF_CHECK(key >= 0 && key < P.blocks_per_scene * P.n_scenes);
     const int en = e + nwarps;
     if (en < nl) key_next = en < nh ? halo[en] : list[en - nh];
+    // a far-touched block listed before a re-binning may be in the new halo: updated
+    // there once (a second update would read the cleared sums)
+    if (e >= nh && hmark[key] == (int)(*scan_ticket / (unsigned long long)scan_tiles)) {
+      if (lane == 0) flags[key] = 0;
+      continue;
+    }
     const int scene = key / bps;
     const BlockCoord bc = decode_block(key, P);
     const int64_t gb = (int64_t)scene * P.nodes_per_scene + (int64_t)(key - scene * bps) * kBlockNodes;
@@ -1894,13 +1926,13 @@ static bool pdl_enabled() {
   return f == 1;
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int ROT = 0>
-static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS, int ROT, bool GATH>
+static void launch_g2p2g_tg(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
   const size_t smem = sizeof(FusedSmemT<ROWS>);
   if (!attr) {
-    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
@@ -1914,9 +1946,20 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const 
   la[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT>, S, ids, vel, acc, pb->flags, pb->touched,
+  cudaLaunchKernelEx(&cfg, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH>, S, ids, vel, acc, pb->flags, pb->touched,
                      pb->touched + pb->total_blocks, pb->block_start, pb->nonempty, pb->n_nonempty, P, err, d_step,
-                     pb->rg, pb->hmark);
+                     pb->rg, pb->hmark, pb->gather, (const unsigned long long*)pb->scan_ticket, pb->scan_tiles);
+}
+
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int ROT = 0>
+static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
+                           const DevParams& P, DevErr* err, int64_t* d_step) {
+  // the substep after a deferred re-binning gathers (its own instantiation: the
+  // gather's registers must not reach the regular one)
+  if (DO_G2P && pb->gather.S)
+    launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, true>(st, S, ids, vel, acc, pb, P, err, d_step);
+  else
+    launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, false>(st, S, ids, vel, acc, pb, P, err, d_step);
 }
 
 template <int ROT>
@@ -1978,7 +2021,9 @@ void launch_grid_update_flags(cudaStream_t st, PipelineBuffers* pb, float4* acc,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k_grid_update_list, pb->flags, (const int*)pb->touched, pb->touched + pb->total_blocks,
-                     (const int*)pb->halo, (const int*)pb->nhalo, acc, vel, P, d_step, pb->n_nonempty);
+                     (const int*)pb->halo, (const int*)pb->nhalo, (const int*)pb->hmark,
+                     (const unsigned long long*)pb->scan_ticket, pb->scan_tiles, acc, vel, P, d_step,
+                     pb->n_nonempty);
 }
 
 void launch_reorder(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in, int32_t* ids_out,

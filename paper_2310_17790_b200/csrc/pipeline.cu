@@ -74,13 +74,16 @@ int pipeline_create(nsf_mpm* h, PipelineBuffers* pb, const DevParams& P, int64_t
 nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch) {
   if (pb->keys) pipeline_free(h, pb->keys);
   if (pb->perm) pipeline_free(h, pb->perm);
+  if (pb->gmap) pipeline_free(h, pb->gmap);
   if (pb->cellcnt) pipeline_free(h, pb->cellcnt);
   pb->cellcnt = nullptr;
 
   pb->keys = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
   pb->perm = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
+  pb->gmap = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * pitch);
   pb->pitch = pitch;
-  if (!pb->keys || !pb->perm) return NSF_ERR_OUT_OF_MEMORY;
+  pb->gather_pending = false;
+  if (!pb->keys || !pb->perm || !pb->gmap) return NSF_ERR_OUT_OF_MEMORY;
   if (reorder_mode() == 1) {   // a non-empty block holds >= 1 particle
     const int64_t max_nonempty = pitch < pb->total_blocks ? pitch : pb->total_blocks;
     pb->cellcnt = (int32_t*)pipeline_alloc(h, sizeof(int32_t) * 64 * (max_nonempty > 0 ? max_nonempty : 1));
@@ -100,7 +103,18 @@ static bool lpt_enabled() {
   return f == 1;
 }
 
-static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur);
+static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur, bool deferred);
+
+// periodic re-binnings of the fused pipeline leave the reorder to the next substep
+// (GatherIn); NSF_DEFERRED_REORDER=0 copies the store as the re-binning's last pass
+static bool deferred_reorder() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("NSF_DEFERRED_REORDER");
+    f = (e && e[0] == '0') ? 0 : 1;
+  }
+  return f == 1 && reorder_mode() == 1;
+}
 
 // longest-first only for dense scenes: in sparse ones (C4: 1237 vs 1296 us) the
 // spatial order of the non-empty list keeps neighbouring segments' grid lines in L2
@@ -118,18 +132,22 @@ static int rebin_launches(const PipelineBuffers* pb, int64_t n) {
 }
 
 // the fused kernel then processes its segments longest first (k_lpt_order)
-static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
-  const int nxt = enqueue_rebin_body(h, pb, v, cur);
+static int enqueue_rebin(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur, bool deferred = false) {
+  const int nxt = enqueue_rebin_body(h, pb, v, cur, deferred);
   if (lpt_active(pb) && v.n > 0) PLAUNCH(h, "bin_lpt", launch_lpt_order(v.stream, pb));
   if (halo_active(pb)) PLAUNCH(h, "bin_halo", launch_halo(v.stream, pb, *v.P));
   return nxt;
 }
 
-static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur) {
+static int enqueue_rebin_body(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v, int cur, bool deferred) {
   const int nxt = 1 - cur;
   PLAUNCH(h, "bin_keys_hist",
           launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P));
   PLAUNCH(h, "bin_scan", launch_scan(v.stream, pb));
+  if (deferred) {   // the map only; the store stays in buffer cur until the next substep
+    PLAUNCH(h, "reorder_map", launch_reorder_map(v.stream, v.S[cur], v.n, pb, *v.P));
+    return cur;
+  }
   if (reorder_mode() == 1) {
     PLAUNCH(h, "reorder",
             launch_reorder_cells_flat(v.stream, v.S[cur], v.S[nxt], v.n, v.ids[cur], v.ids[nxt], pb, *v.P));
@@ -234,6 +252,7 @@ nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb) {
       launch_gather_xref(v.stream, v.n, v.X, v.pitch, v.ids[0], v.S[0]);
   } else if (pb->fused) {
     pb->mode_ready = false;   // (the variant is chosen below; the segment order and halo follow)
+    pb->gather_pending = false;
     const int cur = enqueue_rebin(h, pb, v, 0);
     set_cur(h, cur);
     v = view(h);
@@ -324,14 +343,18 @@ static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v
   PLAUNCH(h, "bin_scatter", launch_scatter(v.stream, v.n, pb->keys, pb->cursor, pb->perm));
 }
 
+// bit 0: the substep ends with a re-binning; bit 1: it gathers through the
+// deferred reorder map of the previous one (its kernel's buffers differ)
 int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb) {
   (void)h;
-  return ((pb->fused || pb->nsf_sorted) && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
+  const int rebin = ((pb->fused || pb->nsf_sorted) && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
+  return rebin | ((pb->fused && pb->gather_pending) ? 2 : 0);
 }
 
 void pipeline_advance(nsf_mpm* h, PipelineBuffers* pb, int variant, int launches) {
   (void)h;
-  pb->since_rebin = variant ? 0 : pb->since_rebin + 1;
+  pb->since_rebin = (variant & 1) ? 0 : pb->since_rebin + 1;
+  pb->gather_pending = pb->fused && (variant & 1) && deferred_reorder();
   pb->launch_total += launches;
 }
 
@@ -366,11 +389,19 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
   if (pb->fused) {
     if (!pb->rot && !pb->gub)
       PLAUNCH(h, "grid_update", launch_grid_update_flags(v.stream, pb, v.acc, v.vel, *v.P, v.d_step));
-    PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[cur], v.ids[cur], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
-    launches = (pb->rot || pb->gub) ? 1 : 2;
     int next = cur;
-    if (variant) {
-      next = enqueue_rebin(h, pb, v, cur);
+    if (variant & 2) {   // reorder on the way: gather from buffer cur, write buffer 1 - cur in order
+      next = 1 - cur;
+      pb->gather.S = v.S[cur];
+      pb->gather.map = pb->gmap;
+      pb->gather.ids = v.ids[cur];
+      pb->gather.ids_out = v.ids[next];
+    }
+    PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[next], v.ids[next], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
+    pb->gather = GatherIn{};
+    launches = (pb->rot || pb->gub) ? 1 : 2;
+    if (variant & 1) {
+      next = enqueue_rebin(h, pb, v, next, deferred_reorder());
       launches += rebin_launches(pb, v.n);
     }
     pb->launches = launches;
@@ -462,6 +493,7 @@ int pipeline_debug_bins(nsf_mpm* h, PipelineBuffers* pb, int cur, int32_t* count
     // accumulator only depends on the state, which is unchanged)
     set_cur(h, enqueue_rebin(h, pb, v, cur));
     pb->since_rebin = 0;
+    pb->gather_pending = false;
   } else if (pb->tiled) {
     launch_keys_hist(v.stream, v.n, v.S[cur], v.pitch, v.scene_off, v.n_scenes, pb->keys, pb->counts, *v.P);
   }

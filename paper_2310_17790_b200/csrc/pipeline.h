@@ -29,6 +29,18 @@ struct RotGrid {
   int64_t total_blocks = 0;
 };
 
+// Deferred reorder (fused pipeline): a periodic re-binning computes only the map of
+// the new storage order (map[j] = the particle of the previous buffer that goes to
+// slot j); the next substep's k_g2p2g gathers x, F (tau_Y, id) through it and
+// writes its new state into the other buffer in order, so the store is reordered
+// without a copy pass.  S == nullptr: in place.
+struct GatherIn {
+  const float* S = nullptr;
+  const int32_t* map = nullptr;
+  const int32_t* ids = nullptr;
+  int32_t* ids_out = nullptr;
+};
+
 struct PipelineBuffers {
   // binning: block key per particle slot, per-block counts,
   // start offsets (exclusive scan), scatter cursors, permutation, active list
@@ -68,6 +80,9 @@ struct PipelineBuffers {
   float4* dbg_acc = nullptr;        // reduced path: scratch grids for debug_grid
   unsigned long long* fx = nullptr; // deterministic mode: fixed-point P2G accumulator [total_nodes][4]
   float4* dbg_vel = nullptr;
+  int32_t* gmap = nullptr;          // [pitch] deferred reorder map (fused)
+  bool gather_pending = false;      // the next fused substep gathers through gmap
+  GatherIn gather;                  // the gather of the k_g2p2g being enqueued
   int rebin_every = 32;             // fused pipeline: substeps between re-binnings
   int since_rebin = 0;              // host counter
   int64_t launch_total = 0;         // kernel launches enqueued since load
@@ -159,6 +174,7 @@ void launch_reorder_cells(cudaStream_t st, const float* Sin, float* Sout, int64_
                           int32_t* ids_out, const PipelineBuffers* pb, const DevParams& P);
 void launch_reorder_cells_flat(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,
                                int32_t* ids_out, PipelineBuffers* pb, const DevParams& P);
+void launch_reorder_map(cudaStream_t st, const float* S, int64_t n, PipelineBuffers* pb, const DevParams& P);
 int num_sms();
 int stats_read(cudaStream_t st, int64_t* out, int n);   // statistics build only (else 0)
 void launch_g2p_tiled(cudaStream_t st, const float* Sin, float* Sout, int64_t n, const int32_t* ids_in,

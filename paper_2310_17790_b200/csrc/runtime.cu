@@ -87,9 +87,12 @@ struct nsf_mpm {
   size_t staging_bytes = 0;
   // graphs: one captured substep per source buffer (the pipeline may ping-pong
   // particle buffers, so the substep starting from buffer k is graph[k])
-  cudaGraphExec_t graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [source buffer][variant]
-  int graph_next[2][2] = {{0, 0}, {1, 1}};
-  int graph_launches[2][2] = {{0, 0}, {0, 0}};   // kernels in each captured graph
+  // [source buffer][variant]; variant = pipeline_variant: bit 0 re-binning at the end,
+  // bit 1 the gather of a deferred reorder
+  static constexpr int kVariants = 4;
+  cudaGraphExec_t graph[2][kVariants] = {};
+  int graph_next[2][kVariants] = {{0, 0, 0, 0}, {1, 1, 1, 1}};
+  int graph_launches[2][kVariants] = {};   // kernels in each captured graph
   // profiling
   bool profiling = false;
   struct Pending { std::string name; cudaEvent_t a, b; };
@@ -198,7 +201,7 @@ nsf_status to_device(nsf_mpm* h, const void* src, size_t bytes, int on_device, v
 
 void invalidate_graph(nsf_mpm* h) {
   for (int k = 0; k < 2; ++k)
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < nsf_mpm::kVariants; ++v) {
       if (h->graph[k][v]) cudaGraphExecDestroy(h->graph[k][v]);
       h->graph[k][v] = nullptr;
     }
@@ -879,6 +882,7 @@ static nsf_status enqueue_substeps(nsf_mpm* h, int32_t n) {
   const bool use_graph = !h->profiling && pipeline_graphable(h, &h->pb);
   for (int i = 0; i < n; ++i) {
     const int variant = pipeline_variant(h, &h->pb);
+    if (variant < 0 || variant >= nsf_mpm::kVariants) return fail(h, NSF_ERR_CUDA, "substep variant out of range");
     if (!use_graph) {
       int next = pipeline_substep(h, &h->pb, h->cur, variant);
       if (next < 0) return fail(h, NSF_ERR_CUDA, "substep launch failed");
