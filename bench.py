@@ -380,6 +380,25 @@ def run_ours(args):
                     "peak_source": peak_src}
     step_gbs = B_ALG_PER_PARTICLE_SUBSTEP * n / (ms / args.steps * 1e-3) / 1e9
 
+    # ---- back-to-back regime (context, not the headline): ONE nsf_mpm_substep(K) call from the same
+    #      mid-run state -- no L2 flush between substeps (the store is re-read from L2 where it fits),
+    #      and the full-order kernel stores v, C, tau only in the call's last substep ----
+    kb = max(args.steps, 2 * REBIN_EVERY if REBIN_EVERY > 0 else 64)
+    sim.substep(kb)          # every graph variant of a multi-substep call instantiated
+    sim.sync()
+    barrier()
+    ba, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ba.record(stream)
+    sim.substep(kb)
+    bb.record(stream)
+    bb.synchronize()
+    b2b_ms = max_over_ranks(ba.elapsed_time(bb), world, dev)
+    b2b_gbs = B_ALG_PER_PARTICLE_SUBSTEP * n / (b2b_ms / kb * 1e-3) / 1e9
+    back_to_back = {"value": job_rate(world, n * kb, b2b_ms * 1e-3), "unit": "particle-substeps/s",
+                    "ms_per_step": b2b_ms / kb, "substeps": kb, "hbm_alg_frac_whole_step": b2b_gbs / peak,
+                    "note": "one nsf_mpm_substep(K) call, device-timed: no L2 flush between substeps; "
+                            "the periodic re-binning inside at its true rate"}
+
     # ---- C5: network inversion (Eq. (10)), 3 Gauss-Newton iterations over 64 samples per scene ----
     inversion = inference = integration = None
     if args.config == "C5":
@@ -502,6 +521,7 @@ def run_ours(args):
                                   "note": "state prepared outside the timed region: the scene is advanced to "
                                           "substep first_substep (pre-roll + warm-up + alignment), so the "
                                           "window holds the periodic re-binning at least at its true rate"}},
+            "back_to_back": back_to_back,
             "hbm_alg_gbs_whole_step": step_gbs,
             "hbm_alg_frac_whole_step": step_gbs / peak,
             "roofline": roof,

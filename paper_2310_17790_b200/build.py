@@ -18,8 +18,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libnsf_mpm.so")
+# NSF_BUILD_DIR / NSF_LIB_OUT: experiment variants built side by side (tools/ab_build.sh)
+BUILD = os.environ.get("NSF_BUILD_DIR") or os.path.join(PKG, "_build")
+LIB = os.environ.get("NSF_LIB_OUT") or os.path.join(PKG, "libnsf_mpm.so")
 LIB_CHECKED = os.path.join(PKG, "libnsf_mpm_checked.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

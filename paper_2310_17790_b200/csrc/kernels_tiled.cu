@@ -1230,7 +1230,7 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
                                                    const int o[3], const float4* vt, const float4* __restrict__ gvel,
                                                    const DevParams& P, DevErr* err, float xn[3], float vn[3],
                                                    float Cn[9], float tau[6], float y_plate,
-                                                   const int32_t* __restrict__ ids, const GatherIn& gi) {
+                                                   const int32_t* __restrict__ ids, const GatherIn& gi, bool wr) {
   float* base = S + pbase(j);
       if (DO_G2P) {
     float x[3], F[9], G[9];
@@ -1261,10 +1261,15 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       const float tt = xn[a] * P.inv_dx;
       ok &= !(tt < 0.5f || tt >= (float)P.N[a] - 1.5f);   // NaN: non-finite, not out of domain
       st_state(base + (PX + a) * 32, xn[a]);
-      st_state(base + (PV + a) * 32, vn[a]);
     }
+    // v, C (and tau below) only feed the P2G of this kernel: they are stored when the
+    // caller can read them, i.e. by the last substep of a nsf_mpm_substep(n) call
+    if (wr) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) st_state(base + (PC + k) * 32, Cn[k]);
+      for (int a = 0; a < 3; ++a) st_state(base + (PV + a) * 32, vn[a]);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) st_state(base + (PC + k) * 32, Cn[k]);
+    }
     float Ft[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -1286,7 +1291,11 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 #pragma unroll
     for (int k = 0; k < 9; ++k) { st_state(base + (PF + k) * 32, FE[k]); chk += FE[k]; }
 #pragma unroll
-    for (int k = 0; k < 6; ++k) { st_state(base + (PT + k) * 32, tau[k]); chk += tau[k]; }
+    for (int k = 0; k < 6; ++k) chk += tau[k];
+    if (wr) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) st_state(base + (PT + k) * 32, tau[k]);
+    }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
     if (!ok || !isfinite(chk)) {
       atomicOr(&err->bits, (ok ? 0u : (uint32_t)ERR_OUT_OF_DOMAIN) | (isfinite(chk) ? 0u : (uint32_t)ERR_NONFINITE));
@@ -1366,7 +1375,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
         int64_t* d_step, RotGrid rg, const int* __restrict__ hmark, GatherIn gi,
-        const unsigned long long* __restrict__ scan_ticket, int64_t scan_tiles) {
+        const unsigned long long* __restrict__ scan_ticket, int64_t scan_tiles, int wr_vct) {
   constexpr bool ROT = GUM == 1, GUB = GUM == 2;
   constexpr bool HALO = GUM == 0;   // the grid-update pass visits the halo list (k_halo) + far-touched blocks
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1524,7 +1533,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       if (DO_G2P && j != s0 + tid) load_xF_g<GATH>(S, gi, j, x0, F0);
 #endif
       fused_g2p_particle<DO_G2P, HS, ROT, GATH>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau, y_plate, ids,
-                                                gi);
+                                                gi, wr_vct != 0);
       if (GATH) {   // the rest of the gathered particle: id, and tau_Y unless the update above wrote it
         const int g = gi.map[j];
         gi.ids_out[j] = gi.ids[g];
@@ -1948,7 +1957,8 @@ static void launch_g2p2g_tg(cudaStream_t st, float* S, const int32_t* ids, const
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH>, S, ids, vel, acc, pb->flags, pb->touched,
                      pb->touched + pb->total_blocks, pb->block_start, pb->nonempty, pb->n_nonempty, P, err, d_step,
-                     pb->rg, pb->hmark, pb->gather, (const unsigned long long*)pb->scan_ticket, pb->scan_tiles);
+                     pb->rg, pb->hmark, pb->gather, (const unsigned long long*)pb->scan_ticket, pb->scan_tiles,
+                     pb->skip_vct ? 0 : 1);
 }
 
 template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int ROT = 0>

@@ -344,7 +344,9 @@ static void enqueue_binning(nsf_mpm* h, PipelineBuffers* pb, const HandleView& v
 }
 
 // bit 0: the substep ends with a re-binning; bit 1: it gathers through the
-// deferred reorder map of the previous one (its kernel's buffers differ)
+// deferred reorder map of the previous one (its kernel's buffers differ); bit 2
+// (added by the caller, runtime.cu enqueue_substeps): not the last substep of its
+// call, so the fused kernel keeps v, C, tau in registers only
 int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb) {
   (void)h;
   const int rebin = ((pb->fused || pb->nsf_sorted) && pb->since_rebin + 1 >= pb->rebin_every) ? 1 : 0;
@@ -397,7 +399,9 @@ int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant) {
       pb->gather.ids = v.ids[cur];
       pb->gather.ids_out = v.ids[next];
     }
+    pb->skip_vct = (variant & 4) != 0;
     PLAUNCH(h, "g2p2g", launch_g2p2g(v.stream, true, v.S[next], v.ids[next], v.vel, v.acc, pb, *v.P, v.err, v.d_step));
+    pb->skip_vct = false;
     pb->gather = GatherIn{};
     launches = (pb->rot || pb->gub) ? 1 : 2;
     if (variant & 1) {

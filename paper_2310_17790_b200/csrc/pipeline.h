@@ -82,6 +82,8 @@ struct PipelineBuffers {
   float4* dbg_vel = nullptr;
   int32_t* gmap = nullptr;          // [pitch] deferred reorder map (fused)
   bool gather_pending = false;      // the next fused substep gathers through gmap
+  bool skip_vct = false;            // set around a k_g2p2g launch: v, C, tau are not written back (a substep
+                                    // that is not the last of its nsf_mpm_substep(n) call: nothing can read them)
   GatherIn gather;                  // the gather of the k_g2p2g being enqueued
   int rebin_every = 32;             // fused pipeline: substeps between re-binnings
   int since_rebin = 0;              // host counter
@@ -127,6 +129,7 @@ nsf_status pipeline_particles(nsf_mpm* h, PipelineBuffers* pb, int64_t pitch);
 nsf_status pipeline_on_load(nsf_mpm* h, PipelineBuffers* pb);
 void pipeline_on_mlp(nsf_mpm* h, PipelineBuffers* pb);
 bool pipeline_graphable(nsf_mpm* h, PipelineBuffers* pb);
+inline bool pipeline_fused(const PipelineBuffers* pb) { return pb->fused; }   // k_g2p2g path (full-order, MLS)
 int pipeline_variant(nsf_mpm* h, PipelineBuffers* pb);             // graph variant of the next substep
 int pipeline_substep(nsf_mpm* h, PipelineBuffers* pb, int cur, int variant);   // returns next buffer or -1
 void pipeline_advance(nsf_mpm* h, PipelineBuffers* pb, int variant, int launches);          // host bookkeeping after one substep

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -88,10 +89,10 @@ struct nsf_mpm {
   // graphs: one captured substep per source buffer (the pipeline may ping-pong
   // particle buffers, so the substep starting from buffer k is graph[k])
   // [source buffer][variant]; variant = pipeline_variant: bit 0 re-binning at the end,
-  // bit 1 the gather of a deferred reorder
-  static constexpr int kVariants = 4;
+  // bit 1 the gather of a deferred reorder, bit 2 v, C, tau not stored (not the last substep of a call)
+  static constexpr int kVariants = 8;
   cudaGraphExec_t graph[2][kVariants] = {};
-  int graph_next[2][kVariants] = {{0, 0, 0, 0}, {1, 1, 1, 1}};
+  int graph_next[2][kVariants] = {{0, 0, 0, 0, 0, 0, 0, 0}, {1, 1, 1, 1, 1, 1, 1, 1}};
   int graph_launches[2][kVariants] = {};   // kernels in each captured graph
   // profiling
   bool profiling = false;
@@ -878,10 +879,18 @@ nsf_status nsf_mpm_set_latents(nsf_mpm* h, int32_t r, const float* z, const floa
   return NSF_OK;
 }
 
+// NSF_WRITE_EVERY=1: every substep stores v, C, tau (A/B; read per call, so a test runs both)
+static bool write_last_only() {
+  const char* e = getenv("NSF_WRITE_EVERY");
+  return !(e && e[0] == '1');
+}
+
 static nsf_status enqueue_substeps(nsf_mpm* h, int32_t n) {
-  const bool use_graph = !h->profiling && pipeline_graphable(h, &h->pb);
+  static const bool graph_env = [] { const char* e = getenv("NSF_GRAPH"); return !(e && e[0] == '0'); }();   // A/B
+  const bool use_graph = graph_env && !h->profiling && pipeline_graphable(h, &h->pb);
   for (int i = 0; i < n; ++i) {
-    const int variant = pipeline_variant(h, &h->pb);
+    // bit 2: a fused substep that is not the call's last does not store v, C, tau
+    const int variant = pipeline_variant(h, &h->pb) | ((i + 1 < n && pipeline_fused(&h->pb) && write_last_only()) ? 4 : 0);
     if (variant < 0 || variant >= nsf_mpm::kVariants) return fail(h, NSF_ERR_CUDA, "substep variant out of range");
     if (!use_graph) {
       int next = pipeline_substep(h, &h->pb, h->cur, variant);
