@@ -1225,12 +1225,12 @@ __device__ __forceinline__ void load_xF_g(const float* __restrict__ S, const Gat
   else load_xF(S, j, x, F);
 }
 
-template <bool DO_G2P, bool HS, bool ROT, bool GATH>
+template <bool DO_G2P, bool HS, bool ROT, bool GATH, bool WR>
 __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j, const float xin[3], const float Fin[9],
                                                    const int o[3], const float4* vt, const float4* __restrict__ gvel,
                                                    const DevParams& P, DevErr* err, float xn[3], float vn[3],
                                                    float Cn[9], float tau[6], float y_plate,
-                                                   const int32_t* __restrict__ ids, const GatherIn& gi, bool wr) {
+                                                   const int32_t* __restrict__ ids, const GatherIn& gi) {
   float* base = S + pbase(j);
       if (DO_G2P) {
     float x[3], F[9], G[9];
@@ -1261,15 +1261,13 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       const float tt = xn[a] * P.inv_dx;
       ok &= !(tt < 0.5f || tt >= (float)P.N[a] - 1.5f);   // NaN: non-finite, not out of domain
       st_state(base + (PX + a) * 32, xn[a]);
+      // v, C (and tau below) only feed the P2G of this kernel: they are stored when the
+      // caller can read them, i.e. by the last substep of a nsf_mpm_substep(n) call (WR)
+      if (WR) st_state(base + (PV + a) * 32, vn[a]);
     }
-    // v, C (and tau below) only feed the P2G of this kernel: they are stored when the
-    // caller can read them, i.e. by the last substep of a nsf_mpm_substep(n) call
-    if (wr) {
 #pragma unroll
-      for (int a = 0; a < 3; ++a) st_state(base + (PV + a) * 32, vn[a]);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) st_state(base + (PC + k) * 32, Cn[k]);
-    }
+    for (int k = 0; k < 9; ++k)
+      if (WR) st_state(base + (PC + k) * 32, Cn[k]);
     float Ft[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -1291,10 +1289,9 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
 #pragma unroll
     for (int k = 0; k < 9; ++k) { st_state(base + (PF + k) * 32, FE[k]); chk += FE[k]; }
 #pragma unroll
-    for (int k = 0; k < 6; ++k) chk += tau[k];
-    if (wr) {
-#pragma unroll
-      for (int k = 0; k < 6; ++k) st_state(base + (PT + k) * 32, tau[k]);
+    for (int k = 0; k < 6; ++k) {
+      if (WR) st_state(base + (PT + k) * 32, tau[k]);
+      chk += tau[k];
     }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
     if (!ok || !isfinite(chk)) {
@@ -1369,13 +1366,14 @@ __device__ __forceinline__ void claim_segment(SM& sm, int32_t* counters, const i
 //   2  (GUB) at the end of this kernel, after a grid-wide barrier (every CTA of the
 //      persistent grid is resident): all CTAs update the touched blocks, so a substep
 //      is one launch and the next G2P reads `vel` directly.
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int GUM = 0, bool GATH = false>
+// WR: v, C, tau are stored (false: a substep that is not the last of its call).
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int GUM = 0, bool GATH = false, bool WR = true>
 __global__ void __launch_bounds__(NT, MINB)
 k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __restrict__ vel, float4* __restrict__ acc, int* __restrict__ flags,
         int* __restrict__ list, int* __restrict__ list_count, const int32_t* __restrict__ block_start,
         const int32_t* __restrict__ nonempty, int32_t* __restrict__ counters, DevParams P, DevErr* err,
         int64_t* d_step, RotGrid rg, const int* __restrict__ hmark, GatherIn gi,
-        const unsigned long long* __restrict__ scan_ticket, int64_t scan_tiles, int wr_vct) {
+        const unsigned long long* __restrict__ scan_ticket, int64_t scan_tiles) {
   constexpr bool ROT = GUM == 1, GUB = GUM == 2;
   constexpr bool HALO = GUM == 0;   // the grid-update pass visits the halo list (k_halo) + far-touched blocks
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1532,8 +1530,8 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
 #else
       if (DO_G2P && j != s0 + tid) load_xF_g<GATH>(S, gi, j, x0, F0);
 #endif
-      fused_g2p_particle<DO_G2P, HS, ROT, GATH>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau, y_plate, ids,
-                                                gi, wr_vct != 0);
+      fused_g2p_particle<DO_G2P, HS, ROT, GATH, WR>(S, j, x0, F0, o, sm.vt, gvel, P, err, xn, vn, Cn, tau, y_plate,
+                                                    ids, gi);
       if (GATH) {   // the rest of the gathered particle: id, and tau_Y unless the update above wrote it
         const int g = gi.map[j];
         gi.ids_out[j] = gi.ids[g];
@@ -1935,13 +1933,13 @@ static bool pdl_enabled() {
   return f == 1;
 }
 
-template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS, int ROT, bool GATH>
+template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS, int ROT, bool GATH, bool WR>
 static void launch_g2p2g_tg(cudaStream_t st, float* S, const int32_t* ids, const float4* vel, float4* acc, PipelineBuffers* pb,
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   static bool attr = false;
   const size_t smem = sizeof(FusedSmemT<ROWS>);
   if (!attr) {
-    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
@@ -1955,10 +1953,9 @@ static void launch_g2p2g_tg(cudaStream_t st, float* S, const int32_t* ids, const
   la[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH>, S, ids, vel, acc, pb->flags, pb->touched,
+  cudaLaunchKernelEx(&cfg, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH, WR>, S, ids, vel, acc, pb->flags, pb->touched,
                      pb->touched + pb->total_blocks, pb->block_start, pb->nonempty, pb->n_nonempty, P, err, d_step,
-                     pb->rg, pb->hmark, pb->gather, (const unsigned long long*)pb->scan_ticket, pb->scan_tiles,
-                     pb->skip_vct ? 0 : 1);
+                     pb->rg, pb->hmark, pb->gather, (const unsigned long long*)pb->scan_ticket, pb->scan_tiles);
 }
 
 template <bool DO_G2P, int ROWS, int MINB, int NT, bool HS = false, int ROT = 0>
@@ -1966,10 +1963,15 @@ static void launch_g2p2g_t(cudaStream_t st, float* S, const int32_t* ids, const 
                            const DevParams& P, DevErr* err, int64_t* d_step) {
   // the substep after a deferred re-binning gathers (its own instantiation: the
   // gather's registers must not reach the regular one)
-  if (DO_G2P && pb->gather.S)
-    launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, true>(st, S, ids, vel, acc, pb, P, err, d_step);
-  else
-    launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, false>(st, S, ids, vel, acc, pb, P, err, d_step);
+  // (and one that keeps v, C, tau in registers: pb->skip_vct)
+  if (DO_G2P && pb->gather.S) {
+    if (pb->skip_vct) launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, true, false>(st, S, ids, vel, acc, pb, P, err, d_step);
+    else launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, true, true>(st, S, ids, vel, acc, pb, P, err, d_step);
+  } else if (DO_G2P && pb->skip_vct) {
+    launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, false, false>(st, S, ids, vel, acc, pb, P, err, d_step);
+  } else {
+    launch_g2p2g_tg<DO_G2P, ROWS, MINB, NT, HS, ROT, false, true>(st, S, ids, vel, acc, pb, P, err, d_step);
+  }
 }
 
 template <int ROT>

@@ -901,17 +901,22 @@ static nsf_status enqueue_substeps(nsf_mpm* h, int32_t n) {
       continue;
     }
     const int c = h->cur;
-    if (!h->graph[c][variant]) {
+    // a fused substep's graph is captured together with its sibling (stores v, C, tau /
+    // does not), so a long call also prepares the graphs of the single-substep calls
+    // that may follow it (and the reverse): no capture lands in a later timed region
+    for (int sib = 0; sib < (pipeline_fused(&h->pb) ? 2 : 1); ++sib) {
+      const int var = sib ? (variant ^ 4) : variant;
+      if (h->graph[c][var]) continue;
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-      int next = pipeline_substep(h, &h->pb, c, variant);
+      int next = pipeline_substep(h, &h->pb, c, var);
       cudaError_t ec = cudaStreamEndCapture(h->stream, &g);
       if (next < 0 || ec != cudaSuccess)
         return cuda_fail(h, ec == cudaSuccess ? cudaErrorUnknown : ec, "graph capture");
-      CK(cudaGraphInstantiate(&h->graph[c][variant], g, 0));
+      CK(cudaGraphInstantiate(&h->graph[c][var], g, 0));
       cudaGraphDestroy(g);
-      h->graph_next[c][variant] = next;
-      h->graph_launches[c][variant] = pipeline_launches_per_substep(h, &h->pb);
+      h->graph_next[c][var] = next;
+      h->graph_launches[c][var] = pipeline_launches_per_substep(h, &h->pb);
     }
     CK(cudaGraphLaunch(h->graph[c][variant], h->stream));
     h->cur = h->graph_next[c][variant];
