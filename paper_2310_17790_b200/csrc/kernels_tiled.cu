@@ -947,6 +947,7 @@ struct __align__(16) FusedSmemT {
   int next;                                    // the next segment: ticket, block key and storage range
   int nkey, ns0, ns1;                          //   (fetched by thread NT - 1 during phase 1)
   int nsc;                                     // entries of sc this segment
+  unsigned long long tbar;                     // mbarrier of the velocity tile's bulk copies (NSF_TILE_TMA)
 };
 static_assert(sizeof(FusedSmemT<kRowsF>) + 1024 <= 228 * 1024 / NSF_DENSE_MIN_BLOCKS, "fused kernel: CTAs per SM");
 static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPARSE_MIN_BLOCKS,
@@ -955,6 +956,50 @@ static_assert(sizeof(FusedSmemT<NSF_SPARSE_ROWS>) + 1024 <= 228 * 1024 / NSF_SPA
 __device__ __forceinline__ void cp_async16_f(void* smem, const void* gmem, int src_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(src_bytes) : "memory");
+}
+
+// Velocity tile by TMA bulk copies (cp.async.bulk, SASS UBLKCP; north star: "TMA-staged
+// grid tiles").  The grid is stored in 4x4x4-node blocks, so a tile row (fixed x, y; 8
+// nodes in z from 4 b_z - 1) is three contiguous runs: 1 node of block b_z - 1 (16 B),
+// 4 of block b_z (64 B), 3 of block b_z + 1 (48 B); 64 rows x 3 runs = 192 copies, one
+// per thread, straight into the padded tile layout, all completing on one mbarrier
+// (every thread arrives, the copying ones with their byte count).  Runs outside the
+// grid are zero-filled by their thread.
+// Measured (same-box A/B, -DNSF_TILE_TMA=1, parity-green): C3 103.0 vs 88.2 us per substep,
+// C2 37.9 vs 35.2, C4 1363 vs 1174 -- 192 requests of 16-64 bytes per tile cost the TMA
+// unit more than the 512 16-byte LDGSTS they replace (and the 96-register instantiation
+// spills 128 bytes with them), so the default stays cp.async; kept as an A/B option.
+#ifndef NSF_TILE_TMA
+#define NSF_TILE_TMA 0
+#endif
+__device__ __forceinline__ unsigned smem_addr_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tile_bar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// (the arrival's state token names the phase to wait for: no loop-carried parity register)
+__device__ __forceinline__ unsigned long long tile_bar_arrive(unsigned long long* bar, int tx_bytes) {
+  unsigned long long tok;
+  if (tx_bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                 : "=l"(tok) : "r"(smem_addr_u32(bar)), "r"(tx_bytes) : "memory");
+  else
+    asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];" : "=l"(tok) : "r"(smem_addr_u32(bar)) : "memory");
+  return tok;
+}
+__device__ __forceinline__ void tile_bar_wait(unsigned long long* bar, unsigned long long tok) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TILE_WAIT_%=:\n\t"
+      "mbarrier.try_wait.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TILE_WAIT_%=;\n\t}" ::"r"(smem_addr_u32(bar)), "l"(tok)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, int bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_addr_u32(bar))
+               : "memory");
 }
 
 #ifndef NSF_P2G_ROW_UNROLL
@@ -1434,6 +1479,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
   // segment tickets: the first here, each next one claimed (with its key and
   // range) during phase 1 of the current segment
   if (tid == 0) claim_segment(sm, counters, nonempty, block_start, nblk);
+  if (DO_G2P && NSF_FUSED_VTILE && NSF_TILE_TMA && !ROT && tid == 0) tile_bar_init(&sm.tbar, NT);   // (barrier at the loop top)
 #if NSF_STATS
   long long t_mark = clock64();
 #endif
@@ -1471,6 +1517,7 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
     const int o[3] = {4 * bc.b[0] - 1, 4 * bc.b[1] - 1, 4 * bc.b[2] - 1};   // tile origin (grid node)
 
     float x0[3], F0[9];   // the first particle's x, F: loaded under the tile copy
+    unsigned long long ttok = 0;
     if (DO_G2P && NSF_FUSED_VTILE && ROT) {
       // raw P2G sums of the tile's nodes (L2-resident: reduced by the previous
       // kernel) copied asynchronously; after the wait each thread updates the
@@ -1504,6 +1551,28 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
           *t = grid_node_update_rcp(*t, i, jn, k, P, y_plate, walls);
         }
       }
+    } else if (DO_G2P && NSF_FUSED_VTILE && NSF_TILE_TMA) {
+      int tx = 0;
+      if (tid < 192) {
+        const int r = tid / 3, pc = tid - 3 * r;            // tile row (x, y), run in z
+        const int ti = r >> 3, tj = r & 7;
+        const int k0 = pc == 0 ? 0 : (pc == 1 ? 1 : 5), nk = pc == 0 ? 1 : (pc == 1 ? 4 : 3);
+        const int i = o[0] + ti, jn = o[1] + tj, k = o[2] + k0;
+        float4* dst = &sm.vt[ti * kVTx + tj * kVTy + k0];
+        if (i >= 0 && jn >= 0 && k >= 0 && i < P.N[0] && jn < P.N[1] && k < P.N[2]) {
+          tx = 16 * nk;
+          // (the tile's readers of the previous segment passed two barriers; order them,
+          // and any zero fill, before the async-proxy writes)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          ttok = tile_bar_arrive(&sm.tbar, tx);
+          bulk_g2s(dst, gvel + node_index(i, jn, k, P), tx, &sm.tbar);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nk) dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (tx == 0) ttok = tile_bar_arrive(&sm.tbar, 0);
     } else if (DO_G2P && NSF_FUSED_VTILE) {
       for (int e = tid; e < kVT * kVT * kVT; e += NT) {
         const int i = o[0] + (e >> 6), jn = o[1] + ((e >> 3) & 7), k = o[2] + (e & 7);
@@ -1514,8 +1583,14 @@ k_g2p2g(float* __restrict__ S, const int32_t* __restrict__ ids, const float4* __
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     if (DO_G2P && !ROT && s0 + tid < s1) load_xF_g<GATH>(S, gi, s0 + tid, x0, F0);
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
+    if (DO_G2P && NSF_FUSED_VTILE && NSF_TILE_TMA && !ROT) {
+      // every thread arrived after its stores above (pop, nsc, zero fill): the phase
+      // completes when all have and the copies' bytes landed -- also the CTA barrier
+      tile_bar_wait(&sm.tbar, ttok);
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();
+    }
 #if NSF_STATS
     if (tid == 0) { const long long t = clock64(); NSF_STAT_ADD(kStCycTile, t - t_mark); t_mark = t; }
 #endif
