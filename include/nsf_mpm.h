@@ -295,7 +295,12 @@ nsf_status nsf_mpm_rom_step(nsf_mpm* h, int64_t n_ref, const float* X_all, int32
 
 /* Enqueue n >= 0 substeps on the handle's stream (a cached CUDA graph of the
  * substep is replayed).  Asynchronous.  NSF_ERR_BAD_STATE before
- * load_particles, or for NSF without load_stress_field / set_latents. */
+ * load_particles, or for NSF without load_stress_field / set_latents.
+ * The state every other call sees is that after the n-th substep.  On the
+ * full-order MLS path, where G2P and the next P2G are one
+ * kernel, v_p, C_p and tau_p of the first n - 1 substeps only feed that P2G and
+ * stay in registers; the n-th substep stores them (x_p and F_E are stored by
+ * every substep), so one call of n substeps moves less memory than n calls. */
 nsf_status nsf_mpm_substep(nsf_mpm* h, int32_t n);
 
 /* Evaluate tau = sigma_tau h(X, z) at m points (m x 3) for one latent z (r
