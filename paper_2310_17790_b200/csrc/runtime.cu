@@ -894,7 +894,10 @@ static nsf_status enqueue_substeps(nsf_mpm* h, int32_t n) {
     if (variant < 0 || variant >= nsf_mpm::kVariants) return fail(h, NSF_ERR_CUDA, "substep variant out of range");
     if (!use_graph) {
       int next = pipeline_substep(h, &h->pb, h->cur, variant);
-      if (next < 0) return fail(h, NSF_ERR_CUDA, "substep launch failed");
+      if (next < 0) {
+        h->poisoned = true;   // (earlier substeps of this call may not have stored v, C, tau)
+        return fail(h, NSF_ERR_CUDA, "substep launch failed");
+      }
       CK(cudaGetLastError());
       h->cur = next;
       pipeline_advance(h, &h->pb, variant, pipeline_launches_per_substep(h, &h->pb));
