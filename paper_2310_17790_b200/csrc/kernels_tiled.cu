@@ -19,6 +19,7 @@
 //              (sort-on-write), with its next block key and the histogram for
 //              the next binning.
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <cstdlib>
 #include <cstdint>
 #include "mpm_math.cuh"
@@ -2016,6 +2017,12 @@ static void launch_g2p2g_tg(cudaStream_t st, float* S, const int32_t* ids, const
   if (!attr) {
     cudaFuncSetAttribute(k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH, WR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    // the persistent grid is one wave of MINB CTAs per SM (the barrier mode relies on it).
+    // (Measured: a register cap above 96 for 3 x 192 threads -- __maxnreg__(104 / 112) --
+    // leaves 2 CTAs per SM: C3 102.7 / 104.6 vs 88.5 us.)
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_g2p2g<DO_G2P, ROWS, MINB, NT, HS, ROT, GATH, WR>, NT, smem);
+    if (nb < MINB) fprintf(stderr, "nsf_mpm: k_g2p2g<%d x %d> fits %d CTAs per SM, %d wanted\n", NT, MINB, nb, MINB);
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
