@@ -1252,6 +1252,22 @@ __device__ __forceinline__ void st_state(float* p, float v) {
   *p = v;
 #endif
 }
+// v, C, tau: written for the caller, never read back by the substep loop, so their
+// lines are stored evict-first and leave the L2 to x, F and the grid (same-box A/B on C3:
+// flushed 87.9 -> 87.4 us, single-substep calls back to back 84.3 -> 81.8; st.global.wt
+// and evict-first on every state access: no gain)
+#ifndef NSF_OUT_HINT
+#define NSF_OUT_HINT 1   // 0: default policy, 1: st.global.cs (evict first), 2: st.global.wt
+#endif
+__device__ __forceinline__ void st_out(float* p, float v) {
+#if NSF_OUT_HINT == 1
+  __stcs(p, v);
+#elif NSF_OUT_HINT == 2
+  __stwt(p, v);
+#else
+  st_state(p, v);
+#endif
+}
 __device__ __forceinline__ void load_xF(const float* __restrict__ S, int j, float x[3], float F[9]) {
   const float* base = S + pbase(j);
 #pragma unroll
@@ -1309,11 +1325,11 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
       st_state(base + (PX + a) * 32, xn[a]);
       // v, C (and tau below) only feed the P2G of this kernel: they are stored when the
       // caller can read them, i.e. by the last substep of a nsf_mpm_substep(n) call (WR)
-      if (WR) st_state(base + (PV + a) * 32, vn[a]);
+      if (WR) st_out(base + (PV + a) * 32, vn[a]);
     }
 #pragma unroll
     for (int k = 0; k < 9; ++k)
-      if (WR) st_state(base + (PC + k) * 32, Cn[k]);
+      if (WR) st_out(base + (PC + k) * 32, Cn[k]);
     float Ft[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -1336,7 +1352,7 @@ __device__ __forceinline__ void fused_g2p_particle(float* __restrict__ S, int j,
     for (int k = 0; k < 9; ++k) { st_state(base + (PF + k) * 32, FE[k]); chk += FE[k]; }
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-      if (WR) st_state(base + (PT + k) * 32, tau[k]);
+      if (WR) st_out(base + (PT + k) * 32, tau[k]);
       chk += tau[k];
     }
     if (!(J > 0.0f)) atomicAdd(&err->inverted, 1ull);
